@@ -1,0 +1,212 @@
+/* cpddg -- B200-native (sm_100a, FP64) solve path for the closest-point
+ * surface Helmholtz discretisation with RAS / ORAS Schwarz methods.
+ *
+ * The C ABI that a reference ("cpdd", proj/include/cpdd/) caller binds to in
+ * place of its own hot path.  Plain pointers and sizes only; no exceptions
+ * cross it.  Every entry point cites the reference interface it replaces.
+ *
+ * Status codes map 1:1 to the reference exception hierarchy
+ * (proj/include/cpdd/core.hpp:73-95) and thus to the CLI exit codes of
+ * proj/tools/cpm.cpp:181-193:
+ *   0 ok, 1 InternalError, 2 ConfigError, 3 DivergenceError (singular local
+ *   factorisation, non-finite residual, divergence), 4 IoError, 5 CUDA error.
+ * cpddg_last_error() returns the message of the calling thread's last failure.
+ *
+ * Memory: arguments named *_dev are device pointers (FP64, length n);
+ * `stream` is a cudaStream_t (NULL = legacy default stream).  Handles own
+ * their device buffers and are released by the matching *_destroy.  Calls on
+ * one handle must be serialised by the caller (the reference's const apply()
+ * is likewise not re-entrant across pools, proj/include/cpdd/solve.hpp:62-86).
+ */
+#ifndef CPDDG_H
+#define CPDDG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    CPDDG_OK = 0,
+    CPDDG_ERR_INTERNAL = 1,
+    CPDDG_ERR_CONFIG = 2,
+    CPDDG_ERR_DIVERGENCE = 3,
+    CPDDG_ERR_IO = 4,
+    CPDDG_ERR_CUDA = 5
+};
+
+/** Copy the calling thread's last error message into buf; returns its code. */
+int cpddg_last_error(char* buf, size_t len);
+const char* cpddg_version(void);
+
+/* ======================================================================
+ * Host setup.  Mirrors build_problem (proj/include/cpdd/pipeline.hpp:155-168)
+ * and the setup half of run_solve (pipeline.hpp:186-216): band, E, A,
+ * partition alignment, subdomains, local systems.  Bit-exact with the
+ * reference (index sets, orderings, and the bits of every matrix entry).
+ * ==================================================================== */
+typedef struct cpddg_setup cpddg_setup;
+
+enum { CPDDG_CIRCLE = 0, CPDDG_SPHERE = 1, CPDDG_TORUS = 2, CPDDG_TRIMESH = 3 };
+
+typedef struct {
+    int dim;              /* 2 (circle) or 3 */
+    int surface;          /* CPDDG_CIRCLE ... CPDDG_TRIMESH (RunConfig::surface, config.hpp:21) */
+    double radius;        /* circle / sphere (config.hpp:22) */
+    double major_radius;  /* torus (config.hpp:25-26) */
+    double minor_radius;
+    const char* obj_path; /* trimesh: Wavefront OBJ (geometry.hpp:137-170) */
+    double h;             /* lattice spacing (config.hpp:32) */
+    int p;                /* interpolation degree (config.hpp:33) */
+    double tube_radius;   /* <= 0: reference (p+1)/2 sqrt(d) h (interp.hpp:95-98) */
+    double c;             /* Helmholtz shift (SolverConfig::c, solve.hpp:31) */
+    int workers;          /* host threads for setup; 0 = all */
+} cpddg_problem_desc;
+
+/** build_band_tube + build_extension + assemble_helmholtz
+ *  (band.hpp:150-182, operators.hpp:30-51, 96-112). */
+int cpddg_setup_create(const cpddg_problem_desc* desc, cpddg_setup** out);
+int cpddg_setup_destroy(cpddg_setup* s);
+/** n_active, n_ghost, nnz(E), nnz(A). */
+int cpddg_setup_sizes(const cpddg_setup* s, int* n_active, int* n_ghost, int64_t* nnz_E,
+                      int64_t* nnz_A);
+/** Band nodes in band-code order (BandGrid::active then ::ghost,
+ *  band.hpp:36-60): lattice index (N_B x dim), cp, normal (N_B x dim), dist. */
+int cpddg_setup_band(const cpddg_setup* s, int32_t* ix, double* cp, double* normal, double* dist);
+/** CSR of E (which = 0) or A (which = 1) (SparseOperator, sparse.hpp:19-103). */
+int cpddg_setup_csr(const cpddg_setup* s, int which, int64_t* row_ptr, int32_t* col, double* val);
+
+enum { CPDDG_RAS = 0, CPDDG_ORAS = 1 };
+
+/** Partition (validated as load_partition, partition.hpp:519-552), then
+ *  align_interfaces (partition.hpp:474-508), build_subdomains
+ *  (subdomain.hpp:153-313) and assemble_local for every subdomain
+ *  (transmission.hpp:73-138, factor = false).  alpha_cross < 0 means alpha
+ *  (SolverConfig::effective_alpha_cross, solve.hpp:38).  part_out (may be
+ *  NULL) receives the aligned labels, moves the alignment move count. */
+int cpddg_setup_decompose(cpddg_setup* s, const int32_t* part, int n_overlap, int method,
+                          double alpha, double alpha_cross, int32_t* part_out, int* moves);
+int cpddg_setup_n_subdomains(const cpddg_setup* s);
+/** counts[8] = |disjoint|, |overlap|, |final_layer|, |ghosts|, |bc|,
+ *  fallback_count, n_lambda, #cross_flagged (Subdomain, subdomain.hpp:47-56). */
+int cpddg_setup_subdomain_counts(const cpddg_setup* s, int j, int32_t* counts);
+/** bc_int: |bc| x (dim+4) = ix..., global_active, is_ghost_type,
+ *  cross_flagged, fallback; bc_real: |bc| x (4 dim + 1) = x, cp, cp_local,
+ *  conormal, dq (BoundaryNode, subdomain.hpp:30-44). */
+int cpddg_setup_subdomain_sets(const cpddg_setup* s, int j, int32_t* disjoint, int32_t* overlap,
+                               int32_t* final_layer, int32_t* ghosts, int32_t* bc_int,
+                               double* bc_real);
+/** sizes[4] = n_overlap, n_bc, nnz, |scatter| (LocalOperator,
+ *  transmission.hpp:47-70). */
+int cpddg_setup_local_sizes(const cpddg_setup* s, int j, int64_t* sizes);
+int cpddg_setup_local(const cpddg_setup* s, int j, int64_t* row_ptr, int32_t* col, double* val,
+                      int32_t* scatter_local, int32_t* scatter_global);
+
+/* ======================================================================
+ * Device operator.  Replaces Eigen::VectorXd SparseOperator::apply(x) on the
+ * assembled Helmholtz matrix A (sparse.hpp:65-75, A from operators.hpp:96-112)
+ * with the matrix-free form y = (c + 2d/h^2) x - h^-2 sum_{2d nbrs} (E x).
+ * ==================================================================== */
+typedef struct cpddg_op cpddg_op;
+
+typedef struct {
+    int dim, p;
+    int n_active, n_ghost;
+    double h, c;
+    const int32_t* ix; /* (n_active + n_ghost) x dim lattice indices, band-code order */
+    const double* cp;  /* (n_active + n_ghost) x dim closest points */
+} cpddg_band_desc;
+
+int cpddg_op_create(const cpddg_band_desc* band, cpddg_op** out);
+int cpddg_op_create_from_setup(const cpddg_setup* s, cpddg_op** out);
+/** y_dev = A x_dev (sizes n_active). */
+int cpddg_op_apply(cpddg_op* op, const double* x_dev, double* y_dev, void* stream);
+/** r_dev = b_dev - A x_dev, and ||r||_2 into *rnorm (host, synchronises). */
+int cpddg_op_residual(cpddg_op* op, const double* b_dev, const double* x_dev, double* r_dev,
+                      double* rnorm, void* stream);
+int cpddg_op_size(const cpddg_op* op);
+/** Bytes one apply must move at minimum (SURVEY.md 8(d) B_op) and the bytes
+ *  the kernels stream (index tables included). */
+int cpddg_op_bytes(const cpddg_op* op, int64_t* algorithmic, int64_t* streamed);
+int cpddg_op_destroy(cpddg_op* op);
+
+/* ======================================================================
+ * Device Schwarz preconditioner.  Replaces the factored LocalOperator
+ * vector (assemble_local(..., factor = true), transmission.hpp:73-138;
+ * DirectSolver::factor, direct.hpp:41-52) and
+ * SchwarzPreconditioner::apply (solve.hpp:64-86): z = sum_j Rt_j^T A_j^-1 R_j r.
+ * ==================================================================== */
+typedef struct cpddg_pc cpddg_pc;
+
+typedef struct {
+    int n_overlap, n_bc;
+    const int32_t* overlap;        /* n_overlap global ordinals (LocalOperator::overlap) */
+    int n_scatter;
+    const int32_t* scatter_local;  /* LocalOperator::scatter .first  */
+    const int32_t* scatter_global; /* LocalOperator::scatter .second */
+    const int64_t* row_ptr;        /* n_local + 1 (SparseOperator::row_ptr) */
+    const int32_t* col;
+    const double* val;
+} cpddg_local_desc;
+
+typedef struct {
+    int workers;        /* host threads for ordering / symbolic analysis; 0 = all */
+    int check_residual; /* 1: verify every local factor on a probe vector */
+} cpddg_pc_options;
+
+typedef struct {
+    int n_sub;
+    int n_reduced;              /* subdomains whose Dirichlet closure block was eliminated */
+    int64_t n_rows_total;       /* sum of factored system sizes */
+    int64_t factor_entries;     /* stored L + U + diag entries */
+    int64_t factor_bytes;       /* bytes the triangular solves stream per apply */
+    int64_t algorithmic_bytes;  /* B_pc of SURVEY.md 8(d) */
+    int max_rows;
+    double factor_seconds;      /* device factorisation time */
+    double analyse_seconds;     /* host ordering + symbolic time */
+    double max_probe_residual;  /* when check_residual */
+} cpddg_pc_stats;
+
+int cpddg_pc_create(int n_global, int n_sub, const cpddg_local_desc* locals,
+                    const cpddg_pc_options* opt, cpddg_pc** out);
+int cpddg_pc_create_from_setup(const cpddg_setup* s, const cpddg_pc_options* opt, cpddg_pc** out);
+/** z_dev = M r_dev (sizes n_global). */
+int cpddg_pc_apply(cpddg_pc* pc, const double* r_dev, double* z_dev, void* stream);
+int cpddg_pc_stats_get(const cpddg_pc* pc, cpddg_pc_stats* st);
+int cpddg_pc_destroy(cpddg_pc* pc);
+
+/* ======================================================================
+ * Solvers.  Replace stationary_solve and gmres_solve (solve.hpp:95-214);
+ * the log mirrors IterationLog (solve.hpp:49-55): residuals start with the
+ * initial residual, iterations = preconditioner applications counted as
+ * the reference counts them, final_true_residual = ||b - A u|| at exit.
+ * ==================================================================== */
+typedef struct {
+    double rel_tol;
+    int max_iter;
+    int restart; /* gmres: 0 = no restart (cycle = max_iter) */
+} cpddg_solve_params;
+
+typedef struct {
+    double* residuals;   /* caller buffer of `capacity` entries (may be NULL) */
+    int capacity;
+    int n_residuals;     /* entries produced (may exceed capacity) */
+    int iterations;
+    int converged;
+    double final_true_residual;
+    double seconds;      /* device-timed solve loop (CUDA events) */
+    int64_t kernel_launches;
+} cpddg_log;
+
+int cpddg_gmres(cpddg_op* op, cpddg_pc* pc, const double* b_dev, double* u_dev,
+                const cpddg_solve_params* prm, cpddg_log* log, void* stream);
+int cpddg_stationary(cpddg_op* op, cpddg_pc* pc, const double* b_dev, double* u_dev,
+                     const cpddg_solve_params* prm, cpddg_log* log, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CPDDG_H */
