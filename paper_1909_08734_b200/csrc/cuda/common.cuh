@@ -1,0 +1,114 @@
+// Shared device plumbing: error checks, owning device buffers, and
+// deterministic (fixed-order) block reductions.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace cpddg {
+
+inline void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw std::runtime_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+#define CPDDG_CUDA(call) ::cpddg::cuda_check((call), #call)
+
+/** Owning device allocation. */
+template <class T>
+class DevBuf {
+public:
+    DevBuf() = default;
+    explicit DevBuf(std::size_t n) { alloc(n); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_) {
+        o.p_ = nullptr;
+        o.n_ = 0;
+    }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) {
+            release();
+            p_ = o.p_;
+            n_ = o.n_;
+            o.p_ = nullptr;
+            o.n_ = 0;
+        }
+        return *this;
+    }
+    ~DevBuf() { release(); }
+    void alloc(std::size_t n) {
+        release();
+        if (n) CPDDG_CUDA(cudaMalloc(&p_, n * sizeof(T)));
+        n_ = n;
+    }
+    void upload(const std::vector<T>& h) {
+        alloc(h.size());
+        if (!h.empty()) CPDDG_CUDA(cudaMemcpy(p_, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+    }
+    void upload(const T* h, std::size_t n) {
+        alloc(n);
+        if (n) CPDDG_CUDA(cudaMemcpy(p_, h, n * sizeof(T), cudaMemcpyHostToDevice));
+    }
+    void zero(cudaStream_t s = nullptr) {
+        if (n_) CPDDG_CUDA(cudaMemsetAsync(p_, 0, n_ * sizeof(T), s));
+    }
+    T* get() const { return p_; }
+    std::size_t size() const { return n_; }
+    std::size_t bytes() const { return n_ * sizeof(T); }
+
+private:
+    void release() {
+        if (p_) cudaFree(p_);
+        p_ = nullptr;
+        n_ = 0;
+    }
+    T* p_ = nullptr;
+    std::size_t n_ = 0;
+};
+
+/** Number of SMs of the current device (148 on B200). */
+int sm_count();
+
+/** Grid size used by every reduction kernel: a fixed multiple of the SM
+ *  count, so partial sums (and hence results) do not depend on the launch
+ *  history. */
+int reduction_blocks();
+
+constexpr int kRedThreads = 256;
+
+// Fixed-order block sum: warp shuffles (xor tree) then warp 0 over the 8
+// warp partials.  Deterministic for a fixed blockDim.
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+    v = warp_sum(v);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (w == 0) {
+        r = l < NT / 32 ? sh[l] : 0.0;
+        r = warp_sum(r);
+    }
+    __syncthreads();
+    return r;  // valid in thread 0
+}
+
+/** Device scalar slots used by the Krylov kernels. */
+struct ReduceWork {
+    DevBuf<double> partials;      // reduction_blocks() entries per slot
+    DevBuf<unsigned int> counter; // last-block-done tickets
+    void ensure(int slots);
+    int slots = 0;
+};
+
+}  // namespace cpddg

@@ -1,0 +1,366 @@
+// Device-resident Krylov drivers: restarted right-preconditioned GMRES with
+// modified Gram-Schmidt (solve.hpp:128-214) and the stationary Schwarz
+// iteration (solve.hpp:95-123).
+//
+// All vectors (basis V, w, r, u) live in HBM; the host keeps only the
+// (m+2)-entry Hessenberg column, the Givens rotations and the residual
+// history -- the reference's own scalar arithmetic, in the same order, so
+// the rotated estimates follow the reference step for step.  Each MGS step
+// is one fused streaming pass `w -= h_{i-1} V_{i-1}; h_i = V_i . w`
+// (deterministic two-level reduction, last-block-done), the norm of the
+// operator image rides on the first pass, and the correction
+// u += M^-1 (V y) scatters straight into u (owned slots are disjoint).
+#include "../host/setup.hpp"
+#include "common.cuh"
+#include "op.cuh"
+
+#include <cmath>
+#include <vector>
+
+namespace cpddg {
+
+namespace {
+
+/** One MGS pass over w.  If vprev: w -= (*hprev) * vprev.  Then
+ *  out[0] = vnext . w (or w . w when vnext == nullptr); if out2:
+ *  out2[0] = w . w as well.  Deterministic: fixed grid, fixed-order sums. */
+__global__ void __launch_bounds__(kRedThreads) k_mgs(int n, const double* __restrict__ hprev,
+                                                     const double* __restrict__ vprev, double* __restrict__ w,
+                                                     const double* __restrict__ vnext, double* partials,
+                                                     unsigned int* counter, double* out, double* out2) {
+    const double h = vprev ? *hprev : 0.0;
+    double a1 = 0.0, a2 = 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        double wi = w[i];
+        if (vprev) {
+            wi -= h * __ldg(vprev + i);
+            w[i] = wi;
+        }
+        a1 = fma(vnext ? __ldg(vnext + i) : wi, wi, a1);
+        if (out2) a2 = fma(wi, wi, a2);
+    }
+    __shared__ double sh[kRedThreads / 32];
+    __shared__ bool last;
+    const double b1 = block_sum<kRedThreads>(a1, sh);
+    const double b2 = out2 ? block_sum<kRedThreads>(a2, sh) : 0.0;
+    if (threadIdx.x == 0) {
+        partials[blockIdx.x] = b1;
+        partials[gridDim.x + blockIdx.x] = b2;
+        __threadfence();
+        last = atomicInc(counter, gridDim.x - 1) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last) {
+        __threadfence();
+        double s1 = 0.0, s2 = 0.0;
+        for (int q = threadIdx.x; q < static_cast<int>(gridDim.x); q += blockDim.x) {
+            s1 += static_cast<volatile double*>(partials)[q];
+            s2 += static_cast<volatile double*>(partials)[gridDim.x + q];
+        }
+        const double t1 = block_sum<kRedThreads>(s1, sh);
+        const double t2 = out2 ? block_sum<kRedThreads>(s2, sh) : 0.0;
+        if (threadIdx.x == 0) {
+            *out = t1;
+            if (out2) *out2 = t2;
+        }
+    }
+}
+
+__global__ void k_scale(int n, const double* __restrict__ src, double s, double* __restrict__ dst) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = src[i] / s;
+}
+
+/** out = sum_k y[k] V_k  (V_k at vbase[k]). */
+__global__ void k_combine(int n, int m, const double* const* __restrict__ vptr, const double* __restrict__ y,
+                          double* __restrict__ out) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int k = 0; k < m; ++k) s = fma(y[k], __ldg(vptr[k] + i), s);
+        out[i] = s;
+    }
+}
+
+__global__ void k_axpy1(int n, const double* __restrict__ x, double* __restrict__ y) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) y[i] += x[i];
+}
+
+void check_finite(double v, const char* what) {
+    if (!std::isfinite(v)) throw DivergenceError(std::string(what) + " is not finite");
+}
+
+struct Pinned {
+    double* p = nullptr;
+    explicit Pinned(std::size_t n) { CPDDG_CUDA(cudaMallocHost(&p, n * sizeof(double))); }
+    ~Pinned() {
+        if (p) cudaFreeHost(p);
+    }
+};
+
+struct Timer {
+    cudaEvent_t a, b;
+    cudaStream_t s;
+    explicit Timer(cudaStream_t st) : s(st) {
+        CPDDG_CUDA(cudaEventCreate(&a));
+        CPDDG_CUDA(cudaEventCreate(&b));
+        CPDDG_CUDA(cudaEventRecord(a, s));
+    }
+    double stop() {
+        CPDDG_CUDA(cudaEventRecord(b, s));
+        CPDDG_CUDA(cudaEventSynchronize(b));
+        float ms = 0;
+        CPDDG_CUDA(cudaEventElapsedTime(&ms, a, b));
+        return ms * 1e-3;
+    }
+    ~Timer() {
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+    }
+};
+
+struct Workspace {
+    int n;
+    cudaStream_t st;
+    int grid;
+    ReduceWork red;
+    DevBuf<double> scal;  // device scalars: [0..cap) h, plus norms
+    std::int64_t launches = 0;
+    Workspace(int n_, cudaStream_t s) : n(n_), st(s) {
+        grid = reduction_blocks();
+        red.ensure(2);
+    }
+    /** out = (vnext ? vnext . w : w . w) after the optional update. */
+    void mgs(const double* hprev, const double* vprev, double* w, const double* vnext, double* out,
+             double* out2) {
+        k_mgs<<<grid, kRedThreads, 0, st>>>(n, hprev, vprev, w, vnext, red.partials.get(), red.counter.get(), out,
+                                            out2);
+        CPDDG_CUDA(cudaGetLastError());
+        ++launches;
+    }
+    void scale(const double* src, double s, double* dst) {
+        k_scale<<<grid, kRedThreads, 0, st>>>(n, src, s, dst);
+        CPDDG_CUDA(cudaGetLastError());
+        ++launches;
+    }
+};
+
+void record(cpddg_log* log, const std::vector<double>& res, int iters, bool conv, double final_true, double secs,
+            std::int64_t launches) {
+    if (!log) return;
+    log->n_residuals = static_cast<int>(res.size());
+    if (log->residuals)
+        for (int k = 0; k < std::min(log->capacity, log->n_residuals); ++k) log->residuals[k] = res[static_cast<std::size_t>(k)];
+    log->iterations = iters;
+    log->converged = conv ? 1 : 0;
+    log->final_true_residual = final_true;
+    log->seconds = secs;
+    log->kernel_launches = launches;
+}
+
+}  // namespace
+
+// solve.hpp:128-214
+static void gmres(cpddg_op* op, cpddg_pc* pc, const double* b, double* u, const cpddg_solve_params& prm,
+                  cpddg_log* log, cudaStream_t st) {
+    const int n = op->na;
+    if (pc && pc->n_global != n) throw InternalError("preconditioner size does not match the operator");
+    const int max_iter = prm.max_iter;
+    const int cycle = prm.restart > 0 ? prm.restart : max_iter;
+    Workspace ws(n, st);
+    const int cap = std::max(cycle, 1) + 2;
+    ws.scal.alloc(static_cast<std::size_t>(cap) + 4);
+    double* hd = ws.scal.get();      // h[0..m+1]
+    double* nd = hd + cap;           // [0] ||w0||^2, [1] ||r||^2
+    Pinned hh(static_cast<std::size_t>(cap) + 4);
+    DevBuf<double> w(static_cast<std::size_t>(n)), r(static_cast<std::size_t>(n)), tmp(static_cast<std::size_t>(n));
+    std::vector<DevBuf<double>> V;
+    auto basis = [&](int k) -> double* {
+        while (static_cast<int>(V.size()) <= k) V.emplace_back(static_cast<std::size_t>(n));
+        return V[static_cast<std::size_t>(k)].get();
+    };
+    DevBuf<const double*> vptr(static_cast<std::size_t>(cap));
+    DevBuf<double> yd(static_cast<std::size_t>(cap));
+    std::vector<const double*> vptr_h(static_cast<std::size_t>(cap));
+
+    Timer timer(st);
+    CPDDG_CUDA(cudaMemsetAsync(u, 0, sizeof(double) * n, st));
+    CPDDG_CUDA(cudaMemcpyAsync(r.get(), b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    auto fetch = [&](const double* dev, int cnt) {
+        CPDDG_CUDA(cudaMemcpyAsync(hh.p, dev, sizeof(double) * cnt, cudaMemcpyDeviceToHost, st));
+        CPDDG_CUDA(cudaStreamSynchronize(st));
+    };
+    ws.mgs(nullptr, nullptr, r.get(), nullptr, nd + 1, nullptr);
+    fetch(nd + 1, 1);
+    double rnorm = std::sqrt(hh.p[0]);
+    std::vector<double> residuals{rnorm};
+    const double beta0 = rnorm;
+    int total = 0;
+    bool converged = false;
+    if (beta0 == 0.0) {
+        record(log, residuals, 0, true, 0.0, timer.stop(), ws.launches);
+        return;
+    }
+    const double target = prm.rel_tol * beta0;
+    while (total < max_iter && !converged) {
+        const double beta = rnorm;
+        check_finite(beta, "gmres residual");
+        if (beta <= target) {
+            converged = true;
+            break;
+        }
+        ws.scale(r.get(), beta, basis(0));
+        std::vector<std::vector<double>> H;
+        std::vector<double> cs, sn, g{beta};
+        int m = 0;
+        bool breakdown = false;
+        while (m < cycle && total < max_iter) {
+            const double* z = basis(m);
+            if (pc) {
+                pc_apply(pc, basis(m), tmp.get(), false, st);
+                ++ws.launches;
+                z = tmp.get();
+            }
+            op_apply(op, z, w.get(), st);
+            ws.launches += 2;
+            // MGS: pass 0 also yields ||w||^2 before orthogonalisation
+            ws.mgs(nullptr, nullptr, w.get(), basis(0), hd + 0, nd + 0);
+            for (int i = 1; i <= m; ++i) ws.mgs(hd + i - 1, basis(i - 1), w.get(), basis(i), hd + i, nullptr);
+            ws.mgs(hd + m, basis(m), w.get(), nullptr, hd + m + 1, nullptr);
+            CPDDG_CUDA(cudaMemcpyAsync(hh.p, hd, sizeof(double) * (m + 2), cudaMemcpyDeviceToHost, st));
+            CPDDG_CUDA(cudaMemcpyAsync(hh.p + cap, nd, sizeof(double), cudaMemcpyDeviceToHost, st));
+            CPDDG_CUDA(cudaStreamSynchronize(st));
+            std::vector<double> h(hh.p, hh.p + m + 2);
+            h[static_cast<std::size_t>(m) + 1] = std::sqrt(h[static_cast<std::size_t>(m) + 1]);
+            const double wnorm0 = std::sqrt(hh.p[cap]);
+            const double subdiag = h[static_cast<std::size_t>(m) + 1];
+            check_finite(subdiag, "gmres basis norm");
+            for (int i = 0; i < m; ++i) {
+                const double t = cs[static_cast<std::size_t>(i)] * h[static_cast<std::size_t>(i)] + sn[static_cast<std::size_t>(i)] * h[static_cast<std::size_t>(i) + 1];
+                h[static_cast<std::size_t>(i) + 1] = -sn[static_cast<std::size_t>(i)] * h[static_cast<std::size_t>(i)] + cs[static_cast<std::size_t>(i)] * h[static_cast<std::size_t>(i) + 1];
+                h[static_cast<std::size_t>(i)] = t;
+            }
+            const double denom = std::hypot(h[static_cast<std::size_t>(m)], h[static_cast<std::size_t>(m) + 1]);
+            cs.push_back(denom == 0 ? 1.0 : h[static_cast<std::size_t>(m)] / denom);
+            sn.push_back(denom == 0 ? 0.0 : h[static_cast<std::size_t>(m) + 1] / denom);
+            h[static_cast<std::size_t>(m)] = denom;
+            g.push_back(-sn[static_cast<std::size_t>(m)] * g[static_cast<std::size_t>(m)]);
+            g[static_cast<std::size_t>(m)] = cs[static_cast<std::size_t>(m)] * g[static_cast<std::size_t>(m)];
+            H.push_back(std::move(h));
+            ++m;
+            ++total;
+            const double est = std::abs(g[static_cast<std::size_t>(m)]);
+            check_finite(est, "gmres residual estimate");
+            residuals.push_back(est);
+            if (subdiag <= 1e-14 * wnorm0) breakdown = true;
+            if (est <= target || breakdown) {
+                converged = true;
+                break;
+            }
+            ws.scale(w.get(), subdiag, basis(m));
+        }
+        if (m > 0) {
+            std::vector<double> y(static_cast<std::size_t>(m), 0.0);
+            for (int i = m - 1; i >= 0; --i) {
+                double s = g[static_cast<std::size_t>(i)];
+                for (int k = i + 1; k < m; ++k) s -= H[static_cast<std::size_t>(k)][static_cast<std::size_t>(i)] * y[static_cast<std::size_t>(k)];
+                if (H[static_cast<std::size_t>(i)][static_cast<std::size_t>(i)] == 0.0)
+                    throw DivergenceError("gmres encountered a singular projection");
+                y[static_cast<std::size_t>(i)] = s / H[static_cast<std::size_t>(i)][static_cast<std::size_t>(i)];
+            }
+            for (int k = 0; k < m; ++k) {
+                vptr_h[static_cast<std::size_t>(k)] = basis(k);
+                hh.p[k] = y[static_cast<std::size_t>(k)];
+            }
+            CPDDG_CUDA(cudaMemcpyAsync(vptr.get(), vptr_h.data(), sizeof(double*) * m, cudaMemcpyHostToDevice, st));
+            CPDDG_CUDA(cudaMemcpyAsync(yd.get(), hh.p, sizeof(double) * m, cudaMemcpyHostToDevice, st));
+            k_combine<<<ws.grid, kRedThreads, 0, st>>>(n, m, vptr.get(), yd.get(), tmp.get());
+            CPDDG_CUDA(cudaGetLastError());
+            ++ws.launches;
+            if (pc) {
+                pc_apply(pc, tmp.get(), u, true, st);
+            } else {
+                k_axpy1<<<ws.grid, kRedThreads, 0, st>>>(n, tmp.get(), u);
+                CPDDG_CUDA(cudaGetLastError());
+            }
+            ++ws.launches;
+            // keep the host copy of y alive until the transfer completed
+            CPDDG_CUDA(cudaStreamSynchronize(st));
+        }
+        op_residual(op, b, u, r.get(), nd + 1, st);
+        ws.launches += 2;
+        fetch(nd + 1, 1);
+        rnorm = std::sqrt(hh.p[0]);
+    }
+    // final_true_residual = ||b - A u|| (solve.hpp:212): r was just recomputed from u
+    record(log, residuals, total, converged, rnorm, timer.stop(), ws.launches);
+}
+
+// solve.hpp:95-123
+static void stationary(cpddg_op* op, cpddg_pc* pc, const double* b, double* u, const cpddg_solve_params& prm,
+                       cpddg_log* log, cudaStream_t st) {
+    const int n = op->na;
+    if (!pc) throw InternalError("stationary iteration needs a preconditioner");
+    if (pc->n_global != n) throw InternalError("preconditioner size does not match the operator");
+    Workspace ws(n, st);
+    ws.scal.alloc(2);
+    Pinned hh(2);
+    DevBuf<double> r(static_cast<std::size_t>(n));
+    Timer timer(st);
+    CPDDG_CUDA(cudaMemsetAsync(u, 0, sizeof(double) * n, st));
+    CPDDG_CUDA(cudaMemcpyAsync(r.get(), b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    ws.mgs(nullptr, nullptr, r.get(), nullptr, ws.scal.get(), nullptr);
+    CPDDG_CUDA(cudaMemcpyAsync(hh.p, ws.scal.get(), sizeof(double), cudaMemcpyDeviceToHost, st));
+    CPDDG_CUDA(cudaStreamSynchronize(st));
+    const double r0 = std::sqrt(hh.p[0]);
+    std::vector<double> residuals{r0};
+    if (r0 == 0.0) {
+        record(log, residuals, 0, true, 0.0, timer.stop(), ws.launches);
+        return;
+    }
+    bool converged = false;
+    int iters = 0;
+    double rn = r0;
+    for (int it = 1; it <= prm.max_iter; ++it) {
+        pc_apply(pc, r.get(), u, true, st);
+        op_residual(op, b, u, r.get(), ws.scal.get(), st);
+        ws.launches += 3;
+        CPDDG_CUDA(cudaMemcpyAsync(hh.p, ws.scal.get(), sizeof(double), cudaMemcpyDeviceToHost, st));
+        CPDDG_CUDA(cudaStreamSynchronize(st));
+        rn = std::sqrt(hh.p[0]);
+        check_finite(rn, "stationary residual");
+        residuals.push_back(rn);
+        iters = it;
+        if (rn > 1e8 * r0) throw DivergenceError("stationary iteration diverged");
+        if (rn <= prm.rel_tol * r0) {
+            converged = true;
+            break;
+        }
+    }
+    record(log, residuals, iters, converged, rn, timer.stop(), ws.launches);
+}
+
+}  // namespace cpddg
+
+using namespace cpddg;
+
+extern "C" {
+
+int cpddg_gmres(cpddg_op* op, cpddg_pc* pc, const double* b, double* u, const cpddg_solve_params* prm,
+                cpddg_log* log, void* stream) {
+    return guarded([&] {
+        if (!op || !b || !u || !prm) throw InternalError("null argument");
+        if (prm->max_iter < 0 || prm->restart < 0) throw ConfigError("max_iter and restart must be >= 0");
+        if (!(prm->rel_tol > 0 && prm->rel_tol < 1)) throw ConfigError("rel_tol must lie strictly between 0 and 1");
+        gmres(op, pc, b, u, *prm, log, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int cpddg_stationary(cpddg_op* op, cpddg_pc* pc, const double* b, double* u, const cpddg_solve_params* prm,
+                     cpddg_log* log, void* stream) {
+    return guarded([&] {
+        if (!op || !b || !u || !prm) throw InternalError("null argument");
+        if (!(prm->rel_tol > 0 && prm->rel_tol < 1)) throw ConfigError("rel_tol must lie strictly between 0 and 1");
+        stationary(op, pc, b, u, *prm, log, static_cast<cudaStream_t>(stream));
+    });
+}
+
+}  // extern "C"

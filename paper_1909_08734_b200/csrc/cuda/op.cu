@@ -1,0 +1,379 @@
+// Matrix-free CPM operator on the device.
+//
+// Replaces SparseOperator::apply on the assembled Helmholtz matrix
+// (proj/include/cpdd/sparse.hpp:65-75; A from operators.hpp:96-112):
+//
+//   (A x)_i = (c + 2d/h^2) x_i - h^-2 sum_{k in 2d axis nbrs of i} (E x)_k
+//
+// Two streaming kernels, both HBM-bound:
+//   k_extend : v_k = (E x)_k for every band node (actives + ghosts).  The
+//              (p+1)^d stencil of cp_k is (p+1)^(d-1) runs of p+1
+//              CONSECUTIVE active ordinals (lexicographic band order, last
+//              axis fastest -- verified at create time), so a node stores
+//              one int32 start per run plus its d stencil offsets t_a; the
+//              1-D barycentric weights are recomputed from t_a in registers
+//              (interp.hpp:35-54, same exact-hit rule) instead of loading
+//              (p+1)^d weights.
+//   k_helm   : y_i = (c+gamma) x_i - ih2 sum_k v[nbr_k(i)], optionally fused
+//              with r = b - y and a deterministic ||r||^2 partial sum.
+// Layout: every per-node table is structure-of-arrays ([entry][node]) so a
+// warp's loads of one table entry are one contiguous 128-byte line.
+#include "../host/setup.hpp"
+#include "common.cuh"
+#include "op.cuh"
+
+#include <cmath>
+
+namespace cpddg {
+
+int sm_count() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        CPDDG_CUDA(cudaGetDevice(&dev));
+        CPDDG_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+    }
+    return n;
+}
+
+int reduction_blocks() { return 4 * sm_count(); }
+
+void ReduceWork::ensure(int s) {
+    if (s <= slots) return;
+    partials.alloc(static_cast<std::size_t>(s) * reduction_blocks());
+    counter.alloc(static_cast<std::size_t>(s));
+    counter.zero();
+    CPDDG_CUDA(cudaDeviceSynchronize());
+    slots = s;
+}
+
+namespace {
+
+/** interp_weights_1d (interp.hpp:35-54) for a compile-time degree. */
+template <int P>
+__device__ __forceinline__ void weights_1d(double t, double* w) {
+#pragma unroll
+    for (int j = 0; j <= P; ++j) w[j] = 0.0;
+    int hit = -1;
+#pragma unroll
+    for (int j = 0; j <= P; ++j)
+        if (hit < 0 && fabs(t - j) < 1e-12) hit = j;
+    if (hit >= 0) {
+#pragma unroll
+        for (int j = 0; j <= P; ++j) w[j] = (j == hit) ? 1.0 : 0.0;
+        return;
+    }
+    double sum = 0.0, b = 1.0;
+#pragma unroll
+    for (int j = 0; j <= P; ++j) {
+        w[j] = __ddiv_rn(b, __dsub_rn(t, static_cast<double>(j)));
+        sum = __dadd_rn(sum, w[j]);
+        b *= -static_cast<double>(P - j) / (j + 1);
+    }
+#pragma unroll
+    for (int j = 0; j <= P; ++j) w[j] = __ddiv_rn(w[j], sum);
+}
+
+template <int D, int P>
+__global__ void __launch_bounds__(256) k_extend(int nb, const double* __restrict__ t,
+                                                const int* __restrict__ lines,
+                                                const double* __restrict__ x, double* __restrict__ v) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= nb) return;
+    constexpr int Q = P + 1;
+    double wl[Q];  // weights along the contiguous (last) axis
+    weights_1d<P>(__ldg(t + static_cast<std::size_t>(D - 1) * nb + k), wl);
+    double acc = 0.0;
+    if constexpr (D == 2) {
+        double w0[Q];
+        weights_1d<P>(__ldg(t + k), w0);
+#pragma unroll
+        for (int a = 0; a < Q; ++a) {
+            const int o = __ldg(lines + static_cast<std::size_t>(a) * nb + k);
+            double s = 0.0;
+#pragma unroll
+            for (int c = 0; c < Q; ++c) s = fma(wl[c], __ldg(x + o + c), s);
+            acc = fma(w0[a], s, acc);
+        }
+    } else {
+        double w0[Q], w1[Q];
+        weights_1d<P>(__ldg(t + k), w0);
+        weights_1d<P>(__ldg(t + static_cast<std::size_t>(nb) + k), w1);
+#pragma unroll
+        for (int a = 0; a < Q; ++a) {
+            double sa = 0.0;
+#pragma unroll
+            for (int b = 0; b < Q; ++b) {
+                const int o = __ldg(lines + static_cast<std::size_t>(a * Q + b) * nb + k);
+                double s = 0.0;
+#pragma unroll
+                for (int c = 0; c < Q; ++c) s = fma(wl[c], __ldg(x + o + c), s);
+                sa = fma(w1[b], s, sa);
+            }
+            acc = fma(w0[a], sa, acc);
+        }
+    }
+    v[k] = acc;
+}
+
+/** y = cg x - ih2 sum v[nbr]; if b != nullptr: y <- b - y and partial ||y||^2. */
+template <int D, bool RESID>
+__global__ void __launch_bounds__(kRedThreads) k_helm(int na, double cg, double ih2,
+                                                      const int* __restrict__ nbr,
+                                                      const double* __restrict__ v,
+                                                      const double* __restrict__ x,
+                                                      const double* __restrict__ b,
+                                                      double* __restrict__ y, double* partials,
+                                                      unsigned int* counter, double* result) {
+    double local = 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < na; i += gridDim.x * blockDim.x) {
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < 2 * D; ++k) s += __ldg(v + __ldg(nbr + static_cast<std::size_t>(k) * na + i));
+        const double ax = cg * __ldg(x + i) - ih2 * s;
+        if constexpr (RESID) {
+            const double r = __ldg(b + i) - ax;
+            y[i] = r;
+            local = fma(r, r, local);
+        } else {
+            y[i] = ax;
+        }
+    }
+    if constexpr (RESID) {
+        __shared__ double sh[kRedThreads / 32];
+        __shared__ bool last;
+        const double bs = block_sum<kRedThreads>(local, sh);
+        if (threadIdx.x == 0) {
+            partials[blockIdx.x] = bs;
+            __threadfence();
+            last = atomicInc(counter, gridDim.x - 1) == gridDim.x - 1;
+        }
+        __syncthreads();
+        if (last) {
+            __threadfence();
+            double acc = 0.0;
+            for (int q = threadIdx.x; q < static_cast<int>(gridDim.x); q += blockDim.x)
+                acc += static_cast<volatile double*>(partials)[q];
+            const double tot = block_sum<kRedThreads>(acc, sh);
+            if (threadIdx.x == 0) *result = tot;
+        }
+    }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- host side
+
+template <int D>
+static void build_tables(cpddg_op* op, const Ix<D>* ix, const Vec<D>* cp, const LatticeMap& map) {
+    const int nb = op->na + op->ng, p = op->p, Q = p + 1;
+    int nlines = 1;
+    for (int a = 0; a < D - 1; ++a) nlines *= Q;
+    std::vector<double> t(static_cast<std::size_t>(D) * nb);
+    std::vector<int> lines(static_cast<std::size_t>(nlines) * nb);
+    auto lookup = [&](const Ix<D>& q) { return map.find(LatticeMap::pack(q.data(), D)); };
+    parallel_for((nb + 8191) / 8192, 0, [&](int chunk, int) {
+        const int k1 = std::min(nb, (chunk + 1) * 8192);
+        for (int k = chunk * 8192; k < k1; ++k) {
+            const Stencil1D<D> s = stencil_of<D>(cp[k], op->h, p);
+            for (int a = 0; a < D; ++a) {
+                const double g = (cp[k][a] - 0.0) / op->h;
+                t[static_cast<std::size_t>(a) * nb + k] = g - s.base[a];
+            }
+            for (int l = 0; l < nlines; ++l) {
+                Ix<D> q;
+                int rem = l;
+                for (int a = D - 2; a >= 0; --a) {
+                    q[a] = s.base[a] + rem % Q;
+                    rem /= Q;
+                }
+                q[D - 1] = s.base[D - 1];
+                const std::int64_t o = lookup(q);
+                if (o < 0 || o >= op->na)
+                    throw InternalError("extension stencil node is not active: band closure violated");
+                for (int c = 1; c < Q; ++c) {
+                    Ix<D> r = q;
+                    r[D - 1] += c;
+                    if (lookup(r) != o + c)
+                        throw InternalError("stencil run is not contiguous in band order");
+                }
+                lines[static_cast<std::size_t>(l) * nb + k] = static_cast<int>(o);
+            }
+        }
+    });
+    std::vector<int> nbr(static_cast<std::size_t>(2 * D) * op->na);
+    for (int i = 0; i < op->na; ++i) {
+        Ix<D> around[2 * D];
+        neighbors_of<D>(ix[i], around);
+        for (int k = 0; k < 2 * D; ++k) {
+            const std::int64_t c = lookup(around[k]);
+            if (c < 0) throw InternalError("finite-difference neighbor missing from band");
+            nbr[static_cast<std::size_t>(k) * op->na + i] = static_cast<int>(c);
+        }
+    }
+    op->t.upload(t);
+    op->lines.upload(lines);
+    op->nbr.upload(nbr);
+    op->v.alloc(static_cast<std::size_t>(nb));
+    op->nlines = nlines;
+    // B_op = 16 N_A + [8d + 4 (p+1)^(d-1)] N_B + 8d N_A
+    op->alg_bytes = 16LL * op->na + (8LL * D + 4LL * nlines) * nb + 8LL * D * op->na;
+    // streamed: x read + y write, t + lines per band node, v write+read, nbr
+    op->streamed_bytes = 16LL * op->na + (8LL * D + 4LL * nlines) * nb + 16LL * nb + 8LL * D * op->na;
+}
+
+template <int D>
+static void launch_apply(const cpddg_op* op, const double* x, const double* b, double* y, double* rn2,
+                         cudaStream_t st) {
+    const int nb = op->na + op->ng;
+    const int thr = 256;
+    switch (op->p) {
+#define CPDDG_EXT(PP) \
+    case PP: k_extend<D, PP><<<(nb + thr - 1) / thr, thr, 0, st>>>(nb, op->t.get(), op->lines.get(), x, op->v.get()); break;
+        CPDDG_EXT(1) CPDDG_EXT(2) CPDDG_EXT(3) CPDDG_EXT(4) CPDDG_EXT(5) CPDDG_EXT(6) CPDDG_EXT(7)
+#undef CPDDG_EXT
+        default: throw ConfigError("interpolation degree must be in [1,7]");
+    }
+    CPDDG_CUDA(cudaGetLastError());
+    const int rb = reduction_blocks();
+    const int grid = std::min(rb, (op->na + kRedThreads - 1) / kRedThreads);
+    if (b)
+        k_helm<D, true><<<rb, kRedThreads, 0, st>>>(op->na, op->cg, op->ih2, op->nbr.get(), op->v.get(), x,
+                                                    b, y, op->red.partials.get(), op->red.counter.get(), rn2);
+    else
+        k_helm<D, false><<<std::max(grid, 1), kRedThreads, 0, st>>>(op->na, op->cg, op->ih2, op->nbr.get(),
+                                                                   op->v.get(), x, nullptr, y, nullptr,
+                                                                   nullptr, nullptr);
+    CPDDG_CUDA(cudaGetLastError());
+}
+
+void op_apply(const cpddg_op* op, const double* x, double* y, cudaStream_t st) {
+    if (op->dim == 2)
+        launch_apply<2>(op, x, nullptr, y, nullptr, st);
+    else
+        launch_apply<3>(op, x, nullptr, y, nullptr, st);
+}
+
+void op_residual(const cpddg_op* op, const double* b, const double* x, double* r, double* rn2_dev,
+                 cudaStream_t st) {
+    if (op->dim == 2)
+        launch_apply<2>(op, x, b, r, rn2_dev, st);
+    else
+        launch_apply<3>(op, x, b, r, rn2_dev, st);
+}
+
+template <int D>
+static cpddg_op* create_from(int p, int na, int ng, double h, double c, const Ix<D>* ix, const Vec<D>* cp,
+                             const LatticeMap* map_in) {
+    if (c <= 0) throw ConfigError("Helmholtz constant c must be positive");
+    if (!(h > 0)) throw ConfigError("grid spacing h must be positive");
+    if (p < 1 || p > 7) throw ConfigError("interpolation degree must be in [1,7]");
+    auto op = std::make_unique<cpddg_op>();
+    op->dim = D;
+    op->p = p;
+    op->na = na;
+    op->ng = ng;
+    op->h = h;
+    op->c = c;
+    op->cg = c + 2.0 * D / (h * h);
+    op->ih2 = 1.0 / (h * h);
+    LatticeMap own;
+    const LatticeMap* map = map_in;
+    if (!map) {
+        own.reserve(static_cast<std::size_t>(na + ng));
+        for (int k = 0; k < na + ng; ++k)
+            if (!own.insert(LatticeMap::pack(ix[k].data(), D), k))
+                throw InternalError("duplicate lattice index in band description");
+        map = &own;
+    }
+    build_tables<D>(op.get(), ix, cp, *map);
+    op->red.ensure(1);
+    op->rn2.alloc(1);
+    return op.release();
+}
+
+}  // namespace cpddg
+
+using namespace cpddg;
+
+extern "C" {
+
+int cpddg_op_create(const cpddg_band_desc* d, cpddg_op** out) {
+    return guarded([&] {
+        if (!d || !out || !d->ix || !d->cp) throw InternalError("null argument");
+        if (d->n_active <= 0) throw ConfigError("band is empty");
+        const int nb = d->n_active + d->n_ghost;
+        if (d->dim == 2) {
+            std::vector<Ix<2>> ix(static_cast<std::size_t>(nb));
+            std::vector<Vec<2>> cp(static_cast<std::size_t>(nb));
+            for (int k = 0; k < nb; ++k)
+                for (int a = 0; a < 2; ++a) {
+                    ix[static_cast<std::size_t>(k)][a] = d->ix[2 * k + a];
+                    cp[static_cast<std::size_t>(k)][a] = d->cp[2 * k + a];
+                }
+            *out = create_from<2>(d->p, d->n_active, d->n_ghost, d->h, d->c, ix.data(), cp.data(), nullptr);
+        } else if (d->dim == 3) {
+            std::vector<Ix<3>> ix(static_cast<std::size_t>(nb));
+            std::vector<Vec<3>> cp(static_cast<std::size_t>(nb));
+            for (int k = 0; k < nb; ++k)
+                for (int a = 0; a < 3; ++a) {
+                    ix[static_cast<std::size_t>(k)][a] = d->ix[3 * k + a];
+                    cp[static_cast<std::size_t>(k)][a] = d->cp[3 * k + a];
+                }
+            *out = create_from<3>(d->p, d->n_active, d->n_ghost, d->h, d->c, ix.data(), cp.data(), nullptr);
+        } else {
+            throw ConfigError("dimension must be 2 or 3");
+        }
+    });
+}
+
+int cpddg_op_create_from_setup(const cpddg_setup* s, cpddg_op** out) {
+    return guarded([&] {
+        if (!s || !out) throw InternalError("null argument");
+        if (s->dim == 2) {
+            auto& I = impl_of<2>(s);
+            *out = create_from<2>(I.band.p, I.band.n_active, I.band.n_ghost, I.band.h, s->c, I.band.ix.data(),
+                                  I.band.cp.data(), &I.band.map);
+        } else {
+            auto& I = impl_of<3>(s);
+            *out = create_from<3>(I.band.p, I.band.n_active, I.band.n_ghost, I.band.h, s->c, I.band.ix.data(),
+                                  I.band.cp.data(), &I.band.map);
+        }
+    });
+}
+
+int cpddg_op_apply(cpddg_op* op, const double* x, double* y, void* stream) {
+    return guarded([&] {
+        if (!op || !x || !y) throw InternalError("null argument");
+        op_apply(op, x, y, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int cpddg_op_residual(cpddg_op* op, const double* b, const double* x, double* r, double* rnorm, void* stream) {
+    return guarded([&] {
+        if (!op || !b || !x || !r) throw InternalError("null argument");
+        auto st = static_cast<cudaStream_t>(stream);
+        op_residual(op, b, x, r, op->rn2.get(), st);
+        double h = 0;
+        CPDDG_CUDA(cudaMemcpyAsync(&h, op->rn2.get(), sizeof(double), cudaMemcpyDeviceToHost, st));
+        CPDDG_CUDA(cudaStreamSynchronize(st));
+        if (rnorm) *rnorm = std::sqrt(h);
+    });
+}
+
+int cpddg_op_size(const cpddg_op* op) { return op ? op->na : -1; }
+
+int cpddg_op_bytes(const cpddg_op* op, int64_t* alg, int64_t* streamed) {
+    return guarded([&] {
+        if (!op) throw InternalError("null argument");
+        if (alg) *alg = op->alg_bytes;
+        if (streamed) *streamed = op->streamed_bytes;
+    });
+}
+
+int cpddg_op_destroy(cpddg_op* op) {
+    delete op;
+    return CPDDG_OK;
+}
+
+}  // extern "C"

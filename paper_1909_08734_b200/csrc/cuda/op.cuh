@@ -1,0 +1,56 @@
+// Internal definitions of the device operator and preconditioner handles,
+// shared by op.cu, pc.cu and krylov.cu.
+#pragma once
+
+#include "common.cuh"
+
+#include <cstdint>
+#include <vector>
+
+struct cpddg_op {
+    int dim = 0, p = 0, na = 0, ng = 0, nlines = 0;
+    double h = 0, c = 0, cg = 0, ih2 = 0;
+    cpddg::DevBuf<double> t;    // [dim][N_B] stencil offsets g_a - base_a
+    cpddg::DevBuf<int> lines;   // [(p+1)^(d-1)][N_B] first ordinal of each contiguous run
+    cpddg::DevBuf<int> nbr;     // [2d][N_A] band codes of the axis neighbours
+    cpddg::DevBuf<double> v;    // [N_B] extension values E x
+    cpddg::DevBuf<double> rn2;  // scalar slot for ||b - A x||^2
+    cpddg::ReduceWork red;
+    std::int64_t alg_bytes = 0, streamed_bytes = 0;
+};
+
+/** Envelope (profile) LU factors of every subdomain system, batched. */
+struct cpddg_pc {
+    int n_global = 0, n_sub = 0, max_rows = 0;
+    int n_reduced = 0;
+    std::int64_t rows_total = 0, entries = 0;
+    // per subdomain (device)
+    cpddg::DevBuf<int> n_rows;         // [n_sub]
+    cpddg::DevBuf<std::int64_t> vbase; // [n_sub] first row in the concatenated per-row arrays
+    cpddg::DevBuf<std::int64_t> ebase; // [n_sub] first entry in the concatenated L / U arrays
+    cpddg::DevBuf<int> order;          // [n_sub] launch order (largest first)
+    // per row (device, concatenated over subdomains, in factor order)
+    cpddg::DevBuf<int> first;          // envelope start column f_i (local index)
+    cpddg::DevBuf<std::int64_t> roff;  // offset of row i inside its subdomain's L/U arrays
+    cpddg::DevBuf<int> rlast;          // largest row whose envelope starts at or before i
+    cpddg::DevBuf<int> gidx;           // global index gathered into row i (R_j), or -1
+    cpddg::DevBuf<int> sidx;           // global index row i scatters to (owned), or -1
+    cpddg::DevBuf<double> diag;        // U_ii
+    // per envelope entry
+    cpddg::DevBuf<double> L;           // L_ij, j in [f_i, i), row-contiguous
+    cpddg::DevBuf<double> U;           // U_ji (column i of U), j in [f_i, i), contiguous
+    std::int64_t factor_bytes = 0, alg_bytes = 0;
+    double factor_seconds = 0, analyse_seconds = 0, max_probe_residual = -1;
+    int solve_smem = 0;
+};
+
+namespace cpddg {
+void op_apply(const cpddg_op* op, const double* x, double* y, cudaStream_t st);
+/** r = b - A x and ||r||^2 into *rn2_dev (device scalar). */
+void op_residual(const cpddg_op* op, const double* b, const double* x, double* r, double* rn2_dev,
+                 cudaStream_t st);
+/** z = M r (accumulate = false) or z += M r (accumulate = true: the owned
+ *  slots are disjoint, so this is accumulate_correction of
+ *  transmission.hpp:66-69 applied for every subdomain). */
+void pc_apply(const cpddg_pc* pc, const double* r, double* z, bool accumulate, cudaStream_t st);
+}  // namespace cpddg

@@ -1,0 +1,193 @@
+"""Device path vs the reference (golden vectors from oracle/_ref) and the
+oracle restatement (oracle/cpdd_oracle.py), through the C ABI.
+
+Tolerances (BASELINE.json north_star): operator applies 1e-12 in the
+componentwise-scaled metric max_i |dy_i| / sum_j |A_ij x_j|; final solutions
+1e-8 relative; GMRES / stationary iteration counts within +-2.  The
+preconditioner apply is checked at 1e-9 relative (different LU backends,
+each with a ~1e-12 residual contract)."""
+import ast
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+CASES = sorted(f[:-4] for f in os.listdir(GOLDEN) if f.endswith(".npz"))
+
+
+def _setup(name):
+    import torch
+
+    from paper_1909_08734_b200 import api
+    g = np.load(os.path.join(GOLDEN, name + ".npz"))
+    cfg = ast.literal_eval(str(g["cfg"]))
+    P = api.Problem(cfg["surface"], h=cfg["h"], p=cfg["p"], c=cfg["c"],
+                    major_radius=cfg.get("major_radius", 2.0 / 3.0), minor_radius=cfg.get("minor_radius", 1.0 / 3.0))
+    assert P.n_active == int(g["n_active"]) and P.n_ghost == int(g["n_ghost"])
+    aligned, moves = P.decompose(g["part_in"], cfg["n_overlap"], cfg["method"], cfg.get("alpha", 1.0),
+                                 cfg.get("alpha_cross", -1.0))
+    assert np.array_equal(aligned, g["part_aligned"]) and moves == int(g["moves"])
+    A = api.DeviceHelmholtz.from_problem(P)
+    M = api.SchwarzPreconditioner.from_problem(P)
+    return g, cfg, P, A, M, torch
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_operator_matches_reference(name):
+    import cpdd_oracle as O
+    g, cfg, P, A, M, torch = _setup(name)
+    x = g["x"]
+    y = A.apply(torch.from_numpy(x).cuda()).cpu().numpy()
+    ptr, col, val = P.csr("A")
+    assert O.op_rel_error(ptr, col, val, x, y, g["Ax"]) <= 1e-12
+    # normwise as well
+    assert np.linalg.norm(y - g["Ax"]) <= 1e-13 * np.linalg.norm(np.abs(val)) * np.linalg.norm(x) + 1e-12 * np.linalg.norm(g["Ax"])
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_preconditioner_matches_reference(name):
+    g, cfg, P, A, M, torch = _setup(name)
+    z = M.apply(torch.from_numpy(g["x"]).cuda()).cpu().numpy()
+    assert np.linalg.norm(z - g["Mx"]) <= 1e-9 * np.linalg.norm(g["Mx"])
+    # deterministic: a second apply is bitwise identical
+    z2 = M.apply(torch.from_numpy(g["x"]).cuda()).cpu().numpy()
+    assert np.array_equal(z, z2)
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_solve_matches_reference(name):
+    from paper_1909_08734_b200 import api
+    g, cfg, P, A, M, torch = _setup(name)
+    b = torch.from_numpy(g["b"]).cuda()
+    if cfg["mode"] == "gmres":
+        res = api.gmres_solve(A, b, M, cfg["rel_tol"], cfg["max_iter"], cfg.get("gmres_restart", 0))
+    else:
+        res = api.stationary_solve(A, b, M, cfg["rel_tol"], cfg["max_iter"])
+    u = res.u.cpu().numpy()
+    it_ref = int(g["iterations"])
+    assert res.log.converged
+    assert abs(res.log.iterations - it_ref) <= 2, (res.log.iterations, it_ref)
+    assert len(res.log.residuals) == res.log.iterations + 1
+    assert abs(res.log.residuals[0] - np.linalg.norm(g["b"])) <= 1e-12 * np.linalg.norm(g["b"])
+    assert res.log.residuals[-1] <= cfg["rel_tol"] * res.log.residuals[0]
+    assert np.linalg.norm(u - g["u"]) <= 1e-8 * np.linalg.norm(g["u"])
+    assert abs(res.log.final_true_residual - np.linalg.norm(g["b"] - A.apply(res.u).cpu().numpy())) <= \
+        1e-6 * res.log.final_true_residual + 1e-300
+
+
+def test_against_oracle_restatement_small_sphere():
+    """GMRES(50) ORAS on a sphere, device vs the numpy/scipy restatement."""
+    import torch
+
+    import cpdd_oracle as O
+    from paper_1909_08734_b200 import api, inputs
+    P = api.Problem("sphere", h=0.1, p=3, c=1.0)
+    part = inputs.rcb_partition(P.active_cp, 8)
+    P.decompose(part, 2, "oras", 2.0, 20.0)
+    A = api.DeviceHelmholtz.from_problem(P)
+    M = api.SchwarzPreconditioner.from_problem(P)
+    ptr, col, val = P.csr("A")
+    Mo = O.Schwarz([P.local(j) for j in range(P.n_sub)])
+    b = inputs.rhs_sphere(P.active_cp)
+    ref = O.gmres_solve(lambda v: O.csr_apply(ptr, col, val, v), Mo, b, 1e-10, 500, 50)
+    res = api.gmres_solve(A, torch.from_numpy(b).cuda(), M, 1e-10, 500, 50)
+    assert abs(res.log.iterations - ref["iterations"]) <= 2
+    assert np.linalg.norm(res.u.cpu().numpy() - ref["u"]) <= 1e-8 * np.linalg.norm(ref["u"])
+    x = inputs.uniform_vector(P.n_active, 5)
+    z = M.apply(torch.from_numpy(x).cuda()).cpu().numpy()
+    zo = Mo(x)
+    assert np.linalg.norm(z - zo) <= 1e-9 * np.linalg.norm(zo)
+
+
+def test_plain_gmres_without_preconditioner():
+    import torch
+
+    import cpdd_oracle as O
+    from paper_1909_08734_b200 import api, inputs
+    P = api.Problem("circle", h=0.05, p=3, c=1.0)
+    A = api.DeviceHelmholtz.from_problem(P)
+    ptr, col, val = P.csr("A")
+    b = inputs.rhs_circle(P.active_cp)
+    ref = O.gmres_solve(lambda v: O.csr_apply(ptr, col, val, v), None, b, 1e-10, 400)
+    res = api.gmres_solve(A, torch.from_numpy(b).cuda(), None, 1e-10, 400)
+    assert res.log.converged and abs(res.log.iterations - ref["iterations"]) <= 2
+    assert np.linalg.norm(res.u.cpu().numpy() - ref["u"]) <= 1e-8 * np.linalg.norm(ref["u"])
+
+
+def test_zero_rhs_short_circuits():
+    import torch
+
+    from paper_1909_08734_b200 import api, inputs
+    P = api.Problem("circle", h=0.1, p=2, c=1.0)
+    P.decompose(inputs.sector_partition(P.active_cp, 2), 2, "ras")
+    A = api.DeviceHelmholtz.from_problem(P)
+    M = api.SchwarzPreconditioner.from_problem(P)
+    zero = torch.zeros(P.n_active, dtype=torch.float64, device="cuda")
+    for res in (api.stationary_solve(A, zero, M, 1e-8, 50), api.gmres_solve(A, zero, M, 1e-8, 50)):
+        assert res.log.converged and res.log.iterations == 0
+        assert res.log.residuals == [0.0] and res.log.final_true_residual == 0.0
+        assert float(res.u.abs().max()) == 0.0
+
+
+def test_single_subdomain_is_exact_inverse():
+    import torch
+
+    from paper_1909_08734_b200 import api, inputs
+    P = api.Problem("circle", h=0.1, p=2, c=1.0)
+    P.decompose(np.zeros(P.n_active, np.int32), 4, "ras")
+    A = api.DeviceHelmholtz.from_problem(P)
+    M = api.SchwarzPreconditioner.from_problem(P)
+    b = torch.from_numpy(inputs.uniform_vector(P.n_active, 3)).cuda()
+    res = api.stationary_solve(A, b, M, 1e-10, 50)
+    assert res.log.converged and res.log.iterations == 1 and len(res.log.residuals) == 2
+    assert res.log.final_true_residual <= 1e-10 * float(b.norm())
+
+
+def _identity_locals(n, s):
+    return [dict(n_overlap=n, n_bc=0, overlap=np.arange(n), scatter_local=np.arange(n),
+                 scatter_global=np.arange(n), ptr=np.arange(n + 1), col=np.arange(n), val=np.full(n, s))]
+
+
+def test_divergence_is_detected():
+    """solve.hpp:115 -- a preconditioner scaled -3x makes the iteration grow."""
+    import torch
+
+    from paper_1909_08734_b200 import api, errors, inputs
+    P = api.Problem("circle", h=0.1, p=2, c=1.0)
+    A = api.DeviceHelmholtz.from_problem(P)
+    M = api.SchwarzPreconditioner.from_locals(P.n_active, _identity_locals(P.n_active, -1.0 / 3.0))
+    b = torch.from_numpy(inputs.uniform_vector(P.n_active, 41)).cuda()
+    with pytest.raises(errors.DivergenceError):
+        api.stationary_solve(A, b, M, 1e-8, 1000)
+
+
+def test_singular_local_factor_raises():
+    """direct.hpp:47-50: a singular local system is a DivergenceError."""
+    from paper_1909_08734_b200 import api, errors
+    with pytest.raises(errors.DivergenceError, match="singular factorization of subdomain 0"):
+        api.SchwarzPreconditioner.from_locals(10, _identity_locals(10, 0.0))
+
+
+def test_overlapping_scatter_rejected():
+    from paper_1909_08734_b200 import api, errors
+    L = _identity_locals(10, 1.0) * 2
+    with pytest.raises(errors.InternalError):
+        api.SchwarzPreconditioner.from_locals(10, L)
+
+
+def test_drop_in_band_descriptor_matches_setup():
+    """cpddg_op_create from plain band arrays (the reference BandGrid fields)
+    gives the same operator as the setup-built one, bit for bit."""
+    import torch
+
+    from paper_1909_08734_b200 import api, inputs
+    P = api.Problem("sphere", h=0.1, p=3, c=1.0)
+    B = P.band()
+    A1 = api.DeviceHelmholtz.from_problem(P)
+    A2 = api.DeviceHelmholtz.from_band(3, 3, 0.1, 1.0, P.n_active, B["ix"], B["cp"])
+    x = torch.from_numpy(inputs.uniform_vector(P.n_active, 9)).cuda()
+    assert torch.equal(A1.apply(x), A2.apply(x))
