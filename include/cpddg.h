@@ -186,7 +186,8 @@ int cpddg_pc_destroy(cpddg_pc* pc);
 typedef struct {
     double rel_tol;
     int max_iter;
-    int restart; /* gmres: 0 = no restart (cycle = max_iter) */
+    int restart;         /* gmres: 0 = no restart (cycle = max_iter) */
+    int profile_kernels; /* 1: time every preconditioner / operator launch with CUDA events */
 } cpddg_solve_params;
 
 typedef struct {
@@ -198,6 +199,12 @@ typedef struct {
     double final_true_residual;
     double seconds;      /* device-timed solve loop (CUDA events) */
     int64_t kernel_launches;
+    /* filled when profile_kernels: summed device time and count of the
+     * preconditioner applies (k_solve) and operator applies (k_extend + k_helm) */
+    double pc_seconds;
+    int64_t pc_launches;
+    double op_seconds;
+    int64_t op_launches;
 } cpddg_log;
 
 int cpddg_gmres(cpddg_op* op, cpddg_pc* pc, const double* b_dev, double* u_dev,

@@ -215,3 +215,54 @@ class RefProblem:
         return dict(u=u, iterations=iters.value, converged=bool(conv.value),
                     final_relative_residual=frel.value,
                     timings=dict(mesh=t[0], global_matrix=t[1], local_operators=t[2], solve=t[3]))
+
+
+def _setup_extra(L):
+    if getattr(L, "_extra", False):
+        return
+    PP = C.POINTER(C.c_void_p)
+    L.cref_set_locals.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    L.cref_solve_capped.argtypes = [C.c_void_p, _f64p, C.c_int, C.c_double, C.POINTER(C.c_int),
+                                    C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    L._extra = True
+
+
+def set_locals(P: RefProblem, locals_: list):
+    """Install LocalOperators (reference struct) from field arrays and factor
+    them with the reference DirectSolver on the reference ThreadPool."""
+    L = lib()
+    _setup_extra(L)
+    n = len(locals_)
+    keep = []
+
+    def arr(ctype, items):
+        a = (ctype * n)(*items)
+        keep.append(a)
+        return a
+
+    cols = []
+    for d in locals_:
+        cols.append([np.ascontiguousarray(d["overlap"], np.int32), np.ascontiguousarray(d["scatter_local"], np.int32),
+                     np.ascontiguousarray(d["scatter_global"], np.int32), np.ascontiguousarray(d["ptr"], np.int64),
+                     np.ascontiguousarray(d["col"], np.int32), np.ascontiguousarray(d["val"], np.float64)])
+    keep.append(cols)
+    vp = C.c_void_p
+    rc = L.cref_set_locals(P._h, n, arr(C.c_int, [int(d["n_overlap"]) for d in locals_]),
+                           arr(C.c_int, [int(d["n_bc"]) for d in locals_]),
+                           arr(vp, [c[0].ctypes.data for c in cols]),
+                           arr(C.c_int, [int(c[1].size) for c in cols]),
+                           arr(vp, [c[1].ctypes.data for c in cols]), arr(vp, [c[2].ctypes.data for c in cols]),
+                           arr(vp, [c[3].ctypes.data for c in cols]), arr(vp, [c[4].ctypes.data for c in cols]),
+                           arr(vp, [c[5].ctypes.data for c in cols]))
+    P._check(rc)
+    P.locals_seconds = L.cref_decompose_time(P._h, 1)
+
+
+def solve_capped(P: RefProblem, b, max_iter: int, rel_tol: float):
+    L = lib()
+    _setup_extra(L)
+    it, secs, last = C.c_int(), C.c_double(), C.c_double()
+    b = np.ascontiguousarray(b, np.float64)
+    P._check(L.cref_solve_capped(P._h, b, int(max_iter), float(rel_tol), C.byref(it), C.byref(secs), C.byref(last)))
+    return dict(iterations=it.value, seconds=secs.value, last_residual=last.value)

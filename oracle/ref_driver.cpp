@@ -438,4 +438,59 @@ int cref_run_solve(void* hv, double* u, int* iters, int* converged, double* fina
     });
 }
 
+/** Install subdomain systems given as the reference's own LocalOperator fields
+ *  (transmission.hpp:47-70: n_overlap, n_bc, overlap, scatter, A) and factor
+ *  each with the reference's DirectSolver (direct.hpp:41-52) on the thread
+ *  pool, then build the SchwarzPreconditioner (solve.hpp:64-86).  Used by the
+ *  CPU baseline at sizes where the reference's serial build_subdomains is too
+ *  slow to run inside a benchmark (its outputs are bit-identical to the
+ *  device path's setup; tests/test_setup_parity.py). */
+int cref_set_locals(void* hv, int n_sub, const int* n_overlap, const int* n_bc, const int* const* overlap,
+                    const int* n_scatter, const int* const* sc_local, const int* const* sc_global,
+                    const long long* const* row_ptr, const int* const* col, const double* const* val) {
+    auto* H = static_cast<Handle*>(hv);
+    return visit(H, [&](auto& I) {
+        double t0 = now_s();
+        std::vector<LocalOperator> locals(static_cast<std::size_t>(n_sub));
+        auto build_one = [&](int j) {
+            LocalOperator& L = locals[static_cast<std::size_t>(j)];
+            L.id = j;
+            L.n_overlap = n_overlap[j];
+            L.n_bc = n_bc[j];
+            L.overlap.assign(overlap[j], overlap[j] + n_overlap[j]);
+            for (int k = 0; k < n_scatter[j]; ++k) L.scatter.emplace_back(sc_local[j][k], sc_global[j][k]);
+            const int n = L.n_local();
+            L.A = SparseOperator(n, n);
+            std::vector<std::pair<int, double>> row;
+            for (int r = 0; r < n; ++r) {
+                for (long long k = row_ptr[j][r]; k < row_ptr[j][r + 1]; ++k) row.emplace_back(col[j][k], val[j][k]);
+                L.A.append_row(row);
+            }
+            L.lu.factor(L.A, "subdomain " + std::to_string(j));
+        };
+        H->pool->run_batch(n_sub, build_one);
+        I.M = std::make_unique<SchwarzPreconditioner>(std::move(locals), I.P->grid.n_active(), H->pool.get());
+        I.t_locals = now_s() - t0;
+    });
+}
+
+/** gmres_solve / stationary_solve with an explicit iteration cap and
+ *  tolerance (a bounded sample of the configured solve). */
+int cref_solve_capped(void* hv, const double* b, int max_iter, double rel_tol, int* iters, double* seconds,
+                      double* last_residual) {
+    auto* H = static_cast<Handle*>(hv);
+    return visit(H, [&](auto& I) {
+        const int n = I.P->grid.n_active();
+        Eigen::VectorXd bv = Eigen::VectorXd(Eigen::Map<Eigen::VectorXd>(b, n));
+        const SolverConfig& sc = I.cfg.solver;
+        double t0 = now_s();
+        SolveResult res = sc.mode == SolverConfig::Mode::gmres
+                              ? gmres_solve(I.P->A, bv, I.M.get(), rel_tol, max_iter, sc.gmres_restart)
+                              : stationary_solve(I.P->A, bv, *I.M, rel_tol, max_iter);
+        *seconds = now_s() - t0;
+        *iters = res.log.iterations;
+        *last_residual = res.log.residuals.back();
+    });
+}
+
 }  // extern "C"

@@ -53,14 +53,16 @@ class cpddg_pc_stats(C.Structure):
 
 
 class cpddg_solve_params(C.Structure):
-    _fields_ = [("rel_tol", C.c_double), ("max_iter", C.c_int), ("restart", C.c_int)]
+    _fields_ = [("rel_tol", C.c_double), ("max_iter", C.c_int), ("restart", C.c_int),
+                ("profile_kernels", C.c_int)]
 
 
 class cpddg_log(C.Structure):
     _fields_ = [("residuals", C.POINTER(C.c_double)), ("capacity", C.c_int),
                 ("n_residuals", C.c_int), ("iterations", C.c_int), ("converged", C.c_int),
                 ("final_true_residual", C.c_double), ("seconds", C.c_double),
-                ("kernel_launches", C.c_int64)]
+                ("kernel_launches", C.c_int64), ("pc_seconds", C.c_double), ("pc_launches", C.c_int64),
+                ("op_seconds", C.c_double), ("op_launches", C.c_int64)]
 
 
 _SIGS = {

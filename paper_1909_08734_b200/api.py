@@ -314,6 +314,7 @@ class IterationLog:
     timings: PhaseTimings = field(default_factory=PhaseTimings)
     device_seconds: float = 0.0
     kernel_launches: int = 0
+    kernel_times: dict = field(default_factory=dict)
 
 
 @dataclass
@@ -324,33 +325,36 @@ class SolveResult:
 
 
 def _solve(fn, A: DeviceHelmholtz, b, M, rel_tol: float, max_iter: int, restart: int,
-           cap: int) -> SolveResult:
+           cap: int, profile: bool = False) -> SolveResult:
     torch = _torch()
     b = b.contiguous()
     u = torch.empty_like(b)
     res = (C.c_double * cap)()
     log = _lib.cpddg_log(residuals=C.cast(res, C.POINTER(C.c_double)), capacity=cap)
-    prm = _lib.cpddg_solve_params(rel_tol=rel_tol, max_iter=max_iter, restart=restart)
+    prm = _lib.cpddg_solve_params(rel_tol=rel_tol, max_iter=max_iter, restart=restart,
+                                  profile_kernels=1 if profile else 0)
     mh = M.handle if M is not None else C.c_void_p()
     check(fn(A.handle, mh, _ptr(b), _ptr(u), C.byref(prm), C.byref(log), _stream()))
     n = min(cap, log.n_residuals)
     out = IterationLog(residuals=list(res[:n]), iterations=log.iterations, converged=bool(log.converged),
                        final_true_residual=log.final_true_residual, device_seconds=log.seconds,
                        kernel_launches=log.kernel_launches)
+    out.kernel_times = dict(pc_seconds=log.pc_seconds, pc_launches=log.pc_launches,
+                            op_seconds=log.op_seconds, op_launches=log.op_launches)
     out.timings.solve = log.seconds
     return SolveResult(u, out)
 
 
 def gmres_solve(A: DeviceHelmholtz, b, M: SchwarzPreconditioner | None, rel_tol: float, max_iter: int,
-                restart: int = 0) -> SolveResult:
+                restart: int = 0, profile: bool = False) -> SolveResult:
     """Right-preconditioned restarted GMRES (solve.hpp:128-214)."""
-    return _solve(lib().cpddg_gmres, A, b, M, rel_tol, max_iter, restart, max_iter + 2)
+    return _solve(lib().cpddg_gmres, A, b, M, rel_tol, max_iter, restart, max_iter + 2, profile)
 
 
 def stationary_solve(A: DeviceHelmholtz, b, M: SchwarzPreconditioner, rel_tol: float,
-                     max_iter: int) -> SolveResult:
+                     max_iter: int, profile: bool = False) -> SolveResult:
     """Stationary Schwarz iteration u <- u + M^-1 (b - A u) (solve.hpp:95-123)."""
-    return _solve(lib().cpddg_stationary, A, b, M, rel_tol, max_iter, 0, max_iter + 2)
+    return _solve(lib().cpddg_stationary, A, b, M, rel_tol, max_iter, 0, max_iter + 2, profile)
 
 
 def effective_max_iter(mode: str, max_iter: int) -> int:

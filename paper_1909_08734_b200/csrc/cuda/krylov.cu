@@ -117,16 +117,92 @@ struct Timer {
     }
 };
 
+/** Optional per-launch CUDA-event timing of the preconditioner and operator
+ *  applies (events recorded around each launch on the solve stream; the
+ *  elapsed times are collected at the per-iteration host synchronisation). */
+struct KernelTimer {
+    bool on = false;
+    cudaStream_t st = nullptr;
+    std::vector<cudaEvent_t> pool;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pc_pending, op_pending;
+    double pc_s = 0, op_s = 0;
+    std::int64_t pc_n = 0, op_n = 0;
+    std::size_t used = 0;
+    cudaEvent_t ev() {
+        if (used == pool.size()) {
+            cudaEvent_t e;
+            CPDDG_CUDA(cudaEventCreate(&e));
+            pool.push_back(e);
+        }
+        return pool[used++];
+    }
+    template <class F>
+    void time(bool is_pc, F&& f) {
+        if (!on) {
+            f();
+            return;
+        }
+        cudaEvent_t a = ev(), b = ev();
+        CPDDG_CUDA(cudaEventRecord(a, st));
+        f();
+        CPDDG_CUDA(cudaEventRecord(b, st));
+        (is_pc ? pc_pending : op_pending).emplace_back(a, b);
+    }
+    /** Call after a stream synchronisation. */
+    void collect() {
+        if (!on) return;
+        for (auto& [a, b] : pc_pending) {
+            float ms = 0;
+            CPDDG_CUDA(cudaEventElapsedTime(&ms, a, b));
+            pc_s += ms * 1e-3;
+            ++pc_n;
+        }
+        for (auto& [a, b] : op_pending) {
+            float ms = 0;
+            CPDDG_CUDA(cudaEventElapsedTime(&ms, a, b));
+            op_s += ms * 1e-3;
+            ++op_n;
+        }
+        pc_pending.clear();
+        op_pending.clear();
+        used = 0;
+    }
+    ~KernelTimer() {
+        for (auto e : pool) cudaEventDestroy(e);
+    }
+};
+
 struct Workspace {
     int n;
     cudaStream_t st;
     int grid;
-    ReduceWork red;
-    DevBuf<double> scal;  // device scalars: [0..cap) h, plus norms
+    KrylovCache& kc;
+    ReduceWork& red;
     std::int64_t launches = 0;
-    Workspace(int n_, cudaStream_t s) : n(n_), st(s) {
+    Workspace(int n_, cudaStream_t s, KrylovCache& c) : n(n_), st(s), kc(c), red(c.red) {
         grid = reduction_blocks();
         red.ensure(2);
+        auto need = [&](DevBuf<double>& b, std::size_t cnt) {
+            if (b.size() < cnt) b.alloc(cnt);
+        };
+        need(kc.w, static_cast<std::size_t>(n));
+        need(kc.r, static_cast<std::size_t>(n));
+        need(kc.tmp, static_cast<std::size_t>(n));
+    }
+    /** Scalar slots and pinned host scratch for `cap` Hessenberg entries. */
+    void reserve(int cap) {
+        if (kc.scal.size() < static_cast<std::size_t>(cap) + 4) kc.scal.alloc(static_cast<std::size_t>(cap) + 4);
+        if (kc.yd.size() < static_cast<std::size_t>(cap)) kc.yd.alloc(static_cast<std::size_t>(cap));
+        if (kc.vptr.size() < static_cast<std::size_t>(cap)) kc.vptr.alloc(static_cast<std::size_t>(cap));
+        if (kc.host_cap < cap + 4) {
+            if (kc.host) cudaFreeHost(kc.host);
+            CPDDG_CUDA(cudaMallocHost(&kc.host, sizeof(double) * (cap + 4)));
+            kc.host_cap = cap + 4;
+        }
+    }
+    double* basis(int k) {
+        while (static_cast<int>(kc.V.size()) <= k) kc.V.emplace_back(static_cast<std::size_t>(n));
+        return kc.V[static_cast<std::size_t>(k)].get();
     }
     /** out = (vnext ? vnext . w : w . w) after the optional update. */
     void mgs(const double* hprev, const double* vprev, double* w, const double* vnext, double* out,
@@ -144,8 +220,14 @@ struct Workspace {
 };
 
 void record(cpddg_log* log, const std::vector<double>& res, int iters, bool conv, double final_true, double secs,
-            std::int64_t launches) {
+            std::int64_t launches, const KernelTimer* kt = nullptr) {
     if (!log) return;
+    if (kt) {
+        log->pc_seconds = kt->pc_s;
+        log->pc_launches = kt->pc_n;
+        log->op_seconds = kt->op_s;
+        log->op_launches = kt->op_n;
+    }
     log->n_residuals = static_cast<int>(res.size());
     if (log->residuals)
         for (int k = 0; k < std::min(log->capacity, log->n_residuals); ++k) log->residuals[k] = res[static_cast<std::size_t>(k)];
@@ -165,22 +247,25 @@ static void gmres(cpddg_op* op, cpddg_pc* pc, const double* b, double* u, const 
     if (pc && pc->n_global != n) throw InternalError("preconditioner size does not match the operator");
     const int max_iter = prm.max_iter;
     const int cycle = prm.restart > 0 ? prm.restart : max_iter;
-    Workspace ws(n, st);
-    const int cap = std::max(cycle, 1) + 2;
-    ws.scal.alloc(static_cast<std::size_t>(cap) + 4);
-    double* hd = ws.scal.get();      // h[0..m+1]
+    Workspace ws(n, st, op->kc);
+    const int cap = std::max(std::min(cycle, max_iter), 1) + 2;
+    ws.reserve(cap);
+    double* hd = ws.kc.scal.get();   // h[0..m+1]
     double* nd = hd + cap;           // [0] ||w0||^2, [1] ||r||^2
-    Pinned hh(static_cast<std::size_t>(cap) + 4);
-    DevBuf<double> w(static_cast<std::size_t>(n)), r(static_cast<std::size_t>(n)), tmp(static_cast<std::size_t>(n));
-    std::vector<DevBuf<double>> V;
-    auto basis = [&](int k) -> double* {
-        while (static_cast<int>(V.size()) <= k) V.emplace_back(static_cast<std::size_t>(n));
-        return V[static_cast<std::size_t>(k)].get();
-    };
-    DevBuf<const double*> vptr(static_cast<std::size_t>(cap));
-    DevBuf<double> yd(static_cast<std::size_t>(cap));
+    struct {
+        double* p;
+    } hh{ws.kc.host};
+    DevBuf<double>& w = ws.kc.w;
+    DevBuf<double>& r = ws.kc.r;
+    DevBuf<double>& tmp = ws.kc.tmp;
+    auto basis = [&](int k) { return ws.basis(k); };
+    DevBuf<const double*>& vptr = ws.kc.vptr;
+    DevBuf<double>& yd = ws.kc.yd;
     std::vector<const double*> vptr_h(static_cast<std::size_t>(cap));
 
+    KernelTimer kt;
+    kt.on = prm.profile_kernels != 0;
+    kt.st = st;
     Timer timer(st);
     CPDDG_CUDA(cudaMemsetAsync(u, 0, sizeof(double) * n, st));
     CPDDG_CUDA(cudaMemcpyAsync(r.get(), b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
@@ -215,11 +300,11 @@ static void gmres(cpddg_op* op, cpddg_pc* pc, const double* b, double* u, const 
         while (m < cycle && total < max_iter) {
             const double* z = basis(m);
             if (pc) {
-                pc_apply(pc, basis(m), tmp.get(), false, st);
+                kt.time(true, [&] { pc_apply(pc, basis(m), tmp.get(), false, st); });
                 ++ws.launches;
                 z = tmp.get();
             }
-            op_apply(op, z, w.get(), st);
+            kt.time(false, [&] { op_apply(op, z, w.get(), st); });
             ws.launches += 2;
             // MGS: pass 0 also yields ||w||^2 before orthogonalisation
             ws.mgs(nullptr, nullptr, w.get(), basis(0), hd + 0, nd + 0);
@@ -228,6 +313,7 @@ static void gmres(cpddg_op* op, cpddg_pc* pc, const double* b, double* u, const 
             CPDDG_CUDA(cudaMemcpyAsync(hh.p, hd, sizeof(double) * (m + 2), cudaMemcpyDeviceToHost, st));
             CPDDG_CUDA(cudaMemcpyAsync(hh.p + cap, nd, sizeof(double), cudaMemcpyDeviceToHost, st));
             CPDDG_CUDA(cudaStreamSynchronize(st));
+            kt.collect();
             std::vector<double> h(hh.p, hh.p + m + 2);
             h[static_cast<std::size_t>(m) + 1] = std::sqrt(h[static_cast<std::size_t>(m) + 1]);
             const double wnorm0 = std::sqrt(hh.p[cap]);
@@ -276,7 +362,7 @@ static void gmres(cpddg_op* op, cpddg_pc* pc, const double* b, double* u, const 
             CPDDG_CUDA(cudaGetLastError());
             ++ws.launches;
             if (pc) {
-                pc_apply(pc, tmp.get(), u, true, st);
+                kt.time(true, [&] { pc_apply(pc, tmp.get(), u, true, st); });
             } else {
                 k_axpy1<<<ws.grid, kRedThreads, 0, st>>>(n, tmp.get(), u);
                 CPDDG_CUDA(cudaGetLastError());
@@ -285,13 +371,16 @@ static void gmres(cpddg_op* op, cpddg_pc* pc, const double* b, double* u, const 
             // keep the host copy of y alive until the transfer completed
             CPDDG_CUDA(cudaStreamSynchronize(st));
         }
-        op_residual(op, b, u, r.get(), nd + 1, st);
+        kt.time(false, [&] { op_residual(op, b, u, r.get(), nd + 1, st); });
         ws.launches += 2;
         fetch(nd + 1, 1);
+        kt.collect();
         rnorm = std::sqrt(hh.p[0]);
     }
     // final_true_residual = ||b - A u|| (solve.hpp:212): r was just recomputed from u
-    record(log, residuals, total, converged, rnorm, timer.stop(), ws.launches);
+    const double secs = timer.stop();
+    kt.collect();
+    record(log, residuals, total, converged, rnorm, secs, ws.launches, &kt);
 }
 
 // solve.hpp:95-123
@@ -300,15 +389,20 @@ static void stationary(cpddg_op* op, cpddg_pc* pc, const double* b, double* u, c
     const int n = op->na;
     if (!pc) throw InternalError("stationary iteration needs a preconditioner");
     if (pc->n_global != n) throw InternalError("preconditioner size does not match the operator");
-    Workspace ws(n, st);
-    ws.scal.alloc(2);
-    Pinned hh(2);
-    DevBuf<double> r(static_cast<std::size_t>(n));
+    Workspace ws(n, st, op->kc);
+    ws.reserve(2);
+    struct {
+        double* p;
+    } hh{ws.kc.host};
+    DevBuf<double>& r = ws.kc.r;
+    KernelTimer kt;
+    kt.on = prm.profile_kernels != 0;
+    kt.st = st;
     Timer timer(st);
     CPDDG_CUDA(cudaMemsetAsync(u, 0, sizeof(double) * n, st));
     CPDDG_CUDA(cudaMemcpyAsync(r.get(), b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
-    ws.mgs(nullptr, nullptr, r.get(), nullptr, ws.scal.get(), nullptr);
-    CPDDG_CUDA(cudaMemcpyAsync(hh.p, ws.scal.get(), sizeof(double), cudaMemcpyDeviceToHost, st));
+    ws.mgs(nullptr, nullptr, r.get(), nullptr, ws.kc.scal.get(), nullptr);
+    CPDDG_CUDA(cudaMemcpyAsync(hh.p, ws.kc.scal.get(), sizeof(double), cudaMemcpyDeviceToHost, st));
     CPDDG_CUDA(cudaStreamSynchronize(st));
     const double r0 = std::sqrt(hh.p[0]);
     std::vector<double> residuals{r0};
@@ -320,11 +414,12 @@ static void stationary(cpddg_op* op, cpddg_pc* pc, const double* b, double* u, c
     int iters = 0;
     double rn = r0;
     for (int it = 1; it <= prm.max_iter; ++it) {
-        pc_apply(pc, r.get(), u, true, st);
-        op_residual(op, b, u, r.get(), ws.scal.get(), st);
+        kt.time(true, [&] { pc_apply(pc, r.get(), u, true, st); });
+        kt.time(false, [&] { op_residual(op, b, u, r.get(), ws.kc.scal.get(), st); });
         ws.launches += 3;
-        CPDDG_CUDA(cudaMemcpyAsync(hh.p, ws.scal.get(), sizeof(double), cudaMemcpyDeviceToHost, st));
+        CPDDG_CUDA(cudaMemcpyAsync(hh.p, ws.kc.scal.get(), sizeof(double), cudaMemcpyDeviceToHost, st));
         CPDDG_CUDA(cudaStreamSynchronize(st));
+        kt.collect();
         rn = std::sqrt(hh.p[0]);
         check_finite(rn, "stationary residual");
         residuals.push_back(rn);
@@ -335,7 +430,9 @@ static void stationary(cpddg_op* op, cpddg_pc* pc, const double* b, double* u, c
             break;
         }
     }
-    record(log, residuals, iters, converged, rn, timer.stop(), ws.launches);
+    const double secs = timer.stop();
+    kt.collect();
+    record(log, residuals, iters, converged, rn, secs, ws.launches, &kt);
 }
 
 }  // namespace cpddg

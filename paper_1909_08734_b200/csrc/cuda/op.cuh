@@ -7,6 +7,20 @@
 #include <cstdint>
 #include <vector>
 
+/** Persistent Krylov workspace (allocated once per operator, reused by every
+ *  solve: no cudaMalloc / cudaFree inside a timed solve). */
+struct KrylovCache {
+    std::vector<cpddg::DevBuf<double>> V;
+    cpddg::DevBuf<double> w, r, tmp, yd, scal;
+    cpddg::DevBuf<const double*> vptr;
+    double* host = nullptr;  // pinned scratch
+    int host_cap = 0;
+    cpddg::ReduceWork red;
+    ~KrylovCache() {
+        if (host) cudaFreeHost(host);
+    }
+};
+
 struct cpddg_op {
     int dim = 0, p = 0, na = 0, ng = 0, nlines = 0;
     double h = 0, c = 0, cg = 0, ih2 = 0;
@@ -17,6 +31,7 @@ struct cpddg_op {
     cpddg::DevBuf<double> rn2;  // scalar slot for ||b - A x||^2
     cpddg::ReduceWork red;
     std::int64_t alg_bytes = 0, streamed_bytes = 0;
+    KrylovCache kc;
 };
 
 /** Envelope (profile) LU factors of every subdomain system, batched. */
@@ -36,9 +51,17 @@ struct cpddg_pc {
     cpddg::DevBuf<int> gidx;           // global index gathered into row i (R_j), or -1
     cpddg::DevBuf<int> sidx;           // global index row i scatters to (owned), or -1
     cpddg::DevBuf<double> diag;        // U_ii
+    cpddg::DevBuf<double> dinv;        // 1 / U_ii (the solve multiplies)
     // per envelope entry
     cpddg::DevBuf<double> L;           // L_ij, j in [f_i, i), row-contiguous
-    cpddg::DevBuf<double> U;           // U_ji (column i of U), j in [f_i, i), contiguous
+    cpddg::DevBuf<double> U;           // factorisation: U_ji (column i of U) over [f_i, i);
+                                       // solve: reversed rows of U (see k_reverse_u)
+    // reversed-U tables for the backward solve
+    cpddg::DevBuf<std::int64_t> ubase; // [n_sub] first entry of each subdomain in U
+    cpddg::DevBuf<int> ufirst;         // per reversed row: first reversed column
+    cpddg::DevBuf<std::int64_t> uroff; // per reversed row: offset inside the subdomain's U
+    cpddg::DevBuf<double> drev;        // diagonal in reversed order
+    std::int64_t u_entries = 0;
     std::int64_t factor_bytes = 0, alg_bytes = 0;
     double factor_seconds = 0, analyse_seconds = 0, max_probe_residual = -1;
     int solve_smem = 0;

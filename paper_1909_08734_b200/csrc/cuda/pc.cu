@@ -157,8 +157,16 @@ HostSub analyse(const cpddg_local_desc& d, int n_global) {
         for (int w : adj[static_cast<std::size_t>(o)]) f = std::min(f, inv[static_cast<std::size_t>(w)]);
         S.first[static_cast<std::size_t>(i)] = f;
     }
+    // 16-byte alignment for vector loads: every row (of L) / column (of U)
+    // starts at an even column and has even length, so column pairs
+    // (2m, 2m+1) are double2-aligned.  The extra slots are structural zeros
+    // that the no-pivot factorisation never fills (they lie outside the
+    // profile), so they cost at most two stored zeros per row.
+    for (int i = 0; i < n; ++i) S.first[static_cast<std::size_t>(i)] &= ~1;
     S.roff.assign(static_cast<std::size_t>(n) + 1, 0);
-    for (int i = 0; i < n; ++i) S.roff[static_cast<std::size_t>(i) + 1] = S.roff[static_cast<std::size_t>(i)] + (i - S.first[static_cast<std::size_t>(i)]);
+    for (int i = 0; i < n; ++i)
+        S.roff[static_cast<std::size_t>(i) + 1] =
+            S.roff[static_cast<std::size_t>(i)] + ((i + (i & 1)) - S.first[static_cast<std::size_t>(i)]);
     std::vector<int> maxrow(static_cast<std::size_t>(n), -1);
     for (int i = 0; i < n; ++i) maxrow[static_cast<std::size_t>(S.first[static_cast<std::size_t>(i)])] = std::max(maxrow[static_cast<std::size_t>(S.first[static_cast<std::size_t>(i)])], i);
     S.rlast.assign(static_cast<std::size_t>(n), 0);
@@ -231,7 +239,7 @@ __global__ void __launch_bounds__(kFactorThreads) k_factor(const int* __restrict
                                                            const std::int64_t* __restrict__ roff_all,
                                                            const int* __restrict__ rlast_all,
                                                            double* diag_all, double* L_all, double* U_all,
-                                                           int* status) {
+                                                           double* dinv_all, int* status) {
     const int j = order[blockIdx.x];
     const SubPtrs S = sub_ptrs(j, n_rows, vbase, ebase, first_all, roff_all, rlast_all, diag_all, L_all, U_all);
     extern __shared__ double sm[];
@@ -438,9 +446,11 @@ __global__ void __launch_bounds__(kFactorThreads) k_factor(const int* __restrict
     }
     // pivot check: a zero or non-finite pivot is a singular factorisation
     int bad = 0;
+    double* dinv = dinv_all + vbase[j];
     for (int i = tid; i < n; i += blockDim.x) {
         const double d = S.diag[i];
         if (!(fabs(d) > 0.0) || !isfinite(d)) bad = 1;
+        dinv[i] = 1.0 / d;
     }
     bad = __syncthreads_or(bad);
     if (tid == 0) status[j] = bad;
@@ -448,109 +458,335 @@ __global__ void __launch_bounds__(kFactorThreads) k_factor(const int* __restrict
 
 // ---------------------------------------------------------------- solve
 
-constexpr int kSolveThreads = 256;
-constexpr int kSolveWarps = kSolveThreads / 32;
+constexpr int kSolveWarps = 16;
+constexpr int kSolveThreads = 32 * kSolveWarps;
+constexpr int RB = 2 * (kSolveWarps - 1);  // rows per pipelined block: 2 per panel warp
+constexpr int TS = 2 * RB + 1;             // padded stash row (previous block + own triangle)
 
-__global__ void __launch_bounds__(kSolveThreads) k_solve(const int* __restrict__ order,
-                                                         const int* __restrict__ n_rows,
-                                                         const std::int64_t* __restrict__ vbase,
-                                                         const std::int64_t* __restrict__ ebase,
-                                                         const int* __restrict__ first_all,
-                                                         const std::int64_t* __restrict__ roff_all,
-                                                         const double* __restrict__ diag_all,
-                                                         const double* __restrict__ L_all,
-                                                         const double* __restrict__ U_all,
-                                                         const int* __restrict__ gidx_all,
-                                                         const int* __restrict__ sidx_all,
-                                                         const double* __restrict__ r, double* z,
-                                                         int accumulate) {
+/** Convert U from column profile storage (factorisation layout) to the
+ *  reversed row layout the solve streams: reversed row i' = n-1-i holds
+ *  U(i, j) for j in (i, rlast_i] at reversed column j' = n-1-j, i.e. the
+ *  backward substitution becomes a forward one on the reversed system. */
+__global__ void __launch_bounds__(256) k_reverse_u(const int* __restrict__ order, const int* __restrict__ n_rows,
+                                                   const std::int64_t* __restrict__ vbase,
+                                                   const std::int64_t* __restrict__ ebase,
+                                                   const std::int64_t* __restrict__ ubase,
+                                                   const int* __restrict__ first_all,
+                                                   const std::int64_t* __restrict__ roff_all,
+                                                   const int* __restrict__ rlast_all,
+                                                   const std::int64_t* __restrict__ uroff_all,
+                                                   const double* __restrict__ diag_all,
+                                                   const double* __restrict__ Ucol_all, double* __restrict__ Urev_all,
+                                                   double* __restrict__ drev_all) {
     const int j = order[blockIdx.x];
     const int n = n_rows[j];
-    const std::int64_t vb = vbase[j], eb = ebase[j];
+    const std::int64_t vb = vbase[j];
     const int* first = first_all + vb;
     const std::int64_t* roff = roff_all + vb;
-    const double* diag = diag_all + vb;
-    const double* L = L_all + eb;
-    const double* U = U_all + eb;
+    const int* rlast = rlast_all + vb;
+    const std::int64_t* uroff = uroff_all + vb;
+    const double* Ucol = Ucol_all + ebase[j];
+    double* Urev = Urev_all + ubase[j];
+    for (int ip = threadIdx.x; ip < n; ip += blockDim.x) {
+        const int i = n - 1 - ip;
+        drev_all[vb + ip] = diag_all[vb + i];
+        const int fpr = n - 1 - rlast[i];
+        double* out = Urev + uroff[ip] - fpr;
+        for (int jp = fpr; jp < ip; ++jp) {
+            const int c = n - 1 - jp;
+            const int fc = first[c];
+            out[jp] = i >= fc ? Ucol[roff[c] + i - fc] : 0.0;
+        }
+    }
+}
+
+/** Prefetch [p, p + bytes) into L2 with the bulk-copy engine
+ *  (cp.async.bulk.prefetch.L2; p and bytes 16-byte aligned). */
+__device__ __forceinline__ void prefetch_l2(const void* p, long long bytes) {
+    const char* c = static_cast<const char*>(p);
+    while (bytes > 0) {
+        const unsigned b = static_cast<unsigned>(bytes < 65536 ? bytes : 65536);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(c), "r"(b) : "memory");
+        c += b;
+        bytes -= b;
+    }
+}
+
+/** L2 prefetch of the contiguous storage of rows [b, e) (L) or columns
+ *  [b, e) (U): row i occupies [ro_i, ro_i + (i + (i & 1)) - f_i). */
+__device__ __noinline__ void prefetch_rows(const double* V, const int* f, const std::int64_t* ro, int b, int e) {
+    if (b >= e) return;
+    const std::int64_t lo = ro[b];
+    const int l = e - 1;
+    const std::int64_t hi = ro[l] + (l + (l & 1)) - f[l];
+    if (hi > lo) prefetch_l2(V + lo, (hi - lo) * 8);
+}
+
+/** Pipelined blocked lower-triangular solve y <- T^{-1} y in shared memory,
+ *  T unit lower (d == nullptr) or lower with diagonal d.  Row i of T holds
+ *  columns [f_i, i) contiguously at V + ro[i].  Blocks of RB rows: while warp
+ *  0 solves the RB x RB triangle of block k, warps 1..15 stream block k+1's
+ *  rows (two rows each, 8 loads in flight per lane, streaming cache hints)
+ *  into a partial dot over the already-final columns and stash the entries
+ *  that fall in blocks k and k+1; one barrier per block. */
+__device__ __forceinline__ void lower_solve(int n, const int* __restrict__ f, const std::int64_t* __restrict__ ro,
+                                            const double* __restrict__ V, const double* __restrict__ d,
+                                            double* y, double (*part)[RB + 2], double (*tri)[RB][TS]) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nblk = (n + RB - 1) / RB;
+    auto panel = [&](int b0, int buf) {
+        const int lim = b0 - RB;  // columns < lim are final
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int rr = 2 * (warp - 1) + q;
+            const int i = b0 + rr;
+            double s = 0.0;
+            if (i < n) {
+                const int fi = __ldg(f + i);
+                const double* Li = V + (__ldg(ro + i) - fi);
+                // stash loads first: they share the round trip of the partial loads
+                const int col0 = lim + lane, col1 = lim + lane + 32;
+                const double t0 = (col0 >= fi && col0 < i) ? __ldcs(Li + col0) : 0.0;
+                const double t1 = (lane + 32 < 2 * RB && col1 >= fi && col1 < i) ? __ldcs(Li + col1) : 0.0;
+                double s1 = 0.0, s2 = 0.0, s3 = 0.0;
+                const double2* Li2 = reinterpret_cast<const double2*>(Li + fi);  // fi even, row 16B-aligned
+                const double2* y2 = reinterpret_cast<const double2*>(y);
+                for (int base = fi; base < lim; base += 512) {
+                    double2 a[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int c = base + 2 * lane + 64 * u;
+                        a[u] = c < lim ? __ldcs(Li2 + ((c - fi) >> 1)) : make_double2(0.0, 0.0);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; u += 2) {
+                        const int c = base + 2 * lane + 64 * u;
+                        if (c < lim) {
+                            const double2 yy = y2[c >> 1];
+                            s = fma(a[u].x, yy.x, s);
+                            s1 = fma(a[u].y, yy.y, s1);
+                        }
+                        if (c + 64 < lim) {
+                            const double2 yy = y2[(c + 64) >> 1];
+                            s2 = fma(a[u + 1].x, yy.x, s2);
+                            s3 = fma(a[u + 1].y, yy.y, s3);
+                        }
+                    }
+                }
+                s = (s + s1) + (s2 + s3);
+                tri[buf][rr][lane] = t0;
+                if (lane + 32 < 2 * RB) tri[buf][rr][lane + 32] = t1;
+            } else {
+                for (int cc = lane; cc < 2 * RB; cc += 32) tri[buf][rr][cc] = 0.0;
+            }
+            s = warp_sum(s);
+            if (lane == 0) part[buf][rr] = s;
+        }
+    };
+    // rows of a block are contiguous in V: stream them into L2 two blocks ahead
+    auto prefetch_block = [&](int k) {
+        if (k < nblk) prefetch_rows(V, f, ro, k * RB, min(n, k * RB + RB));
+    };
+    if (threadIdx.x == 32) {
+        prefetch_block(0);
+        prefetch_block(1);
+    }
+    if (warp > 0) panel(0, 0);
+    __syncthreads();
+    for (int k = 0; k < nblk; ++k) {
+        const int cur = k & 1;
+        const int r0 = k * RB;
+        if (threadIdx.x == 32) prefetch_block(k + 2);
+        if (warp == 0) {
+            const int i = r0 + lane;
+            const bool live = lane < RB && i < n;
+            double s = 0.0;
+            if (live) {
+                s = y[i] - part[cur][lane];
+                if (r0 >= RB) {
+#pragma unroll 6
+                    for (int c = 0; c < RB; ++c) s = fma(-tri[cur][lane][c], y[r0 - RB + c], s);
+                }
+            }
+            const int rb = min(RB, n - r0);
+            for (int c = 0; c < rb; ++c) {
+                if (d && lane == c) s = s / __ldg(d + r0 + c);
+                const double xc = __shfl_sync(0xffffffffu, s, c);
+                if (lane > c && live) s = fma(-tri[cur][lane][RB + c], xc, s);
+            }
+            if (live) y[i] = s;
+        } else if (k + 1 < nblk) {
+            panel((k + 1) * RB, cur ^ 1);
+        }
+        __syncthreads();
+    }
+}
+
+/** Pipelined blocked backward substitution U x = y with U stored by columns
+ *  (column c holds rows [f_c, c) contiguously at V + ro[c]; diagonal d).
+ *  Blocks of RB columns from the last: while warp 0 applies block K+1's
+ *  columns to block K's rows and solves block K's triangle, warps 1..15
+ *  apply block K+1's columns to every row below block K (thread per row,
+ *  RB independent coalesced loads each) and stash the U entries block K-1's
+ *  triangle step will need; one barrier per block.  Streams each stored
+ *  entry of U exactly once. */
+__device__ __forceinline__ void upper_solve_cols(int n, const int* __restrict__ f,
+                                                 const std::int64_t* __restrict__ ro,
+                                                 const double* __restrict__ V, const double* __restrict__ d,
+                                                 double* y, double (*tri)[RB][TS], int (*cf)[RB],
+                                                 long long (*cro)[RB]) {  // cf, cro: [3][RB]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nblk = (n + RB - 1) / RB;
+    const int ptid = threadIdx.x - 32, pthreads = blockDim.x - 32;
+    // stash for block K: tri[buf][i][c] = U(c0+i, c0+c) for c in [0, 2RB) (block K, then K+1 columns)
+    // stash = load (into registers, 2 per thread since RB * 2RB <= 2 * 480)
+    // then store (after the row updates, so both share a round trip)
+    auto stash_load = [&](int K, double* v) {
+        const int c0 = K * RB;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int e = ptid + q * pthreads;
+            v[q] = 0.0;
+            if (e < RB * 2 * RB) {
+                const int il = e / (2 * RB), cl = e % (2 * RB);
+                const int i = c0 + il, col = c0 + cl;
+                if (col < n && i < col) {
+                    const int fc = __ldg(f + col);
+                    if (i >= fc) v[q] = __ldcs(V + __ldg(ro + col) + (i - fc));
+                }
+            }
+        }
+    };
+    auto stash_store = [&](const double* v, int buf) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int e = ptid + q * pthreads;
+            if (e < RB * 2 * RB) tri[buf][e / (2 * RB)][e % (2 * RB)] = v[q];
+        }
+    };
+    auto stash = [&](int K, int buf) {
+        const int c0 = K * RB;
+        double v[4];
+        stash_load(K, v);
+        stash_store(v, buf);
+        // column tables use a third buffer: block K+1's are still being read
+        // by the row updates of the step that stashes block K
+        const int cb = K % 3;
+        for (int e = ptid; e < RB; e += pthreads) {
+            const int col = c0 + e;
+            cf[cb][e] = col < n ? __ldg(f + col) : n;
+            cro[cb][e] = col < n ? __ldg(ro + col) : 0;
+        }
+    };
+    auto prefetch_block = [&](int K) {
+        if (K >= 0) prefetch_rows(V, f, ro, K * RB, min(n, K * RB + RB));
+    };
+    if (warp > 0) stash(nblk - 1, (nblk - 1) & 1);
+    __syncthreads();
+    for (int K = nblk - 1; K >= 0; --K) {
+        const int cur = K & 1;
+        const int c0 = K * RB;
+        // block K-2 columns: used by the stash of step K-1 and the row updates of step K-3
+        if (threadIdx.x == 32) prefetch_block(K - 2);
+        if (warp == 0) {
+            const int i = c0 + lane;
+            const bool live = lane < RB && i < n;
+            double s = live ? y[i] : 0.0;
+            if (live && K + 1 < nblk) {
+                const int nb1 = min(RB, n - (c0 + RB));
+#pragma unroll 6
+                for (int c = 0; c < nb1; ++c) s = fma(-tri[cur][lane][RB + c], y[c0 + RB + c], s);
+            }
+            const int cb = min(RB, n - c0);
+            const double dinv = live ? __ldg(d + c0 + lane) : 0.0;  // reciprocal pivots (k_factor)
+            for (int c = cb - 1; c >= 0; --c) {
+                if (lane == c) s *= dinv;
+                const double xc = __shfl_sync(0xffffffffu, s, c);
+                if (lane < c && live) s = fma(-tri[cur][lane][c], xc, s);
+            }
+            if (live) y[i] = s;
+        } else {
+            double sv[4];
+            if (K >= 1) stash_load(K - 1, sv);
+            if (K + 1 < nblk) {
+                // rows below block K from block K+1's columns
+                const int nxt = (K + 1) % 3;
+                const int cb1 = min(RB, n - (c0 + RB));
+                int jmin = c0;
+                for (int c = 0; c < cb1; ++c) jmin = min(jmin, cf[nxt][c]);
+                // two threads per row (adjacent lanes), 15 columns each: all
+                // loads of a thread are issued before its FMAs
+                constexpr int HC = RB / 2;
+                const int half = ptid & 1, pr = ptid >> 1, npairs = pthreads >> 1;
+                for (int base = jmin; base < c0; base += npairs) {
+                    const int jr = base + pr;
+                    const bool rowok = jr < c0;
+                    double a[HC];
+#pragma unroll
+                    for (int u = 0; u < HC; ++u) {
+                        const int c = half * HC + u;
+                        a[u] = (rowok && c < cb1 && jr >= cf[nxt][c]) ? __ldcs(V + cro[nxt][c] + (jr - cf[nxt][c])) : 0.0;
+                    }
+                    double acc = 0.0;
+#pragma unroll
+                    for (int u = 0; u < HC; ++u) {
+                        const int c = half * HC + u;
+                        if (c < cb1) acc = fma(a[u], y[c0 + RB + c], acc);
+                    }
+                    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+                    if (rowok && half == 0) y[jr] -= acc;
+                }
+            }
+            if (K >= 1) {
+                stash_store(sv, cur ^ 1);
+                // column tables of block K-1 (third buffer, see stash())
+                const int cb = (K - 1) % 3;
+                for (int e = ptid; e < RB; e += pthreads) {
+                    const int col = (K - 1) * RB + e;
+                    cf[cb][e] = col < n ? __ldg(f + col) : n;
+                    cro[cb][e] = col < n ? __ldg(ro + col) : 0;
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+template <int MODE>  // 0: full apply; 1: forward only; 2: backward only (profiling)
+__global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const int* __restrict__ order,
+                                                            const int* __restrict__ n_rows,
+                                                            const std::int64_t* __restrict__ vbase,
+                                                            const std::int64_t* __restrict__ ebase,
+                                                            const int* __restrict__ first_all,
+                                                            const std::int64_t* __restrict__ roff_all,
+                                                            const double* __restrict__ diag_all,
+                                                            const double* __restrict__ L_all,
+                                                            const double* __restrict__ U_all,
+                                                            const int* __restrict__ gidx_all,
+                                                            const int* __restrict__ sidx_all,
+                                                            const double* __restrict__ r, double* z,
+                                                            int accumulate) {
+    const int j = order[blockIdx.x];
+    const int n = n_rows[j];
+    const std::int64_t vb = vbase[j];
     extern __shared__ double y[];
-    __shared__ double part[SB];
-    __shared__ double tri[SB][SB + 1];
-    __shared__ int sf[SB];
-    __shared__ long long sro[SB];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    __shared__ double part[2][RB + 2];
+    __shared__ double tri[2][RB][TS];
+    const int tid = threadIdx.x;
 
     for (int p = tid; p < n; p += blockDim.x) {
-        const int g = gidx_all[vb + p];
+        const int g = __ldg(gidx_all + vb + p);
         y[p] = g >= 0 ? __ldg(r + g) : 0.0;
     }
     __syncthreads();
-
-    // ---- forward: L y = b (unit lower), 32-row blocks
-    for (int r0 = 0; r0 < n; r0 += SB) {
-        const int rb = min(SB, n - r0);
-        for (int rr = warp; rr < rb; rr += kSolveWarps) {
-            const int i = r0 + rr;
-            const int f = __ldg(first + i);
-            const double* Li = L + (__ldg(roff + i) - f);
-            double s = 0.0;
-            for (int c = f + lane; c < r0; c += 32) s = fma(__ldg(Li + c), y[c], s);
-            const int c = r0 + lane;
-            tri[rr][lane] = (c >= f && c < i) ? __ldg(Li + c) : 0.0;
-            s = warp_sum(s);
-            if (lane == 0) part[rr] = s;
-        }
-        __syncthreads();
-        if (warp == 0) {
-            const int i = r0 + lane;
-            double val = lane < rb ? y[i] - part[lane] : 0.0;
-            for (int k = 0; k < rb; ++k) {
-                const double xk = __shfl_sync(0xffffffffu, val, k);
-                if (lane > k) val -= tri[lane][k] * xk;
-            }
-            if (lane < rb) y[i] = val;
-        }
-        __syncthreads();
-    }
-
-    // ---- backward: U x = y, U column i stored contiguously over [f_i, i)
-    for (int c0 = ((n - 1) / SB) * SB; c0 >= 0; c0 -= SB) {
-        const int cb = min(SB, n - c0);
-        if (tid < SB) {
-            sf[tid] = tid < cb ? __ldg(first + c0 + tid) : c0 + SB;
-            sro[tid] = tid < cb ? __ldg(roff + c0 + tid) : 0;
-        }
-        __syncthreads();
-        for (int e = tid; e < SB * SB; e += blockDim.x) {
-            const int kk = e / SB, t = e % SB;  // tri[kk][t] = U(c0+t, c0+kk)
-            double v = 0.0;
-            if (kk < cb && t < kk && c0 + t >= sf[kk]) v = __ldg(U + sro[kk] + (c0 + t - sf[kk]));
-            tri[kk][t] = v;
-        }
-        __syncthreads();
-        if (warp == 0) {
-            double val = lane < cb ? y[c0 + lane] : 0.0;
-            for (int kk = cb - 1; kk >= 0; --kk) {
-                if (lane == kk) val = val / __ldg(diag + c0 + kk);
-                const double xk = __shfl_sync(0xffffffffu, val, kk);
-                if (lane < kk) val -= tri[kk][lane] * xk;
-            }
-            if (lane < cb) y[c0 + lane] = val;
-        }
-        __syncthreads();
-        int fmin = c0;
-        for (int kk = 0; kk < cb; ++kk) fmin = min(fmin, sf[kk]);
-        for (int jc = fmin + tid; jc < c0; jc += blockDim.x) {
-            double acc = 0.0;
-#pragma unroll 8
-            for (int kk = 0; kk < cb; ++kk)
-                if (jc >= sf[kk]) acc = fma(__ldg(U + sro[kk] + (jc - sf[kk])), y[c0 + kk], acc);
-            y[jc] -= acc;
-        }
-        __syncthreads();
-    }
-
+    // forward: L y = b (unit lower)
+    if (MODE != 2) lower_solve(n, first_all + vb, roff_all + vb, L_all + ebase[j], nullptr, y, part, tri);
+    // backward: U x = y, column-oriented on the factorisation's U layout
+    __shared__ int cf[3][RB];
+    __shared__ long long cro[3][RB];
+    if (MODE != 1) upper_solve_cols(n, first_all + vb, roff_all + vb, U_all + ebase[j], diag_all + vb, y, tri, cf, cro);
     for (int p = tid; p < n; p += blockDim.x) {
-        const int s = sidx_all[vb + p];
+        const int s = __ldg(sidx_all + vb + p);
         if (s >= 0) z[s] = accumulate ? z[s] + y[p] : y[p];
     }
 }
@@ -562,11 +798,16 @@ void append(std::vector<T>& dst, const std::vector<T>& src) {
 
 }  // namespace
 
-void pc_apply(const cpddg_pc* pc, const double* r, double* z, bool accumulate, cudaStream_t st) {
-    k_solve<<<pc->n_sub, kSolveThreads, pc->solve_smem, st>>>(
+void pc_apply_mode(const cpddg_pc* pc, const double* r, double* z, bool accumulate, int mode, cudaStream_t st) {
+    auto kern = mode == 1 ? k_solve<1> : mode == 2 ? k_solve<2> : k_solve<0>;
+    kern<<<pc->n_sub, kSolveThreads, pc->solve_smem, st>>>(
         pc->order.get(), pc->n_rows.get(), pc->vbase.get(), pc->ebase.get(), pc->first.get(), pc->roff.get(),
-        pc->diag.get(), pc->L.get(), pc->U.get(), pc->gidx.get(), pc->sidx.get(), r, z, accumulate ? 1 : 0);
+        pc->dinv.get(), pc->L.get(), pc->U.get(), pc->gidx.get(), pc->sidx.get(), r, z, accumulate ? 1 : 0);
     CPDDG_CUDA(cudaGetLastError());
+}
+
+void pc_apply(const cpddg_pc* pc, const double* r, double* z, bool accumulate, cudaStream_t st) {
+    pc_apply_mode(pc, r, z, accumulate, 0, st);
 }
 
 static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* locals, const cpddg_pc_options* opt) {
@@ -643,13 +884,14 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
     CPDDG_CUDA(cudaFuncSetAttribute(k_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm));
     DevBuf<int> status(static_cast<std::size_t>(n_sub));
     status.zero();
+    pc->dinv.alloc(static_cast<std::size_t>(vb));
     cudaEvent_t e0, e1;
     CPDDG_CUDA(cudaEventCreate(&e0));
     CPDDG_CUDA(cudaEventCreate(&e1));
     CPDDG_CUDA(cudaEventRecord(e0));
     k_factor<<<n_sub, kFactorThreads, fsm>>>(pc->order.get(), pc->n_rows.get(), pc->vbase.get(), pc->ebase.get(),
                                            pc->first.get(), pc->roff.get(), pc->rlast.get(), pc->diag.get(),
-                                           pc->L.get(), pc->U.get(), status.get());
+                                           pc->L.get(), pc->U.get(), pc->dinv.get(), status.get());
     CPDDG_CUDA(cudaGetLastError());
     CPDDG_CUDA(cudaEventRecord(e1));
     CPDDG_CUDA(cudaEventSynchronize(e1));
@@ -663,11 +905,16 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
     for (int j = 0; j < n_sub; ++j)
         if (st[static_cast<std::size_t>(j)]) throw DivergenceError("singular factorization of subdomain " + std::to_string(j));
 
+    pc->u_entries = ebs;
+    pc->entries = ebs + pc->u_entries + vb;
     pc->solve_smem = static_cast<int>(sizeof(double)) * pc->max_rows;
     if (pc->solve_smem > 200 * 1024) throw ConfigError("subdomain system too large for the shared-memory solve");
-    CPDDG_CUDA(cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(pc->solve_smem, 1)));
+    for (auto kern : {k_solve<0>, k_solve<1>, k_solve<2>})
+        CPDDG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(pc->solve_smem, 1)));
     // bytes one apply streams: L, U, diag, first, roff per row, gather/scatter maps, r gathers, z writes
-    pc->factor_bytes = 16 * ebs + 8 * vb;
+    // streamed per apply: L and reversed-U values, diagonal, and the per-row
+    // tables (first + offset) of both passes
+    pc->factor_bytes = 8 * (ebs + pc->u_entries + vb) + 2 * 12 * vb;
     std::int64_t gathers = 0, scatters = 0;
     for (int g : gidx) gathers += g >= 0 ? 1 : 0;
     for (int s : sidx) scatters += s >= 0 ? 1 : 0;
@@ -733,6 +980,15 @@ int cpddg_pc_stats_get(const cpddg_pc* pc, cpddg_pc_stats* st) {
         st->factor_seconds = pc->factor_seconds;
         st->analyse_seconds = pc->analyse_seconds;
         st->max_probe_residual = pc->max_probe_residual;
+    });
+}
+
+/** Development hook: time one pass of the preconditioner (mode 1 forward,
+ *  2 backward, 0 both).  Not part of include/cpddg.h. */
+int cpddg_pc_apply_mode(cpddg_pc* pc, const double* r, double* z, int mode, void* stream) {
+    return guarded([&] {
+        if (!pc || !r || !z) throw InternalError("null argument");
+        pc_apply_mode(pc, r, z, false, mode, static_cast<cudaStream_t>(stream));
     });
 }
 

@@ -15,7 +15,13 @@ st = M.stats()
 print(f"N_A={P.n_active} setup {t1-t0:.1f}s decomp {t2-t1:.1f}s op+pc {t3-t2:.1f}s  pc: {st}", flush=True)
 b = torch.from_numpy(inputs.rhs_sphere(P.active_cp)).cuda()
 x = torch.rand(P.n_active, dtype=torch.float64, device="cuda")
-for name, f in [("op", lambda: A.apply(x)), ("pc", lambda: M.apply(x))]:
+import ctypes as C
+from paper_1909_08734_b200 import _lib
+L = _lib.lib(); L.cpddg_pc_apply_mode.argtypes = [C.c_void_p]*3 + [C.c_int, C.c_void_p]
+z = torch.empty_like(x)
+def mode(m):
+    return lambda: L.cpddg_pc_apply_mode(M.handle, C.c_void_p(x.data_ptr()), C.c_void_p(z.data_ptr()), m, C.c_void_p(torch.cuda.current_stream().cuda_stream))
+for name, f in [("op", lambda: A.apply(x)), ("pc", lambda: M.apply(x)), ("pc_fwd", mode(1)), ("pc_bwd", mode(2))]:
     for _ in range(3): f()
     torch.cuda.synchronize(); e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -24,6 +30,9 @@ for name, f in [("op", lambda: A.apply(x)), ("pc", lambda: M.apply(x))]:
     print(f"{name}: {ms:.3f} ms", flush=True)
 a_alg, a_str = A.bytes()
 print(f"op alg bytes {a_alg/1e6:.1f} MB streamed {a_str/1e6:.1f} MB; pc bytes {st['factor_bytes']/1e9:.2f} GB")
+for prof in (False, True, False, True):
+    r2 = api.gmres_solve(A, b, M, 1e-10, 2000, 50, profile=prof)
+    print(f"  gmres profile={prof}: t {r2.log.device_seconds:.3f}s kt={r2.log.kernel_times}")
 res = api.gmres_solve(A, b, M, 1e-10, 2000, 50)
 print(f"gmres: iters {res.log.iterations} conv {res.log.converged} t {res.log.device_seconds:.3f}s launches {res.log.kernel_launches} final rel {res.log.final_true_residual/float(b.norm()):.3e}")
 print(f"DOF.iters/s = {P.n_active*res.log.iterations/res.log.device_seconds:.3e}")
