@@ -83,10 +83,11 @@ enum { CPDDG_RAS = 0, CPDDG_ORAS = 1 };
 /** Partition (validated as load_partition, partition.hpp:519-552), then
  *  align_interfaces (partition.hpp:474-508), build_subdomains
  *  (subdomain.hpp:153-313) and assemble_local for every subdomain
- *  (transmission.hpp:73-138, factor = false).  alpha_cross < 0 means alpha
+ *  (transmission.hpp:73-138, factor = false).  n_part must equal n_active
+ *  (ConfigError otherwise, as load_partition).  alpha_cross < 0 means alpha
  *  (SolverConfig::effective_alpha_cross, solve.hpp:38).  part_out (may be
  *  NULL) receives the aligned labels, moves the alignment move count. */
-int cpddg_setup_decompose(cpddg_setup* s, const int32_t* part, int n_overlap, int method,
+int cpddg_setup_decompose(cpddg_setup* s, const int32_t* part, int n_part, int n_overlap, int method,
                           double alpha, double alpha_cross, int32_t* part_out, int* moves);
 int cpddg_setup_n_subdomains(const cpddg_setup* s);
 /** counts[8] = |disjoint|, |overlap|, |final_layer|, |ghosts|, |bc|,

@@ -74,7 +74,7 @@ _SIGS = {
                                     C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "cpddg_setup_band": (C.c_int, [_vp, _i32p, _f64p, _f64p, _f64p]),
     "cpddg_setup_csr": (C.c_int, [_vp, C.c_int, _i64p, _i32p, _f64p]),
-    "cpddg_setup_decompose": (C.c_int, [_vp, _i32p, C.c_int, C.c_int, C.c_double, C.c_double,
+    "cpddg_setup_decompose": (C.c_int, [_vp, _i32p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                         _i32p, C.POINTER(C.c_int)]),
     "cpddg_setup_n_subdomains": (C.c_int, [_vp]),
     "cpddg_setup_subdomain_counts": (C.c_int, [_vp, C.c_int, _i32p]),

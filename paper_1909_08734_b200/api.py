@@ -127,7 +127,7 @@ class Problem:
         out = np.zeros(self.n_active, np.int32)
         moves = C.c_int()
         t0 = time.perf_counter()
-        check(lib().cpddg_setup_decompose(self._h, part, int(n_overlap), METHODS[method], float(alpha),
+        check(lib().cpddg_setup_decompose(self._h, part, int(part.size), int(n_overlap), METHODS[method], float(alpha),
                                           float(alpha_cross), out, C.byref(moves)))
         self.timings["decompose"] = time.perf_counter() - t0
         self.n_sub = lib().cpddg_setup_n_subdomains(self._h)

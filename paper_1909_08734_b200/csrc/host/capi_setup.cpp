@@ -57,10 +57,13 @@ void create_impl(const cpddg_problem_desc& d, cpddg_setup* s) {
 }
 
 template <int D>
-void decompose_impl(cpddg_setup* s, const int32_t* part, int n_overlap, int method, double alpha,
+void decompose_impl(cpddg_setup* s, const int32_t* part, int n_part, int n_overlap, int method, double alpha,
                     double alpha_cross, int32_t* part_out, int* moves) {
     SetupImpl<D>& I = impl_of<D>(s);
     if (!part) throw ConfigError("a partition is required (partition_graph is not part of this path)");
+    if (n_part != I.band.n_active)
+        throw ConfigError("partition file has " + std::to_string(n_part) + " entries but the mesh has " +
+                          std::to_string(I.band.n_active) + " active nodes");
     if (n_overlap < 1) throw ConfigError("n_overlap must be at least 1");
     const bool robin = method == CPDDG_ORAS;
     if (robin) {
@@ -179,14 +182,14 @@ int cpddg_setup_csr(const cpddg_setup* s, int which, int64_t* row_ptr, int32_t* 
     });
 }
 
-int cpddg_setup_decompose(cpddg_setup* s, const int32_t* part, int n_overlap, int method, double alpha,
+int cpddg_setup_decompose(cpddg_setup* s, const int32_t* part, int n_part, int n_overlap, int method, double alpha,
                           double alpha_cross, int32_t* part_out, int* moves) {
     return guarded([&] {
         if (!s) throw InternalError("null setup handle");
         if (s->dim == 2)
-            decompose_impl<2>(s, part, n_overlap, method, alpha, alpha_cross, part_out, moves);
+            decompose_impl<2>(s, part, n_part, n_overlap, method, alpha, alpha_cross, part_out, moves);
         else
-            decompose_impl<3>(s, part, n_overlap, method, alpha, alpha_cross, part_out, moves);
+            decompose_impl<3>(s, part, n_part, n_overlap, method, alpha, alpha_cross, part_out, moves);
     });
 }
 
