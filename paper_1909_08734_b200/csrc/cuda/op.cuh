@@ -65,6 +65,7 @@ struct cpddg_pc {
     std::int64_t factor_bytes = 0, alg_bytes = 0;
     double factor_seconds = 0, analyse_seconds = 0, max_probe_residual = -1;
     int solve_smem = 0;
+    int bwd_prefetch = 1;  // backward L2 prefetch distance in blocks (0 = off)
 };
 
 namespace cpddg {

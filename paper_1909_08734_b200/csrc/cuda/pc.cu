@@ -35,6 +35,7 @@
 #include <algorithm>
 #include <chrono>
 #include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <numeric>
 
@@ -634,7 +635,7 @@ __device__ __forceinline__ void upper_solve_cols(int n, const int* __restrict__ 
                                                  const std::int64_t* __restrict__ ro,
                                                  const double* __restrict__ V, const double* __restrict__ d,
                                                  double* y, double (*tri)[RB][TS], int (*cf)[RB],
-                                                 long long (*cro)[RB]) {  // cf, cro: [3][RB]
+                                                 long long (*cro)[RB], int pf) {  // cf, cro: [3][RB]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nblk = (n + RB - 1) / RB;
     const int ptid = threadIdx.x - 32, pthreads = blockDim.x - 32;
@@ -686,8 +687,8 @@ __device__ __forceinline__ void upper_solve_cols(int n, const int* __restrict__ 
     for (int K = nblk - 1; K >= 0; --K) {
         const int cur = K & 1;
         const int c0 = K * RB;
-        // block K-2 columns: used by the stash of step K-1 and the row updates of step K-3
-        if (threadIdx.x == 32) prefetch_block(K - 2);
+        // prefetch the columns the row updates need `pf` steps from now
+        if (threadIdx.x == 32 && pf > 0) prefetch_block(K + 1 - pf);
         if (warp == 0) {
             const int i = c0 + lane;
             const bool live = lane < RB && i < n;
@@ -765,7 +766,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const int* __restric
                                                             const int* __restrict__ gidx_all,
                                                             const int* __restrict__ sidx_all,
                                                             const double* __restrict__ r, double* z,
-                                                            int accumulate) {
+                                                            int accumulate, int pf) {
     const int j = order[blockIdx.x];
     const int n = n_rows[j];
     const std::int64_t vb = vbase[j];
@@ -784,7 +785,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const int* __restric
     // backward: U x = y, column-oriented on the factorisation's U layout
     __shared__ int cf[3][RB];
     __shared__ long long cro[3][RB];
-    if (MODE != 1) upper_solve_cols(n, first_all + vb, roff_all + vb, U_all + ebase[j], diag_all + vb, y, tri, cf, cro);
+    if (MODE != 1) upper_solve_cols(n, first_all + vb, roff_all + vb, U_all + ebase[j], diag_all + vb, y, tri, cf, cro, pf);
     for (int p = tid; p < n; p += blockDim.x) {
         const int s = __ldg(sidx_all + vb + p);
         if (s >= 0) z[s] = accumulate ? z[s] + y[p] : y[p];
@@ -802,7 +803,8 @@ void pc_apply_mode(const cpddg_pc* pc, const double* r, double* z, bool accumula
     auto kern = mode == 1 ? k_solve<1> : mode == 2 ? k_solve<2> : k_solve<0>;
     kern<<<pc->n_sub, kSolveThreads, pc->solve_smem, st>>>(
         pc->order.get(), pc->n_rows.get(), pc->vbase.get(), pc->ebase.get(), pc->first.get(), pc->roff.get(),
-        pc->dinv.get(), pc->L.get(), pc->U.get(), pc->gidx.get(), pc->sidx.get(), r, z, accumulate ? 1 : 0);
+        pc->dinv.get(), pc->L.get(), pc->U.get(), pc->gidx.get(), pc->sidx.get(), r, z, accumulate ? 1 : 0,
+        pc->bwd_prefetch);
     CPDDG_CUDA(cudaGetLastError());
 }
 
@@ -908,6 +910,7 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
     pc->u_entries = ebs;
     pc->entries = ebs + pc->u_entries + vb;
     pc->solve_smem = static_cast<int>(sizeof(double)) * pc->max_rows;
+    if (const char* e = std::getenv("CPDDG_BWD_PREFETCH")) pc->bwd_prefetch = std::atoi(e);
     if (pc->solve_smem > 200 * 1024) throw ConfigError("subdomain system too large for the shared-memory solve");
     for (auto kern : {k_solve<0>, k_solve<1>, k_solve<2>})
         CPDDG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(pc->solve_smem, 1)));
