@@ -14,6 +14,8 @@
 #include "common.cuh"
 #include "op.cuh"
 
+#include <cooperative_groups.h>
+
 #include <cmath>
 #include <vector>
 
@@ -64,6 +66,71 @@ __global__ void __launch_bounds__(kRedThreads) k_mgs(int n, const double* __rest
             if (out2) *out2 = t2;
         }
     }
+}
+
+/** The whole modified Gram-Schmidt step of one Arnoldi iteration in one
+ *  cooperative launch (solve.hpp:162-169, then the basis scaling of :195):
+ *    pass 0:        h_0 = V_0 . w,  ||w||^2 (before orthogonalisation)
+ *    pass i=1..m:   w -= h_{i-1} V_{i-1};  h_i = V_i . w
+ *    pass m+1:      w -= h_m V_m;  h_{m+1} = w . w
+ *    then           V_{m+1} = w / sqrt(h_{m+1})   (speculative; unused if the host stops)
+ *  Passes are separated by grid-wide barriers; every block re-sums the
+ *  per-block partials of a pass in the same fixed order, so all blocks hold
+ *  the identical h_i without a second barrier and results are bitwise
+ *  deterministic (fixed grid).  h[0..m+1] and ||w0||^2 land in `hout`. */
+__global__ void __launch_bounds__(kRedThreads) k_mgs_all(int n, int m, const double* const* __restrict__ V,
+                                                         double* __restrict__ w, double* __restrict__ vnext,
+                                                         double* partials, double* hout, double* wn0) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double sh[kRedThreads / 32];
+    __shared__ double hb;
+    const int nb = gridDim.x;
+    const int stride = gridDim.x * blockDim.x;
+    const int i0 = blockIdx.x * blockDim.x + threadIdx.x;
+    double hprev = 0.0;
+    for (int pass = 0; pass <= m + 1; ++pass) {
+        const double* vp = pass > 0 ? V[pass - 1] : nullptr;
+        const double* vn = pass <= m ? V[pass] : nullptr;
+        double a1 = 0.0, a2 = 0.0;
+        for (int i = i0; i < n; i += stride) {
+            double wi = w[i];
+            if (vp) {
+                wi -= hprev * vp[i];
+                w[i] = wi;
+            }
+            a1 = fma(vn ? vn[i] : wi, wi, a1);
+            if (pass == 0) a2 = fma(wi, wi, a2);
+        }
+        const double b1 = block_sum<kRedThreads>(a1, sh);
+        const double b2 = pass == 0 ? block_sum<kRedThreads>(a2, sh) : 0.0;
+        double* slot = partials + static_cast<std::size_t>(pass) * 2 * nb;
+        if (threadIdx.x == 0) {
+            slot[blockIdx.x] = b1;
+            slot[nb + blockIdx.x] = b2;
+        }
+        grid.sync();
+        double s1 = 0.0, s2 = 0.0;
+        for (int q = threadIdx.x; q < nb; q += blockDim.x) {
+            s1 += slot[q];
+            if (pass == 0) s2 += slot[nb + q];
+        }
+        const double t1 = block_sum<kRedThreads>(s1, sh);
+        const double t2 = pass == 0 ? block_sum<kRedThreads>(s2, sh) : 0.0;
+        if (threadIdx.x == 0) {
+            hb = t1;
+            if (blockIdx.x == 0) {
+                hout[pass] = t1;
+                if (pass == 0) *wn0 = t2;
+            }
+        }
+        __syncthreads();
+        hprev = hb;
+    }
+    // hprev = ||w||^2 after the last pass: speculative next basis vector
+    const double sub = sqrt(hprev);
+    if (vnext)
+        for (int i = i0; i < n; i += stride) vnext[i] = w[i] / sub;
 }
 
 __global__ void k_scale(int n, const double* __restrict__ src, double s, double* __restrict__ dst) {
@@ -212,6 +279,29 @@ struct Workspace {
         CPDDG_CUDA(cudaGetLastError());
         ++launches;
     }
+    DevBuf<double> mgs_partials;
+    int coop_grid = 0;
+    void mgs_all(int m, double* w, double* vnext, double* hout, double* wn0) {
+        if (coop_grid == 0) {
+            int per_sm = 0;
+            CPDDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mgs_all, kRedThreads, 0));
+            coop_grid = std::max(1, std::min(per_sm, 4)) * sm_count();
+        }
+        const std::size_t need = static_cast<std::size_t>(2 * coop_grid) * (m + 2);
+        if (mgs_partials.size() < need) mgs_partials.alloc(std::max(need, static_cast<std::size_t>(2 * coop_grid) * 64));
+        // basis pointer table (V_0..V_m) on the device
+        std::vector<const double*> vp(static_cast<std::size_t>(m) + 1);
+        for (int k = 0; k <= m; ++k) vp[static_cast<std::size_t>(k)] = kc.V[static_cast<std::size_t>(k)].get();
+        if (kc.vptr.size() < vp.size() + 64) kc.vptr.alloc(vp.size() + 64);
+        CPDDG_CUDA(cudaMemcpyAsync(kc.vptr.get(), vp.data(), sizeof(double*) * vp.size(), cudaMemcpyHostToDevice, st));
+        int nn = n, mm = m;
+        const double* const* vpd = kc.vptr.get();
+        double* part = mgs_partials.get();
+        void* args[] = {&nn, &mm, &vpd, &w, &vnext, &part, &hout, &wn0};
+        CPDDG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_mgs_all), dim3(coop_grid), dim3(kRedThreads),
+                                               args, 0, st));
+        ++launches;
+    }
     void scale(const double* src, double s, double* dst) {
         k_scale<<<grid, kRedThreads, 0, st>>>(n, src, s, dst);
         CPDDG_CUDA(cudaGetLastError());
@@ -306,10 +396,9 @@ static void gmres(cpddg_op* op, cpddg_pc* pc, const double* b, double* u, const 
             }
             kt.time(false, [&] { op_apply(op, z, w.get(), st); });
             ws.launches += 2;
-            // MGS: pass 0 also yields ||w||^2 before orthogonalisation
-            ws.mgs(nullptr, nullptr, w.get(), basis(0), hd + 0, nd + 0);
-            for (int i = 1; i <= m; ++i) ws.mgs(hd + i - 1, basis(i - 1), w.get(), basis(i), hd + i, nullptr);
-            ws.mgs(hd + m, basis(m), w.get(), nullptr, hd + m + 1, nullptr);
+            // MGS, all m+2 passes and the next basis vector in one cooperative launch
+            double* vnext = (m + 1 <= cycle) ? basis(m + 1) : nullptr;
+            ws.mgs_all(m, w.get(), vnext, hd, nd + 0);
             CPDDG_CUDA(cudaMemcpyAsync(hh.p, hd, sizeof(double) * (m + 2), cudaMemcpyDeviceToHost, st));
             CPDDG_CUDA(cudaMemcpyAsync(hh.p + cap, nd, sizeof(double), cudaMemcpyDeviceToHost, st));
             CPDDG_CUDA(cudaStreamSynchronize(st));
@@ -341,7 +430,7 @@ static void gmres(cpddg_op* op, cpddg_pc* pc, const double* b, double* u, const 
                 converged = true;
                 break;
             }
-            ws.scale(w.get(), subdiag, basis(m));
+            // V[m] = w / subdiag was written by k_mgs_all (same sqrt of the same h)
         }
         if (m > 0) {
             std::vector<double> y(static_cast<std::size_t>(m), 0.0);

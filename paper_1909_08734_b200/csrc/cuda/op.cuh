@@ -66,6 +66,7 @@ struct cpddg_pc {
     double factor_seconds = 0, analyse_seconds = 0, max_probe_residual = -1;
     int solve_smem = 0;
     int bwd_prefetch = 1;  // backward L2 prefetch distance in blocks (0 = off)
+    bool urows = true;     // backward layout: reversed U rows (true) or U columns (false)
 };
 
 namespace cpddg {

@@ -36,6 +36,7 @@
 #include <chrono>
 #include <climits>
 #include <cstdlib>
+#include <string>
 #include <cmath>
 #include <numeric>
 
@@ -464,42 +465,6 @@ constexpr int kSolveThreads = 32 * kSolveWarps;
 constexpr int RB = 2 * (kSolveWarps - 1);  // rows per pipelined block: 2 per panel warp
 constexpr int TS = 2 * RB + 1;             // padded stash row (previous block + own triangle)
 
-/** Convert U from column profile storage (factorisation layout) to the
- *  reversed row layout the solve streams: reversed row i' = n-1-i holds
- *  U(i, j) for j in (i, rlast_i] at reversed column j' = n-1-j, i.e. the
- *  backward substitution becomes a forward one on the reversed system. */
-__global__ void __launch_bounds__(256) k_reverse_u(const int* __restrict__ order, const int* __restrict__ n_rows,
-                                                   const std::int64_t* __restrict__ vbase,
-                                                   const std::int64_t* __restrict__ ebase,
-                                                   const std::int64_t* __restrict__ ubase,
-                                                   const int* __restrict__ first_all,
-                                                   const std::int64_t* __restrict__ roff_all,
-                                                   const int* __restrict__ rlast_all,
-                                                   const std::int64_t* __restrict__ uroff_all,
-                                                   const double* __restrict__ diag_all,
-                                                   const double* __restrict__ Ucol_all, double* __restrict__ Urev_all,
-                                                   double* __restrict__ drev_all) {
-    const int j = order[blockIdx.x];
-    const int n = n_rows[j];
-    const std::int64_t vb = vbase[j];
-    const int* first = first_all + vb;
-    const std::int64_t* roff = roff_all + vb;
-    const int* rlast = rlast_all + vb;
-    const std::int64_t* uroff = uroff_all + vb;
-    const double* Ucol = Ucol_all + ebase[j];
-    double* Urev = Urev_all + ubase[j];
-    for (int ip = threadIdx.x; ip < n; ip += blockDim.x) {
-        const int i = n - 1 - ip;
-        drev_all[vb + ip] = diag_all[vb + i];
-        const int fpr = n - 1 - rlast[i];
-        double* out = Urev + uroff[ip] - fpr;
-        for (int jp = fpr; jp < ip; ++jp) {
-            const int c = n - 1 - jp;
-            const int fc = first[c];
-            out[jp] = i >= fc ? Ucol[roff[c] + i - fc] : 0.0;
-        }
-    }
-}
 
 /** Prefetch [p, p + bytes) into L2 with the bulk-copy engine
  *  (cp.async.bulk.prefetch.L2; p and bytes 16-byte aligned). */
@@ -611,7 +576,7 @@ __device__ __forceinline__ void lower_solve(int n, const int* __restrict__ f, co
             }
             const int rb = min(RB, n - r0);
             for (int c = 0; c < rb; ++c) {
-                if (d && lane == c) s = s / __ldg(d + r0 + c);
+                if (d && lane == c) s *= __ldg(d + r0 + c);  // d: reciprocal pivots
                 const double xc = __shfl_sync(0xffffffffu, s, c);
                 if (lane > c && live) s = fma(-tri[cur][lane][RB + c], xc, s);
             }
@@ -620,6 +585,49 @@ __device__ __forceinline__ void lower_solve(int n, const int* __restrict__ f, co
             panel((k + 1) * RB, cur ^ 1);
         }
         __syncthreads();
+    }
+}
+
+/** Re-lay U (column profile storage from the factorisation) as reversed
+ *  rows for a row-oriented backward pass: reversed row i' = n-1-i holds
+ *  U(i, j), j in (i, rlast_i], at reversed column j' = n-1-j over
+ *  [uf_i', i') (uf even, lengths even: 16-byte aligned like L).  Entries of
+ *  the row range outside the column profile are stored zeros. */
+__global__ void __launch_bounds__(256) k_reverse_u(const int* __restrict__ order, const int* __restrict__ n_rows,
+                                                   const std::int64_t* __restrict__ vbase,
+                                                   const std::int64_t* __restrict__ ebase,
+                                                   const std::int64_t* __restrict__ ubase,
+                                                   const int* __restrict__ first_all,
+                                                   const std::int64_t* __restrict__ roff_all,
+                                                   const int* __restrict__ ufirst_all,
+                                                   const std::int64_t* __restrict__ uroff_all,
+                                                   const double* __restrict__ dinv_all,
+                                                   const double* __restrict__ Ucol_all, double* __restrict__ Urev_all,
+                                                   double* __restrict__ drev_all) {
+    const int j = order[blockIdx.x];
+    const int n = n_rows[j];
+    const std::int64_t vb = vbase[j];
+    const int* first = first_all + vb;
+    const std::int64_t* roff = roff_all + vb;
+    const int* ufirst = ufirst_all + vb;
+    const std::int64_t* uroff = uroff_all + vb;
+    const double* Ucol = Ucol_all + ebase[j];
+    double* Urev = Urev_all + ubase[j];
+    for (int ip = threadIdx.x; ip < n; ip += blockDim.x) {
+        const int i = n - 1 - ip;
+        drev_all[vb + ip] = dinv_all[vb + i];
+        const int fpr = ufirst[ip];
+        double* out = Urev + uroff[ip] - fpr;
+        const int end = ip + (ip & 1);
+        for (int jp = fpr; jp < end; ++jp) {
+            double v = 0.0;
+            if (jp < ip) {
+                const int c = n - 1 - jp;
+                const int fc = first[c];
+                if (c > i && i >= fc) v = Ucol[roff[c] + i - fc];
+            }
+            out[jp] = v;
+        }
     }
 }
 
@@ -753,7 +761,9 @@ __device__ __forceinline__ void upper_solve_cols(int n, const int* __restrict__ 
     }
 }
 
-template <int MODE>  // 0: full apply; 1: forward only; 2: backward only (profiling)
+// MODE 0: full apply; 1: forward only; 2: backward only (profiling).
+// UROWS: backward on reversed U rows (k_reverse_u) instead of U columns.
+template <int MODE, bool UROWS>
 __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const int* __restrict__ order,
                                                             const int* __restrict__ n_rows,
                                                             const std::int64_t* __restrict__ vbase,
@@ -766,7 +776,11 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const int* __restric
                                                             const int* __restrict__ gidx_all,
                                                             const int* __restrict__ sidx_all,
                                                             const double* __restrict__ r, double* z,
-                                                            int accumulate, int pf) {
+                                                            int accumulate, int pf,
+                                                            const std::int64_t* __restrict__ ubase,
+                                                            const int* __restrict__ ufirst_all,
+                                                            const std::int64_t* __restrict__ uroff_all,
+                                                            const double* __restrict__ drev_all) {
     const int j = order[blockIdx.x];
     const int n = n_rows[j];
     const std::int64_t vb = vbase[j];
@@ -782,13 +796,32 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const int* __restric
     __syncthreads();
     // forward: L y = b (unit lower)
     if (MODE != 2) lower_solve(n, first_all + vb, roff_all + vb, L_all + ebase[j], nullptr, y, part, tri);
-    // backward: U x = y, column-oriented on the factorisation's U layout
-    __shared__ int cf[3][RB];
-    __shared__ long long cro[3][RB];
-    if (MODE != 1) upper_solve_cols(n, first_all + vb, roff_all + vb, U_all + ebase[j], diag_all + vb, y, tri, cf, cro, pf);
-    for (int p = tid; p < n; p += blockDim.x) {
-        const int s = __ldg(sidx_all + vb + p);
-        if (s >= 0) z[s] = accumulate ? z[s] + y[p] : y[p];
+    if constexpr (UROWS) {
+        // backward: U x = y as a forward solve on the reversed system
+        for (int p = tid; p < n / 2; p += blockDim.x) {
+            const double t = y[p];
+            y[p] = y[n - 1 - p];
+            y[n - 1 - p] = t;
+        }
+        __syncthreads();
+        if (MODE != 1)
+            lower_solve(n, ufirst_all + vb, uroff_all + vb, U_all + ubase[j], drev_all + vb, y, part, tri);
+        for (int p = tid; p < n; p += blockDim.x) {
+            const int s = __ldg(sidx_all + vb + p);
+            if (s >= 0) {
+                const double v = y[n - 1 - p];
+                z[s] = accumulate ? z[s] + v : v;
+            }
+        }
+    } else {
+        // backward: U x = y, column-oriented on the factorisation's U layout
+        __shared__ int cf[3][RB];
+        __shared__ long long cro[3][RB];
+        if (MODE != 1) upper_solve_cols(n, first_all + vb, roff_all + vb, U_all + ebase[j], diag_all + vb, y, tri, cf, cro, pf);
+        for (int p = tid; p < n; p += blockDim.x) {
+            const int s = __ldg(sidx_all + vb + p);
+            if (s >= 0) z[s] = accumulate ? z[s] + y[p] : y[p];
+        }
     }
 }
 
@@ -800,11 +833,12 @@ void append(std::vector<T>& dst, const std::vector<T>& src) {
 }  // namespace
 
 void pc_apply_mode(const cpddg_pc* pc, const double* r, double* z, bool accumulate, int mode, cudaStream_t st) {
-    auto kern = mode == 1 ? k_solve<1> : mode == 2 ? k_solve<2> : k_solve<0>;
+    auto kern = pc->urows ? (mode == 1 ? k_solve<1, true> : mode == 2 ? k_solve<2, true> : k_solve<0, true>)
+                          : (mode == 1 ? k_solve<1, false> : mode == 2 ? k_solve<2, false> : k_solve<0, false>);
     kern<<<pc->n_sub, kSolveThreads, pc->solve_smem, st>>>(
         pc->order.get(), pc->n_rows.get(), pc->vbase.get(), pc->ebase.get(), pc->first.get(), pc->roff.get(),
         pc->dinv.get(), pc->L.get(), pc->U.get(), pc->gidx.get(), pc->sidx.get(), r, z, accumulate ? 1 : 0,
-        pc->bwd_prefetch);
+        pc->bwd_prefetch, pc->ubase.get(), pc->ufirst.get(), pc->uroff.get(), pc->drev.get());
     CPDDG_CUDA(cudaGetLastError());
 }
 
@@ -908,11 +942,44 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
         if (st[static_cast<std::size_t>(j)]) throw DivergenceError("singular factorization of subdomain " + std::to_string(j));
 
     pc->u_entries = ebs;
+    if (const char* e = std::getenv("CPDDG_BWD_LAYOUT")) pc->urows = std::string(e) != "cols";
+    if (pc->urows) {
+        std::vector<int> ufirst(static_cast<std::size_t>(vb));
+        std::vector<std::int64_t> uroff(static_cast<std::size_t>(vb)), ubase(static_cast<std::size_t>(n_sub));
+        std::int64_t ub = 0;
+        for (int j = 0; j < n_sub; ++j) {
+            const int nj = n_rows[static_cast<std::size_t>(j)];
+            const std::int64_t v0 = vbase[static_cast<std::size_t>(j)];
+            ubase[static_cast<std::size_t>(j)] = ub;
+            std::int64_t off = 0;
+            for (int ip = 0; ip < nj; ++ip) {
+                const int i = nj - 1 - ip;
+                const int fpr = (nj - 1 - rlast[static_cast<std::size_t>(v0 + i)]) & ~1;
+                ufirst[static_cast<std::size_t>(v0 + ip)] = fpr;
+                uroff[static_cast<std::size_t>(v0 + ip)] = off;
+                off += (ip + (ip & 1)) - fpr;
+            }
+            ub += off;
+        }
+        pc->u_entries = ub;
+        pc->ufirst.upload(ufirst);
+        pc->uroff.upload(uroff);
+        pc->ubase.upload(ubase);
+        DevBuf<double> urev(static_cast<std::size_t>(std::max<std::int64_t>(ub, 1)));
+        pc->drev.alloc(static_cast<std::size_t>(vb));
+        k_reverse_u<<<n_sub, 256>>>(pc->order.get(), pc->n_rows.get(), pc->vbase.get(), pc->ebase.get(),
+                                    pc->ubase.get(), pc->first.get(), pc->roff.get(), pc->ufirst.get(),
+                                    pc->uroff.get(), pc->dinv.get(), pc->U.get(), urev.get(), pc->drev.get());
+        CPDDG_CUDA(cudaGetLastError());
+        CPDDG_CUDA(cudaDeviceSynchronize());
+        pc->U = std::move(urev);
+    }
     pc->entries = ebs + pc->u_entries + vb;
     pc->solve_smem = static_cast<int>(sizeof(double)) * pc->max_rows;
     if (const char* e = std::getenv("CPDDG_BWD_PREFETCH")) pc->bwd_prefetch = std::atoi(e);
     if (pc->solve_smem > 200 * 1024) throw ConfigError("subdomain system too large for the shared-memory solve");
-    for (auto kern : {k_solve<0>, k_solve<1>, k_solve<2>})
+    for (auto kern : {k_solve<0, false>, k_solve<1, false>, k_solve<2, false>, k_solve<0, true>, k_solve<1, true>,
+                      k_solve<2, true>})
         CPDDG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(pc->solve_smem, 1)));
     // bytes one apply streams: L, U, diag, first, roff per row, gather/scatter maps, r gathers, z writes
     // streamed per apply: L and reversed-U values, diagonal, and the per-row
