@@ -116,6 +116,71 @@ __global__ void __launch_bounds__(256) k_extend(int nb, const double* __restrict
     v[k] = acc;
 }
 
+/** Cubic (p = 3) weights in product (Lagrange) form -- no divisions -- with
+ *  the reference's exact-hit rule (interp.hpp:39-44).  Differs from the
+ *  barycentric evaluation only in the last bits; operator parity is 1e-12. */
+__device__ __forceinline__ void weights_p3(double t, double* w) {
+    const double t0 = t, t1 = t - 1.0, t2 = t - 2.0, t3 = t - 3.0;
+    w[0] = -(t1 * t2 * t3) * (1.0 / 6.0);
+    w[1] = (t0 * t2 * t3) * 0.5;
+    w[2] = -(t0 * t1 * t3) * 0.5;
+    w[3] = (t0 * t1 * t2) * (1.0 / 6.0);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+        if (fabs(t - j) < 1e-12) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) w[k] = (k == j) ? 1.0 : 0.0;
+        }
+}
+
+/** v = E x for p = 3 with four threads per band node (one per offset a of
+ *  axis 0): each thread gathers its (p+1)^(d-2) runs of 4 consecutive x,
+ *  the quad reduces with two shuffles.  4x the threads of one-node-per-thread
+ *  and no divisions: the gather from L2 is the only latency left. */
+template <int D>
+__global__ void __launch_bounds__(256) k_extend_p3(int nb, const double* __restrict__ t,
+                                                   const int* __restrict__ lines, const double* __restrict__ x,
+                                                   double* __restrict__ v) {
+    const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+    const int k = gt >> 2, a = gt & 3;
+    double acc = 0.0;
+    if (k < nb) {
+        double wl[4], w0[4];
+        weights_p3(__ldg(t + static_cast<std::size_t>(D - 1) * nb + k), wl);
+        weights_p3(__ldg(t + k), w0);
+        if constexpr (D == 2) {
+            const int o = __ldg(lines + static_cast<std::size_t>(a) * nb + k);
+            double s = 0.0;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) s = fma(wl[c], __ldg(x + o + c), s);
+            acc = (a == 0 ? w0[0] : a == 1 ? w0[1] : a == 2 ? w0[2] : w0[3]) * s;
+        } else {
+            double w1[4];
+            weights_p3(__ldg(t + static_cast<std::size_t>(nb) + k), w1);
+            int o[4];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) o[b] = __ldg(lines + static_cast<std::size_t>(a * 4 + b) * nb + k);
+            double xv[4][4];
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) xv[b][c] = __ldg(x + o[b] + c);
+            double sa = 0.0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                double s = 0.0;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) s = fma(wl[c], xv[b][c], s);
+                sa = fma(w1[b], s, sa);
+            }
+            acc = (a == 0 ? w0[0] : a == 1 ? w0[1] : a == 2 ? w0[2] : w0[3]) * sa;
+        }
+    }
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    if (k < nb && a == 0) v[k] = acc;
+}
+
 /** y = cg x - ih2 sum v[nbr]; if b != nullptr: y <- b - y and partial ||y||^2. */
 template <int D, bool RESID>
 __global__ void __launch_bounds__(kRedThreads) k_helm(int na, double cg, double ih2,
@@ -227,7 +292,11 @@ static void launch_apply(const cpddg_op* op, const double* x, const double* b, d
                          cudaStream_t st) {
     const int nb = op->na + op->ng;
     const int thr = 256;
-    switch (op->p) {
+    if (op->p == 3) {
+        const long long threads = 4LL * nb;
+        k_extend_p3<D><<<static_cast<int>((threads + thr - 1) / thr), thr, 0, st>>>(nb, op->t.get(), op->lines.get(), x,
+                                                                                  op->v.get());
+    } else switch (op->p) {
 #define CPDDG_EXT(PP) \
     case PP: k_extend<D, PP><<<(nb + thr - 1) / thr, thr, 0, st>>>(nb, op->t.get(), op->lines.get(), x, op->v.get()); break;
         CPDDG_EXT(1) CPDDG_EXT(2) CPDDG_EXT(3) CPDDG_EXT(4) CPDDG_EXT(5) CPDDG_EXT(6) CPDDG_EXT(7)
