@@ -34,14 +34,55 @@ sys.path.insert(0, ROOT)
 
 METRIC = "ORAS-GMRES DOF·iters/s (FP64)"
 UNIT = "DOF·iter/s"
-WORKLOAD = dict(surface="sphere", h=0.0125, p=3, c=1.0, n_subdomains=256, n_overlap=3, method="oras",
-                alpha=4.0, alpha_cross=40.0, gmres_restart=50, rel_tol=1e-10, max_iter=2000)
+CONFIGS = {
+    # BASELINE.json configs[2] -- the headline, and the default workload of this bench
+    "headline": dict(surface="sphere", h=0.0125, p=3, c=1.0, n_subdomains=256, n_overlap=3, method="oras",
+                     alpha=4.0, alpha_cross=40.0, gmres_restart=50, rel_tol=1e-10, max_iter=2000,
+                     partition="rcb", rhs="sphere"),
+    # configs[0]: unit circle, 8 angular sectors, ORAS with the reference's default alpha
+    "circle": dict(surface="circle", h=0.0125, p=3, c=1.0, n_subdomains=8, n_overlap=2, method="oras",
+                   alpha=1.0, alpha_cross=-1.0, gmres_restart=50, rel_tol=1e-10, max_iter=2000,
+                   partition="sector", rhs="circle"),
+    # configs[1]: unit sphere h = 0.05, 64 RCB
+    "sphere05": dict(surface="sphere", h=0.05, p=3, c=1.0, n_subdomains=64, n_overlap=2, method="oras",
+                     alpha=4.0, alpha_cross=40.0, gmres_restart=50, rel_tol=1e-10, max_iter=2000,
+                     partition="rcb", rhs="sphere"),
+    # configs[3]: torus R = 1, r = 0.4, h = 0.01, 512 RCB, seeded trigonometric right-hand side
+    "torus": dict(surface="torus", major_radius=1.0, minor_radius=0.4, h=0.01, p=3, c=1.0, n_subdomains=512,
+                  n_overlap=2, method="oras", alpha=4.0, alpha_cross=40.0, gmres_restart=50, rel_tol=1e-10,
+                  max_iter=2000, partition="rcb", rhs="trig"),
+    # configs[4]: displaced icosphere (subdivision 6), h = 0.01, 512 RCB, modified cross-point condition
+    "trimesh": dict(surface="obj", h=0.01, p=3, c=1.0, n_subdomains=512, n_overlap=2, method="oras",
+                    alpha=4.0, alpha_cross=40.0, gmres_restart=50, rel_tol=1e-10, max_iter=2000,
+                    partition="rcb", rhs="trig", subdivisions=6, mesh_seed=5),
+}
+WORKLOAD = CONFIGS["headline"]
 FALLBACK_HBM_GBS = 6650.0
 
 
-def workload_name(w=WORKLOAD):
-    return (f"sphere_h{w['h']}_p{w['p']}_rcb{w['n_subdomains']}_no{w['n_overlap']}_"
+def workload_name(w=None):
+    w = w or WORKLOAD
+    return (f"{w['surface']}_h{w['h']}_p{w['p']}_{w['partition']}{w['n_subdomains']}_no{w['n_overlap']}_"
             f"{w['method']}_a{w['alpha']:g}_ax{w['alpha_cross']:g}_gmres{w['gmres_restart']}_tol{w['rel_tol']:g}")
+
+
+def build_problem(w):
+    """Surface, band, E, A (the device path's host setup) + partition + rhs for config w."""
+    from paper_1909_08734_b200 import api, inputs
+    obj = None
+    if w["surface"] == "obj":
+        import tempfile
+        v, f = inputs.displaced_icosphere(w["subdivisions"], seed=w["mesh_seed"])
+        obj = os.path.join(tempfile.mkdtemp(prefix="cpddg_mesh_"), "icosphere.obj")
+        inputs.write_obj(obj, v, f)
+    P = api.Problem(w["surface"], h=w["h"], p=w["p"], c=w["c"], major_radius=w.get("major_radius", 2 / 3),
+                    minor_radius=w.get("minor_radius", 1 / 3), obj_path=obj)
+    cp = P.active_cp
+    part = inputs.sector_partition(cp, w["n_subdomains"]) if w["partition"] == "sector" \
+        else inputs.rcb_partition(cp, w["n_subdomains"])
+    rhs = {"sphere": inputs.rhs_sphere, "circle": inputs.rhs_circle,
+           "trig": lambda q: inputs.rhs_trig(q, seed=2024)}[w["rhs"]](cp)
+    return P, part, rhs, obj
 
 
 def peaks():
@@ -127,10 +168,14 @@ def cpu_reference(P, locs, b, iters_per_step: int, steps: int, warmup: int):
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import ref
     cores = os.cpu_count() or 1
-    cfg = dict(surface=WORKLOAD["surface"], h=WORKLOAD["h"], p=WORKLOAD["p"], c=WORKLOAD["c"],
-               method=WORKLOAD["method"], mode="gmres", gmres_restart=WORKLOAD["gmres_restart"],
-               n_overlap=WORKLOAD["n_overlap"], n_subdomains=WORKLOAD["n_subdomains"], alpha=WORKLOAD["alpha"],
-               alpha_cross=WORKLOAD["alpha_cross"], rel_tol=WORKLOAD["rel_tol"])
+    w = WORKLOAD
+    cfg = dict(surface=w["surface"], h=w["h"], p=w["p"], c=w["c"], method=w["method"], mode="gmres",
+               gmres_restart=w["gmres_restart"], n_overlap=w["n_overlap"], n_subdomains=w["n_subdomains"],
+               alpha=w["alpha"], alpha_cross=w["alpha_cross"], rel_tol=w["rel_tol"])
+    if w["surface"] == "torus":
+        cfg.update(major_radius=w["major_radius"], minor_radius=w["minor_radius"])
+    if w["surface"] == "obj":
+        cfg.update(obj=P.obj_path)
     t0 = time.perf_counter()
     R = ref.RefProblem(cfg, workers=cores)
     t_build = time.perf_counter() - t0
@@ -163,11 +208,10 @@ def run_reference_arm(args):
     if not ref.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference at build time)"}))
         return 0
-    P = api.Problem("sphere", h=WORKLOAD["h"], p=WORKLOAD["p"], c=WORKLOAD["c"])
-    P.decompose(inputs.rcb_partition(P.active_cp, WORKLOAD["n_subdomains"]), WORKLOAD["n_overlap"],
-                WORKLOAD["method"], WORKLOAD["alpha"], WORKLOAD["alpha_cross"])
+    P, part, b, obj = build_problem(WORKLOAD)
+    P.obj_path = obj
+    P.decompose(part, WORKLOAD["n_overlap"], WORKLOAD["method"], WORKLOAD["alpha"], WORKLOAD["alpha_cross"])
     locs = [P.local(j) for j in range(P.n_sub)]
-    b = inputs.rhs_sphere(P.active_cp)
     base = cpu_reference(P, locs, b, args.ref_iters, args.steps, args.warmup)
     line = {"metric": METRIC, "value": base["value"], "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * base["seconds"] / args.steps, "higher_is_better": True,
@@ -189,7 +233,11 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-iters", type=int, default=4, help="GMRES iterations per reference sample step")
     ap.add_argument("--cpu-baseline", default="auto", choices=["auto", "off"])
+    ap.add_argument("--config", default="headline", choices=sorted(CONFIGS),
+                    help="workload (default: BASELINE's headline; the others are parity / scaling cases)")
     args = ap.parse_args()
+    global WORKLOAD
+    WORKLOAD = CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference_arm(args)
 
@@ -220,9 +268,9 @@ def main():
 
     # ---- setup (untimed): band, E, A, partition, subdomains, device factorisation
     t0 = time.perf_counter()
-    P = api.Problem("sphere", h=WORKLOAD["h"], p=WORKLOAD["p"], c=WORKLOAD["c"])
+    P, part, b_host, obj = build_problem(WORKLOAD)
+    P.obj_path = obj
     t_problem = time.perf_counter() - t0
-    part = inputs.rcb_partition(P.active_cp, WORKLOAD["n_subdomains"])
     t0 = time.perf_counter()
     _, moves = P.decompose(part, WORKLOAD["n_overlap"], WORKLOAD["method"], WORKLOAD["alpha"], WORKLOAD["alpha_cross"])
     t_decomp = time.perf_counter() - t0
@@ -232,7 +280,6 @@ def main():
     torch.cuda.synchronize()
     t_locals = time.perf_counter() - t0
     pcs = M.stats()
-    b_host = inputs.rhs_sphere(P.active_cp)
     b = torch.from_numpy(b_host).cuda()
     n = P.n_active
     tol, mi, rs = WORKLOAD["rel_tol"], WORKLOAD["max_iter"], WORKLOAD["gmres_restart"]
@@ -298,10 +345,15 @@ def main():
             "align_moves": moves, "gmres_iterations": iters[0], "time_to_1e-10_s": t_dev / args.steps,
             "final_true_relative_residual": final_rel, "parallelism": f"replicas x{world}",
             "l2": "inputs larger than L2: 12+ GB of local factors streamed per preconditioner apply",
-            "rhs": "f = 13 u, u = x^3 - 3xy^2 at closest points", "partition": "RCB on closest points",
+            "rhs": {"sphere": "f = 13 u, u = x^3 - 3xy^2 at closest points",
+                    "circle": "f = 2 sin(t) + 145 sin(12 t)",
+                    "trig": "16 seeded modes sin(k.cp + phi), k in [-4,4]^3"}[WORKLOAD["rhs"]],
+            "partition": WORKLOAD["partition"] + " on closest points, then align_interfaces",
             "setup_s": {"problem": t_problem, "decompose": t_decomp, "factor_and_upload": t_locals,
                         "device_factor": pcs["factor_seconds"], "host_analyse": pcs["analyse_seconds"]},
-            "pc": {k: pcs[k] for k in ("factor_entries", "factor_bytes", "n_rows_total", "max_rows", "n_reduced")},
+            "pc": {k: pcs[k] for k in ("factor_entries", "profile_entries", "factor_bytes", "n_rows_total",
+                                       "max_rows", "n_reduced")},
+            "pc_stored_over_profile": pcs["factor_entries"] / pcs["profile_entries"],
             "kernel_ms": {"pc_apply_avg": 1e3 * avg_pc, "op_apply_avg": 1e3 * op_s / max(op_n, 1)},
             "op_roofline_GBs": op_alg / (op_s / max(op_n, 1)) / 1e9 if op_n else None,
         },

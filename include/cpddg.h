@@ -162,6 +162,7 @@ typedef struct {
     int n_reduced;              /* subdomains whose Dirichlet closure block was eliminated */
     int64_t n_rows_total;       /* sum of factored system sizes */
     int64_t factor_entries;     /* stored L + U + diag entries */
+    int64_t profile_entries;    /* minimal symmetric-profile entries (2 sum_i (i - f_i) + n) */
     int64_t factor_bytes;       /* bytes the triangular solves stream per apply */
     int64_t algorithmic_bytes;  /* B_pc of SURVEY.md 8(d) */
     int max_rows;

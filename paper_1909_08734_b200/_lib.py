@@ -46,7 +46,7 @@ class cpddg_pc_options(C.Structure):
 
 class cpddg_pc_stats(C.Structure):
     _fields_ = [("n_sub", C.c_int), ("n_reduced", C.c_int), ("n_rows_total", C.c_int64),
-                ("factor_entries", C.c_int64), ("factor_bytes", C.c_int64),
+                ("factor_entries", C.c_int64), ("profile_entries", C.c_int64), ("factor_bytes", C.c_int64),
                 ("algorithmic_bytes", C.c_int64), ("max_rows", C.c_int),
                 ("factor_seconds", C.c_double), ("analyse_seconds", C.c_double),
                 ("max_probe_residual", C.c_double)]

@@ -61,7 +61,7 @@ struct cpddg_pc {
     cpddg::DevBuf<int> ufirst;         // per reversed row: first reversed column
     cpddg::DevBuf<std::int64_t> uroff; // per reversed row: offset inside the subdomain's U
     cpddg::DevBuf<double> drev;        // diagonal in reversed order
-    std::int64_t u_entries = 0;
+    std::int64_t u_entries = 0, profile_entries = 0;
     std::int64_t factor_bytes = 0, alg_bytes = 0;
     double factor_seconds = 0, analyse_seconds = 0, max_probe_residual = -1;
     int solve_smem = 0;

@@ -975,6 +975,7 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
         pc->U = std::move(urev);
     }
     pc->entries = ebs + pc->u_entries + vb;
+    pc->profile_entries = 2 * ebs + vb;
     pc->solve_smem = static_cast<int>(sizeof(double)) * pc->max_rows;
     if (const char* e = std::getenv("CPDDG_BWD_PREFETCH")) pc->bwd_prefetch = std::atoi(e);
     if (pc->solve_smem > 200 * 1024) throw ConfigError("subdomain system too large for the shared-memory solve");
@@ -1044,6 +1045,7 @@ int cpddg_pc_stats_get(const cpddg_pc* pc, cpddg_pc_stats* st) {
         st->n_reduced = pc->n_reduced;
         st->n_rows_total = pc->rows_total;
         st->factor_entries = pc->entries;
+        st->profile_entries = pc->profile_entries;
         st->factor_bytes = pc->factor_bytes;
         st->algorithmic_bytes = pc->alg_bytes;
         st->max_rows = pc->max_rows;

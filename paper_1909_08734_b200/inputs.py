@@ -138,3 +138,70 @@ def write_vector(path: str, v: np.ndarray) -> None:
 def write_partition(path: str, part: np.ndarray) -> None:
     with open(path, "w") as fh:
         fh.write("".join(f"{int(p)}\n" for p in part))
+
+
+# ------------------------------------------------------------ triangle mesh
+
+def icosphere(subdivisions: int):
+    """Unit icosphere: the icosahedron with each triangle split into four,
+    midpoints projected to the sphere, `subdivisions` times (6 -> 40962
+    vertices, 81920 triangles; BASELINE config 5)."""
+    t = (1.0 + math.sqrt(5.0)) / 2.0
+    verts = [(-1, t, 0), (1, t, 0), (-1, -t, 0), (1, -t, 0), (0, -1, t), (0, 1, t), (0, -1, -t), (0, 1, -t),
+             (t, 0, -1), (t, 0, 1), (-t, 0, -1), (-t, 0, 1)]
+    verts = [tuple(c / math.sqrt(sum(q * q for q in v)) for c in v) for v in verts]
+    faces = [(0, 11, 5), (0, 5, 1), (0, 1, 7), (0, 7, 10), (0, 10, 11), (1, 5, 9), (5, 11, 4), (11, 10, 2),
+             (10, 7, 6), (7, 1, 8), (3, 9, 4), (3, 4, 2), (3, 2, 6), (3, 6, 8), (3, 8, 9), (4, 9, 5), (2, 4, 11),
+             (6, 2, 10), (8, 6, 7), (9, 8, 1)]
+    for _ in range(subdivisions):
+        cache = {}
+
+        def mid(a, b):
+            key = (a, b) if a < b else (b, a)
+            if key not in cache:
+                va, vb = verts[a], verts[b]
+                m = [(va[i] + vb[i]) * 0.5 for i in range(3)]
+                r = math.sqrt(sum(q * q for q in m))
+                verts.append(tuple(q / r for q in m))
+                cache[key] = len(verts) - 1
+            return cache[key]
+
+        nf = []
+        for a, b, c in faces:
+            ab, bc, ca = mid(a, b), mid(b, c), mid(c, a)
+            nf += [(a, ab, ca), (b, bc, ab), (c, ca, bc), (ab, bc, ca)]
+        faces = nf
+    return np.array(verts, np.float64), np.array(faces, np.int64)
+
+
+def real_sph_harm(l: int, m: int, theta: np.ndarray, phi: np.ndarray) -> np.ndarray:
+    """Orthonormal real spherical harmonic Y_lm (theta polar, phi azimuth)."""
+    from scipy.special import lpmv
+    am = abs(m)
+    norm = math.sqrt((2 * l + 1) / (4 * math.pi) * math.factorial(l - am) / math.factorial(l + am))
+    p = lpmv(am, l, np.cos(theta))
+    if m == 0:
+        return norm * p
+    fac = math.sqrt(2.0) * norm * p
+    return fac * (np.cos(am * phi) if m > 0 else np.sin(am * phi))
+
+
+def displaced_icosphere(subdivisions: int = 6, seed: int = 5, amplitude: float = 0.1, lmax: int = 4):
+    """BASELINE config 5 surface: icosphere vertices displaced radially to
+    r = 1 + amplitude * sum_{l<=lmax} a_lm Y_lm, a_lm ~ N(0,1)/(l+1) (seeded)."""
+    v, f = icosphere(subdivisions)
+    theta = np.arccos(np.clip(v[:, 2], -1.0, 1.0))
+    phi = np.arctan2(v[:, 1], v[:, 0])
+    g = SplitMix64(seed)
+    r = np.ones(v.shape[0])
+    for l in range(lmax + 1):
+        for m in range(-l, l + 1):
+            r += amplitude * (g.normal() / (l + 1)) * real_sph_harm(l, m, theta, phi)
+    return v * r[:, None], f
+
+
+def write_obj(path: str, verts: np.ndarray, faces: np.ndarray) -> None:
+    """Wavefront OBJ (1-based faces), %.17g vertices (exact round trip)."""
+    with open(path, "w") as fh:
+        fh.write("".join(f"v {x:.17g} {y:.17g} {z:.17g}\n" for x, y, z in verts))
+        fh.write("".join(f"f {a + 1} {b + 1} {c + 1}\n" for a, b, c in faces))
