@@ -399,47 +399,50 @@ __global__ void __launch_bounds__(kFactorThreads) k_factor(const int* __restrict
                     Yj[p * kTS + r] = yj;
                 }
                 __syncthreads();
-                const int ty = tid / 16, tx = tid % 16;  // rows ty*4.., cols tx*4..
-                double aL[4][4], aU[4][4];
+                // FP64 tensor cores: warp w owns the 8-row band w of the tile and all
+                // eight 8-column blocks; mma.m8n8k4 over the panel width
+                // (k chunks of 4; rows p >= kb of the staged panels are zero).
+                const int warp = tid >> 5, lane = tid & 31;
+                const int lr = lane >> 2, lk = lane & 3;
+                double cL[8][2], cU[8][2];
 #pragma unroll
-                for (int a = 0; a < 4; ++a)
+                for (int cb = 0; cb < 8; ++cb) cL[cb][0] = cL[cb][1] = cU[cb][0] = cU[cb][1] = 0.0;
+                for (int kc = 0; kc < kb; kc += 4) {
+                    const int p = kc + lk;
+                    const double ax = Xi[p * kTS + warp * 8 + lr];  // A(row, k) = X_i
+                    const double ay = Yi[p * kTS + warp * 8 + lr];  // A(row, k) = Y_i
 #pragma unroll
-                    for (int b = 0; b < 4; ++b) aL[a][b] = aU[a][b] = 0.0;
-                for (int p = 0; p < kb; ++p) {
-                    double xr[4], yr[4], yc[4], xc[4];
-#pragma unroll
-                    for (int a = 0; a < 4; ++a) {
-                        xr[a] = Xi[p * kTS + ty * 4 + a];
-                        yr[a] = Yi[p * kTS + ty * 4 + a];
-                        yc[a] = Yj[p * kTS + tx * 4 + a];
-                        xc[a] = Xj[p * kTS + tx * 4 + a];
+                    for (int cb = 0; cb < 8; ++cb) {
+                        const double by = Yj[p * kTS + cb * 8 + lr];  // B(k, col) = Y_j^T
+                        const double bx = Xj[p * kTS + cb * 8 + lr];  // B(k, col) = X_j^T
+                        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                                     : "+d"(cL[cb][0]), "+d"(cL[cb][1])
+                                     : "d"(ax), "d"(by));
+                        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                                     : "+d"(cU[cb][0]), "+d"(cU[cb][1])
+                                     : "d"(ay), "d"(bx));
                     }
-#pragma unroll
-                    for (int a = 0; a < 4; ++a)
-#pragma unroll
-                        for (int b = 0; b < 4; ++b) {
-                            aL[a][b] = fma(xr[a], yc[b], aL[a][b]);
-                            aU[a][b] = fma(yr[a], xc[b], aU[a][b]);
-                        }
                 }
+                {
+                    const int gi = i0 + warp * 8 + lr;
+                    if (gi <= R) {
+                        const int f = S.first[gi];
+                        const std::int64_t ro = S.roff[gi] - f;
 #pragma unroll
-                for (int a = 0; a < 4; ++a) {
-                    const int gi = i0 + ty * 4 + a;
-                    if (gi > R) continue;
-                    const int f = S.first[gi];
-                    const std::int64_t ro = S.roff[gi] - f;
+                        for (int cb = 0; cb < 8; ++cb)
 #pragma unroll
-                    for (int b = 0; b < 4; ++b) {
-                        const int gc = j0 + tx * 4 + b;
-                        if (gc > R) continue;
-                        if (gc < gi) {
-                            if (gc >= f) {
-                                S.L[ro + gc] -= aL[a][b];
-                                S.U[ro + gc] -= aU[a][b];
+                            for (int e = 0; e < 2; ++e) {
+                                const int gc = j0 + cb * 8 + 2 * lk + e;
+                                if (gc > R) continue;
+                                if (gc < gi) {
+                                    if (gc >= f) {
+                                        S.L[ro + gc] -= cL[cb][e];
+                                        S.U[ro + gc] -= cU[cb][e];
+                                    }
+                                } else if (gc == gi) {
+                                    S.diag[gi] -= cL[cb][e];
+                                }
                             }
-                        } else if (gc == gi) {
-                            S.diag[gi] -= aL[a][b];
-                        }
                     }
                 }
             }

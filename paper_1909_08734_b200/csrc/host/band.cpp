@@ -1,6 +1,7 @@
 // Band construction (restates proj/include/cpdd/band.hpp:78-182 and
 // proj/include/cpdd/interp.hpp:35-91; see band.hpp here).
 #include "band.hpp"
+#include "decomp.hpp"
 
 #include <algorithm>
 #include <deque>
@@ -116,34 +117,55 @@ struct Node {
 };
 
 template <int D>
-void close_stencils(const Surface<D>& surface, double h, int p, std::vector<Node<D>>& act,
-                    LatticeMap& amap) {
-    // closure under CP stencils (band.hpp:124-142); the final set is the
-    // least closed superset, independent of visiting order
+void close_stencils(const Surface<D>& surface, double h, int p, std::vector<Node<D>>& act, LatticeMap& amap,
+                    int workers) {
+    // closure under CP stencils (band.hpp:124-142): the final set is the
+    // least closed superset, independent of visiting order, so it is built in
+    // rounds -- check the newest nodes' stencils in parallel, add what is
+    // missing (their CPs in parallel), repeat until nothing is added.
     const int pp = p + 1;
     int count = 1;
     for (int a = 0; a < D; ++a) count *= pp;
-    for (std::size_t w = 0; w < act.size(); ++w) {
-        const Stencil1D<D> s = stencil_of<D>(act[w].cp.cp, h, p);
-        for (int k = 0; k < count; ++k) {
-            Ix<D> q;
-            int rem = k;
-            for (int a = 0; a < D; ++a) {
-                q[a] = s.base[a] + rem % pp;
-                rem /= pp;
+    std::size_t begin = 0;
+    while (begin < act.size()) {
+        const std::size_t end = act.size();
+        const int n = static_cast<int>(end - begin);
+        const int chunk = 4096;
+        const int nch = (n + chunk - 1) / chunk;
+        std::vector<std::vector<Ix<D>>> missing(static_cast<std::size_t>(nch));
+        parallel_for(nch, workers, [&](int c, int) {
+            const std::size_t e = std::min(end, begin + static_cast<std::size_t>(c + 1) * chunk);
+            for (std::size_t w = begin + static_cast<std::size_t>(c) * chunk; w < e; ++w) {
+                const Stencil1D<D> s = stencil_of<D>(act[w].cp.cp, h, p);
+                for (int k = 0; k < count; ++k) {
+                    Ix<D> q;
+                    int rem = k;
+                    for (int a = 0; a < D; ++a) {
+                        q[a] = s.base[a] + rem % pp;
+                        rem /= pp;
+                    }
+                    if (amap.find(LatticeMap::pack(q.data(), D)) < 0) missing[static_cast<std::size_t>(c)].push_back(q);
+                }
             }
-            const std::uint64_t key = LatticeMap::pack(q.data(), D);
-            if (amap.find(key) >= 0) continue;
-            amap.insert(key, static_cast<std::int64_t>(act.size()));
-            act.push_back({q, surface.closest_point(index_to_point<D>(q, h))});
-        }
+        });
+        std::vector<Ix<D>> add;
+        for (auto& m : missing)
+            for (const auto& q : m)
+                if (amap.insert(LatticeMap::pack(q.data(), D), static_cast<std::int64_t>(end + add.size())))
+                    add.push_back(q);
+        std::vector<CpResult<D>> cps(add.size());
+        parallel_for(static_cast<int>(add.size()), workers, [&](int k, int) {
+            cps[static_cast<std::size_t>(k)] = surface.closest_point(index_to_point<D>(add[static_cast<std::size_t>(k)], h));
+        });
+        for (std::size_t k = 0; k < add.size(); ++k) act.push_back({add[k], cps[k]});
+        begin = end;
     }
 }
 
 }  // namespace
 
 template <int D>
-Band<D> build_band_tube(const Surface<D>& surface, double h, int p, double tube_radius) {
+Band<D> build_band_tube(const Surface<D>& surface, double h, int p, double tube_radius, int workers) {
     if (h <= 0) throw ConfigError("grid spacing h must be positive");
     if (p < 1) throw ConfigError("interpolation degree must be at least 1");
     Band<D> g;
@@ -151,27 +173,41 @@ Band<D> build_band_tube(const Surface<D>& surface, double h, int p, double tube_
     g.p = p;
     g.tube_radius = tube_radius > 0 ? tube_radius : stencil_reach<D>(h, p);
 
-    // flood fill from the node nearest a surface sample (band.hpp:158-176)
+    // flood fill from the node nearest a surface sample (band.hpp:158-176),
+    // level-synchronous: the closest points of a whole BFS level are computed
+    // in parallel, then the level is expanded serially.  The accepted set is
+    // the connected component of {dist <= radius} containing the seed, as in
+    // the reference's queue order (finalize sorts, so order is immaterial).
     std::vector<Node<D>> act;
     LatticeMap amap, seen;
-    std::deque<Ix<D>> work;
     const Ix<D> seed = nearest_node<D>(surface.sample_point(), h);
-    work.push_back(seed);
     seen.insert(LatticeMap::pack(seed.data(), D), 0);
+    std::vector<Ix<D>> level{seed}, next;
+    std::vector<CpResult<D>> cps;
     Ix<D> nbr[2 * D];
-    while (!work.empty()) {
-        const Ix<D> ix = work.front();
-        work.pop_front();
-        const CpResult<D> cp = surface.closest_point(index_to_point<D>(ix, h));
-        if (cp.dist > g.tube_radius) continue;
-        amap.insert(LatticeMap::pack(ix.data(), D), static_cast<std::int64_t>(act.size()));
-        act.push_back({ix, cp});
-        neighbors_of<D>(ix, nbr);
-        for (int k = 0; k < 2 * D; ++k)
-            if (seen.insert(LatticeMap::pack(nbr[k].data(), D), 0)) work.push_back(nbr[k]);
+    while (!level.empty()) {
+        cps.resize(level.size());
+        const int nl = static_cast<int>(level.size());
+        const int chunk = 2048;
+        parallel_for((nl + chunk - 1) / chunk, workers, [&](int c, int) {
+            const int e = std::min(nl, (c + 1) * chunk);
+            for (int q = c * chunk; q < e; ++q)
+                cps[static_cast<std::size_t>(q)] = surface.closest_point(index_to_point<D>(level[static_cast<std::size_t>(q)], h));
+        });
+        next.clear();
+        for (int q = 0; q < nl; ++q) {
+            if (cps[static_cast<std::size_t>(q)].dist > g.tube_radius) continue;
+            const Ix<D>& ix = level[static_cast<std::size_t>(q)];
+            amap.insert(LatticeMap::pack(ix.data(), D), static_cast<std::int64_t>(act.size()));
+            act.push_back({ix, cps[static_cast<std::size_t>(q)]});
+            neighbors_of<D>(ix, nbr);
+            for (int k = 0; k < 2 * D; ++k)
+                if (seen.insert(LatticeMap::pack(nbr[k].data(), D), 0)) next.push_back(nbr[k]);
+        }
+        level.swap(next);
     }
     if (act.empty()) throw ConfigError("band is empty: grid spacing too large for the surface");
-    close_stencils<D>(surface, h, p, act, amap);
+    close_stencils<D>(surface, h, p, act, amap, workers);
 
     // finalize (band.hpp:78-118): lexicographic actives, then ghosts
     std::sort(act.begin(), act.end(), [](const Node<D>& a, const Node<D>& b) { return a.ix < b.ix; });
@@ -201,13 +237,20 @@ Band<D> build_band_tube(const Surface<D>& surface, double h, int p, double tube_
         g.normal[k] = act[k].cp.normal;
         g.dist[k] = act[k].cp.dist;
     }
-    for (std::size_t k = 0; k < gh.size(); ++k) {
-        const std::size_t c = act.size() + k;
-        const CpResult<D> r = surface.closest_point(index_to_point<D>(gh[k], h));
-        g.ix[c] = gh[k];
-        g.cp[c] = r.cp;
-        g.normal[c] = r.normal;
-        g.dist[c] = r.dist;
+    {
+        const int ng = static_cast<int>(gh.size());
+        const int chunk = 2048;
+        parallel_for((ng + chunk - 1) / chunk, workers, [&](int cc, int) {
+            const int e = std::min(ng, (cc + 1) * chunk);
+            for (int k = cc * chunk; k < e; ++k) {
+                const std::size_t c = act.size() + static_cast<std::size_t>(k);
+                const CpResult<D> r = surface.closest_point(index_to_point<D>(gh[static_cast<std::size_t>(k)], h));
+                g.ix[c] = gh[static_cast<std::size_t>(k)];
+                g.cp[c] = r.cp;
+                g.normal[c] = r.normal;
+                g.dist[c] = r.dist;
+            }
+        });
     }
     g.map.reserve(nb);
     for (std::size_t k = 0; k < nb; ++k)
@@ -220,7 +263,7 @@ Band<D> build_band_tube(const Surface<D>& surface, double h, int p, double tube_
     return g;
 }
 
-template Band<2> build_band_tube<2>(const Surface<2>&, double, int, double);
-template Band<3> build_band_tube<3>(const Surface<3>&, double, int, double);
+template Band<2> build_band_tube<2>(const Surface<2>&, double, int, double, int);
+template Band<3> build_band_tube<3>(const Surface<3>&, double, int, double, int);
 
 }  // namespace cpddg

@@ -111,6 +111,6 @@ inline void neighbors_of(const Ix<D>& ix, Ix<D>* out) {
  *  radius stencil_reach = (p+1)/2 sqrt(d) h; a positive value overrides it
  *  (BASELINE.json states sqrt(13) h / sqrt(17) h). */
 template <int D>
-Band<D> build_band_tube(const Surface<D>& surface, double h, int p, double tube_radius = 0.0);
+Band<D> build_band_tube(const Surface<D>& surface, double h, int p, double tube_radius = 0.0, int workers = 0);
 
 }  // namespace cpddg

@@ -51,7 +51,7 @@ void create_impl(const cpddg_problem_desc& d, cpddg_setup* s) {
             default: throw ConfigError("surface is not available in 3D");
         }
     }
-    I->band = build_band_tube<D>(S, d.h, d.p, d.tube_radius);
+    I->band = build_band_tube<D>(S, d.h, d.p, d.tube_radius, d.workers);
     I->E = build_extension<D>(I->band, d.workers);
     I->A = assemble_helmholtz<D>(I->band, I->E, d.c, d.workers);
 }
