@@ -42,6 +42,14 @@ CASES = {
                                 part="rcb", rhs="sphere"),
     "sphere05_ras_gmres": dict(cfg=dict(surface="sphere", h=0.05, method="ras", mode="gmres", gmres_restart=50,
                                         n_overlap=2, n_subdomains=64), part="rcb", rhs="sphere"),
+    # standard Robin condition (alpha_cross = alpha) at BASELINE config 2
+    "sphere05_oras_std_gmres": dict(cfg=dict(surface="sphere", h=0.05, method="oras", mode="gmres",
+                                             gmres_restart=50, n_overlap=2, n_subdomains=64, alpha=4.0),
+                                    part="rcb", rhs="sphere"),
+    # displaced icosphere (BASELINE config 5 geometry, subdivision 3), TriMesh closest points
+    "trimesh3_oras_gmres": dict(cfg=dict(surface="obj", obj=os.path.join(HERE, "icosphere3.obj"), h=0.05,
+                                         method="oras", mode="gmres", gmres_restart=50, n_overlap=2,
+                                         n_subdomains=16, alpha=4.0, alpha_cross=40.0), part="rcb", rhs="trig"),
     # coarse torus (BASELINE config 4 geometry), seeded trigonometric right-hand side
     "torus04_oras_gmres": dict(cfg=dict(surface="torus", major_radius=1.0, minor_radius=0.4, h=0.04,
                                         method="oras", mode="gmres", gmres_restart=50, n_overlap=2,
@@ -65,8 +73,11 @@ def make_case(name, spec):
     aligned, moves = R.decompose(part)
     Mx = R.pc_apply(x)
     sol = R.solve(b)
+    cfg_store = dict(cfg)
+    if "obj" in cfg_store:
+        cfg_store["obj"] = os.path.basename(cfg_store["obj"])  # resolved against tests/golden/
     np.savez_compressed(os.path.join(HERE, name + ".npz"),
-                        cfg=np.array(repr(cfg)), n_active=na, n_ghost=R.n_ghost,
+                        cfg=np.array(repr(cfg_store)), n_active=na, n_ghost=R.n_ghost,
                         part_in=part, part_aligned=aligned, moves=moves, x=x, Ax=Ax, Mx=Mx, b=b,
                         u=sol["u"], iterations=sol["iterations"], converged=sol["converged"],
                         residuals=sol["residuals"], final_true_residual=sol["final_true_residual"])

@@ -25,7 +25,8 @@ def _setup(name):
     from paper_1909_08734_b200 import api
     g = np.load(os.path.join(GOLDEN, name + ".npz"))
     cfg = ast.literal_eval(str(g["cfg"]))
-    P = api.Problem(cfg["surface"], h=cfg["h"], p=cfg["p"], c=cfg["c"],
+    obj = os.path.join(GOLDEN, cfg["obj"]) if "obj" in cfg else None
+    P = api.Problem(cfg["surface"], h=cfg["h"], p=cfg["p"], c=cfg["c"], obj_path=obj,
                     major_radius=cfg.get("major_radius", 2.0 / 3.0), minor_radius=cfg.get("minor_radius", 1.0 / 3.0))
     assert P.n_active == int(g["n_active"]) and P.n_ghost == int(g["n_ghost"])
     aligned, moves = P.decompose(g["part_in"], cfg["n_overlap"], cfg["method"], cfg.get("alpha", 1.0),

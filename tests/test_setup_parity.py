@@ -36,17 +36,24 @@ CASES = [
     ("sphere", dict(h=0.1, p=3), "rcb", 16, 2, "oras", 4.0, 40.0),
     ("sphere", dict(h=0.1, p=2), "rcb", 8, 3, "ras", 1.0, -1.0),
     ("torus", dict(h=0.06, p=3, major_radius=1.0, minor_radius=0.4), "rcb", 16, 2, "oras", 2.0, 20.0),
+    ("obj", dict(h=0.1, p=3), "rcb", 8, 2, "oras", 4.0, 40.0),
 ]
 
 
 @needs_ref
 @pytest.mark.parametrize("surf,geo,pk,ns,no,meth,alpha,ax", CASES)
 def test_setup_bit_exact_vs_reference(surf, geo, pk, ns, no, meth, alpha, ax):
+    import os
+
     import ref
+    from conftest import GOLDEN
     cfg = dict(surface=surf, c=1.0, method=meth, n_overlap=no, n_subdomains=ns, alpha=alpha, alpha_cross=ax, **geo)
+    obj = os.path.join(GOLDEN, "icosphere3.obj") if surf == "obj" else None
+    if obj:
+        cfg["obj"] = obj
     R = ref.RefProblem(cfg, workers=4)
     P = api.Problem(surf, h=geo["h"], p=geo["p"], c=1.0, major_radius=geo.get("major_radius", 2 / 3),
-                    minor_radius=geo.get("minor_radius", 1 / 3), workers=4)
+                    minor_radius=geo.get("minor_radius", 1 / 3), obj_path=obj, workers=4)
     assert (P.n_active, P.n_ghost) == (R.n_active, R.n_ghost)
     B, RB = P.band(), R.band()
     for k in ("ix", "cp", "normal", "dist"):
