@@ -902,6 +902,23 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
         for (int j = 0; j < n_sub; ++j)
             cost[static_cast<std::size_t>(j)] = (j + 1 < n_sub ? ebase[static_cast<std::size_t>(j) + 1] : ebs) - ebase[static_cast<std::size_t>(j)];
         std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[static_cast<std::size_t>(a)] > cost[static_cast<std::size_t>(b)]; });
+        // SM balance for the solve (2 resident CTAs per SM, blocks dealt to SMs
+        // round-robin): with n_sub = S + P subdomains on S SMs, the S - P SMs that
+        // get one CTA take the largest systems, and each remaining SM pairs a
+        // large system with a small one.
+        const int S = sm_count();
+        const char* bal = std::getenv("CPDDG_BALANCE");
+        if (n_sub > S && n_sub <= 2 * S && !(bal && std::string(bal) == "0")) {
+            const int P = n_sub - S;          // SMs with two CTAs
+            const int singles = S - P;        // SMs with one CTA
+            std::vector<int> sorted = order, o(static_cast<std::size_t>(n_sub));
+            for (int k = 0; k < singles; ++k) o[static_cast<std::size_t>(P + k)] = sorted[static_cast<std::size_t>(k)];
+            for (int i = 0; i < P; ++i) {
+                o[static_cast<std::size_t>(i)] = sorted[static_cast<std::size_t>(singles + i)];
+                o[static_cast<std::size_t>(S + i)] = sorted[static_cast<std::size_t>(n_sub - 1 - i)];
+            }
+            order = o;
+        }
     }
     pc->n_rows.upload(n_rows);
     pc->vbase.upload(vbase);
