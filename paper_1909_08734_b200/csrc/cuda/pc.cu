@@ -726,27 +726,37 @@ __device__ __forceinline__ void upper_solve_cols(int n, const int* __restrict__ 
                 const int cb1 = min(RB, n - (c0 + RB));
                 int jmin = c0;
                 for (int c = 0; c < cb1; ++c) jmin = min(jmin, cf[nxt][c]);
-                // two threads per row (adjacent lanes), 15 columns each: all
-                // loads of a thread are issued before its FMAs
-                constexpr int HC = RB / 2;
-                const int half = ptid & 1, pr = ptid >> 1, npairs = pthreads >> 1;
-                for (int base = jmin; base < c0; base += npairs) {
-                    const int jr = base + pr;
-                    const bool rowok = jr < c0;
-                    double a[HC];
+                // one thread per row pair (16-byte loads down each column: columns
+                // start at even rows and c0 is even), all RB columns in three
+                // batches of ten loads issued before their FMAs
+                for (int base = jmin & ~1; base < c0; base += 2 * pthreads) {
+                    const int jr = base + 2 * ptid;
+                    const bool ok = jr < c0;
+                    double acc0 = 0.0, acc1 = 0.0;
 #pragma unroll
-                    for (int u = 0; u < HC; ++u) {
-                        const int c = half * HC + u;
-                        a[u] = (rowok && c < cb1 && jr >= cf[nxt][c]) ? __ldcs(V + cro[nxt][c] + (jr - cf[nxt][c])) : 0.0;
-                    }
-                    double acc = 0.0;
+                    for (int cb = 0; cb < RB; cb += 10) {
+                        double2 a[10];
 #pragma unroll
-                    for (int u = 0; u < HC; ++u) {
-                        const int c = half * HC + u;
-                        if (c < cb1) acc = fma(a[u], y[c0 + RB + c], acc);
+                        for (int u = 0; u < 10; ++u) {
+                            const int c = cb + u;
+                            a[u] = (ok && c < cb1 && jr >= cf[nxt][c])
+                                       ? __ldcs(reinterpret_cast<const double2*>(V + cro[nxt][c] + (jr - cf[nxt][c])))
+                                       : make_double2(0.0, 0.0);
+                        }
+#pragma unroll
+                        for (int u = 0; u < 10; ++u) {
+                            const int c = cb + u;
+                            if (c < cb1) {
+                                const double xc = y[c0 + RB + c];
+                                acc0 = fma(a[u].x, xc, acc0);
+                                acc1 = fma(a[u].y, xc, acc1);
+                            }
+                        }
                     }
-                    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-                    if (rowok && half == 0) y[jr] -= acc;
+                    if (ok) {
+                        y[jr] -= acc0;
+                        y[jr + 1] -= acc1;
+                    }
                 }
             }
             if (K >= 1) {
