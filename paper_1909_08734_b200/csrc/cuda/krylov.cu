@@ -133,6 +133,45 @@ __global__ void __launch_bounds__(kRedThreads) k_mgs_all(int n, int m, const dou
         for (int i = i0; i < n; i += stride) vnext[i] = w[i] / sub;
 }
 
+/** Single-CTA variant of k_mgs_all for small systems (n below a few 10^4):
+ *  the same passes and fixed-order sums with __syncthreads instead of grid
+ *  barriers, so a whole Arnoldi orthogonalisation costs a few microseconds. */
+template <int NT>
+__global__ void __launch_bounds__(NT) k_mgs_block(int n, int m, const double* const* __restrict__ V,
+                                                  double* __restrict__ w, double* __restrict__ vnext,
+                                                  double* hout, double* wn0) {
+    __shared__ double sh[NT / 32];
+    __shared__ double hb;
+    double hprev = 0.0;
+    for (int pass = 0; pass <= m + 1; ++pass) {
+        const double* vp = pass > 0 ? V[pass - 1] : nullptr;
+        const double* vn = pass <= m ? V[pass] : nullptr;
+        double a1 = 0.0, a2 = 0.0;
+        for (int i = threadIdx.x; i < n; i += NT) {
+            double wi = w[i];
+            if (vp) {
+                wi -= hprev * vp[i];
+                w[i] = wi;
+            }
+            a1 = fma(vn ? vn[i] : wi, wi, a1);
+            if (pass == 0) a2 = fma(wi, wi, a2);
+        }
+        const double t1 = block_sum<NT>(a1, sh);
+        const double t2 = pass == 0 ? block_sum<NT>(a2, sh) : 0.0;
+        if (threadIdx.x == 0) {
+            hb = t1;
+            hout[pass] = t1;
+            if (pass == 0) *wn0 = t2;
+        }
+        __syncthreads();
+        hprev = hb;
+        __syncthreads();
+    }
+    const double sub = sqrt(hprev);
+    if (vnext)
+        for (int i = threadIdx.x; i < n; i += NT) vnext[i] = w[i] / sub;
+}
+
 __global__ void k_scale(int n, const double* __restrict__ src, double s, double* __restrict__ dst) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = src[i] / s;
 }
@@ -239,6 +278,8 @@ struct KernelTimer {
     }
 };
 
+constexpr int kSmallMgs = 16384;  // single-CTA orthogonalisation below this size
+
 struct Workspace {
     int n;
     cudaStream_t st;
@@ -260,7 +301,10 @@ struct Workspace {
     void reserve(int cap) {
         if (kc.scal.size() < static_cast<std::size_t>(cap) + 4) kc.scal.alloc(static_cast<std::size_t>(cap) + 4);
         if (kc.yd.size() < static_cast<std::size_t>(cap)) kc.yd.alloc(static_cast<std::size_t>(cap));
-        if (kc.vptr.size() < static_cast<std::size_t>(cap)) kc.vptr.alloc(static_cast<std::size_t>(cap));
+        if (kc.vptr.size() < static_cast<std::size_t>(cap)) {
+            kc.vptr.alloc(static_cast<std::size_t>(cap) + 64);
+            kc.vptr_valid = 0;
+        }
         if (kc.host_cap < cap + 4) {
             if (kc.host) cudaFreeHost(kc.host);
             CPDDG_CUDA(cudaMallocHost(&kc.host, sizeof(double) * (cap + 4)));
@@ -289,13 +333,23 @@ struct Workspace {
         }
         const std::size_t need = static_cast<std::size_t>(2 * coop_grid) * (m + 2);
         if (mgs_partials.size() < need) mgs_partials.alloc(std::max(need, static_cast<std::size_t>(2 * coop_grid) * 64));
-        // basis pointer table (V_0..V_m) on the device
-        std::vector<const double*> vp(static_cast<std::size_t>(m) + 1);
-        for (int k = 0; k <= m; ++k) vp[static_cast<std::size_t>(k)] = kc.V[static_cast<std::size_t>(k)].get();
-        if (kc.vptr.size() < vp.size() + 64) kc.vptr.alloc(vp.size() + 64);
-        CPDDG_CUDA(cudaMemcpyAsync(kc.vptr.get(), vp.data(), sizeof(double*) * vp.size(), cudaMemcpyHostToDevice, st));
+        // basis pointer table (V_0..V_m) on the device: basis buffers never
+        // move once allocated, so the table is uploaded only when it grows
+        if (kc.vptr_valid < m + 1) {
+            std::vector<const double*> vp(kc.V.size());
+            for (std::size_t k = 0; k < kc.V.size(); ++k) vp[k] = kc.V[k].get();
+            if (kc.vptr.size() < vp.size()) kc.vptr.alloc(vp.size() + 64);
+            CPDDG_CUDA(cudaMemcpy(kc.vptr.get(), vp.data(), sizeof(double*) * vp.size(), cudaMemcpyHostToDevice));
+            kc.vptr_valid = static_cast<int>(vp.size());
+        }
         int nn = n, mm = m;
         const double* const* vpd = kc.vptr.get();
+        if (n <= kSmallMgs) {
+            k_mgs_block<1024><<<1, 1024, 0, st>>>(nn, mm, vpd, w, vnext, hout, wn0);
+            CPDDG_CUDA(cudaGetLastError());
+            ++launches;
+            return;
+        }
         double* part = mgs_partials.get();
         void* args[] = {&nn, &mm, &vpd, &w, &vnext, &part, &hout, &wn0};
         CPDDG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_mgs_all), dim3(coop_grid), dim3(kRedThreads),
@@ -398,14 +452,13 @@ static void gmres(cpddg_op* op, cpddg_pc* pc, const double* b, double* u, const 
             ws.launches += 2;
             // MGS, all m+2 passes and the next basis vector in one cooperative launch
             double* vnext = (m + 1 <= cycle) ? basis(m + 1) : nullptr;
-            ws.mgs_all(m, w.get(), vnext, hd, nd + 0);
-            CPDDG_CUDA(cudaMemcpyAsync(hh.p, hd, sizeof(double) * (m + 2), cudaMemcpyDeviceToHost, st));
-            CPDDG_CUDA(cudaMemcpyAsync(hh.p + cap, nd, sizeof(double), cudaMemcpyDeviceToHost, st));
+            ws.mgs_all(m, w.get(), vnext, hd, hd + m + 2);
+            CPDDG_CUDA(cudaMemcpyAsync(hh.p, hd, sizeof(double) * (m + 3), cudaMemcpyDeviceToHost, st));
             CPDDG_CUDA(cudaStreamSynchronize(st));
             kt.collect();
             std::vector<double> h(hh.p, hh.p + m + 2);
             h[static_cast<std::size_t>(m) + 1] = std::sqrt(h[static_cast<std::size_t>(m) + 1]);
-            const double wnorm0 = std::sqrt(hh.p[cap]);
+            const double wnorm0 = std::sqrt(hh.p[m + 2]);
             const double subdiag = h[static_cast<std::size_t>(m) + 1];
             check_finite(subdiag, "gmres basis norm");
             for (int i = 0; i < m; ++i) {

@@ -13,6 +13,7 @@ struct KrylovCache {
     std::vector<cpddg::DevBuf<double>> V;
     cpddg::DevBuf<double> w, r, tmp, yd, scal;
     cpddg::DevBuf<const double*> vptr;
+    int vptr_valid = 0;  // entries of vptr that hold the current basis pointers
     double* host = nullptr;  // pinned scratch
     int host_cap = 0;
     cpddg::ReduceWork red;
