@@ -352,7 +352,7 @@ def main():
             "setup_s": {"problem": t_problem, "decompose": t_decomp, "factor_and_upload": t_locals,
                         "device_factor": pcs["factor_seconds"], "host_analyse": pcs["analyse_seconds"]},
             "pc": {k: pcs[k] for k in ("factor_entries", "profile_entries", "factor_bytes", "n_rows_total",
-                                       "max_rows", "n_reduced")},
+                                       "max_rows", "n_reduced", "max_probe_residual")},
             "pc_stored_over_profile": pcs["factor_entries"] / pcs["profile_entries"],
             "kernel_ms": {"pc_apply_avg": 1e3 * avg_pc, "op_apply_avg": 1e3 * op_s / max(op_n, 1)},
             "op_roofline_GBs": op_alg / (op_s / max(op_n, 1)) / 1e9 if op_n else None,

@@ -240,7 +240,7 @@ class SchwarzPreconditioner:
 
     @classmethod
     def from_problem(cls, P: Problem, workers: int = 0) -> "SchwarzPreconditioner":
-        opt = _lib.cpddg_pc_options(workers=workers, check_residual=0)
+        opt = _lib.cpddg_pc_options(workers=workers, check_residual=1)
         h = C.c_void_p()
         check(lib().cpddg_pc_create_from_setup(P.handle, C.byref(opt), C.byref(h)))
         return cls(h, P.n_active)
@@ -264,7 +264,7 @@ class SchwarzPreconditioner:
                                              scatter_local=arrs[1].ctypes.data,
                                              scatter_global=arrs[2].ctypes.data, row_ptr=arrs[3].ctypes.data,
                                              col=arrs[4].ctypes.data, val=arrs[5].ctypes.data)
-        opt = _lib.cpddg_pc_options(workers=workers, check_residual=0)
+        opt = _lib.cpddg_pc_options(workers=workers, check_residual=1)
         h = C.c_void_p()
         check(lib().cpddg_pc_create(int(n_global), len(locals_), descs, C.byref(opt), C.byref(h)))
         return cls(h, n_global)

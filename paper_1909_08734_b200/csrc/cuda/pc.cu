@@ -51,6 +51,8 @@ constexpr int SB = 32;    // solve block
 struct HostSub {
     int n = 0;
     bool reduced = false;
+    std::vector<int> inv;      // local (old) index -> factor order
+    std::vector<double> probe; // b = A_sys x_probe in factor order
     std::vector<int> first, rlast, gidx, sidx;
     std::vector<std::int64_t> roff;
     std::vector<double> L, U, diag;
@@ -194,6 +196,16 @@ HostSub analyse(const cpddg_local_desc& d, int n_global) {
             else
                 S.U[static_cast<std::size_t>(S.roff[static_cast<std::size_t>(pj)] + (pi - S.first[static_cast<std::size_t>(pj)]))] += v;
         }
+    // factor probe: b = A_sys x with x_i = 1 + (i mod 7) / 8 in factor order
+    S.probe.assign(static_cast<std::size_t>(n), 0.0);
+    for (int r = 0; r < n; ++r)
+        for (std::int64_t k = rp[r]; k < rp[r + 1]; ++k) {
+            const int c = d.col[k];
+            if (c >= n) continue;
+            const int pc_ = inv[static_cast<std::size_t>(c)];
+            S.probe[static_cast<std::size_t>(inv[static_cast<std::size_t>(r)])] += d.val[k] * (1.0 + (pc_ % 7) / 8.0);
+        }
+    S.inv = inv;
     S.gidx.assign(static_cast<std::size_t>(n), -1);
     S.sidx.assign(static_cast<std::size_t>(n), -1);
     for (int o = 0; o < std::min(n, d.n_overlap); ++o) {
@@ -774,7 +786,9 @@ __device__ __forceinline__ void upper_solve_cols(int n, const int* __restrict__ 
     }
 }
 
-// MODE 0: full apply; 1: forward only; 2: backward only (profiling).
+// MODE 0: full apply; 1: forward only; 2: backward only (profiling);
+// 3: factor probe -- r / z are per-row arrays in factor order (vbase
+//    indexing) instead of global vectors, no gather / scatter.
 // UROWS: backward on reversed U rows (k_reverse_u) instead of U columns.
 template <int MODE, bool UROWS>
 __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const int* __restrict__ order,
@@ -803,8 +817,12 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const int* __restric
     const int tid = threadIdx.x;
 
     for (int p = tid; p < n; p += blockDim.x) {
-        const int g = __ldg(gidx_all + vb + p);
-        y[p] = g >= 0 ? __ldg(r + g) : 0.0;
+        if (MODE == 3) {
+            y[p] = r[vb + p];
+        } else {
+            const int g = __ldg(gidx_all + vb + p);
+            y[p] = g >= 0 ? __ldg(r + g) : 0.0;
+        }
     }
     __syncthreads();
     // forward: L y = b (unit lower)
@@ -820,6 +838,10 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const int* __restric
         if (MODE != 1)
             lower_solve(n, ufirst_all + vb, uroff_all + vb, U_all + ubase[j], drev_all + vb, y, part, tri);
         for (int p = tid; p < n; p += blockDim.x) {
+            if (MODE == 3) {
+                z[vb + p] = y[n - 1 - p];
+                continue;
+            }
             const int s = __ldg(sidx_all + vb + p);
             if (s >= 0) {
                 const double v = y[n - 1 - p];
@@ -832,6 +854,10 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const int* __restric
         __shared__ long long cro[3][RB];
         if (MODE != 1) upper_solve_cols(n, first_all + vb, roff_all + vb, U_all + ebase[j], diag_all + vb, y, tri, cf, cro, pf);
         for (int p = tid; p < n; p += blockDim.x) {
+            if (MODE == 3) {
+                z[vb + p] = y[p];
+                continue;
+            }
             const int s = __ldg(sidx_all + vb + p);
             if (s >= 0) z[s] = accumulate ? z[s] + y[p] : y[p];
         }
@@ -846,8 +872,8 @@ void append(std::vector<T>& dst, const std::vector<T>& src) {
 }  // namespace
 
 void pc_apply_mode(const cpddg_pc* pc, const double* r, double* z, bool accumulate, int mode, cudaStream_t st) {
-    auto kern = pc->urows ? (mode == 1 ? k_solve<1, true> : mode == 2 ? k_solve<2, true> : k_solve<0, true>)
-                          : (mode == 1 ? k_solve<1, false> : mode == 2 ? k_solve<2, false> : k_solve<0, false>);
+    auto kern = pc->urows ? (mode == 1 ? k_solve<1, true> : mode == 2 ? k_solve<2, true> : mode == 3 ? k_solve<3, true> : k_solve<0, true>)
+                          : (mode == 1 ? k_solve<1, false> : mode == 2 ? k_solve<2, false> : mode == 3 ? k_solve<3, false> : k_solve<0, false>);
     kern<<<pc->n_sub, kSolveThreads, pc->solve_smem, st>>>(
         pc->order.get(), pc->n_rows.get(), pc->vbase.get(), pc->ebase.get(), pc->first.get(), pc->roff.get(),
         pc->dinv.get(), pc->L.get(), pc->U.get(), pc->gidx.get(), pc->sidx.get(), r, z, accumulate ? 1 : 0,
@@ -878,7 +904,8 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
     pc->n_sub = n_sub;
     std::vector<int> n_rows, first, rlast, gidx, sidx;
     std::vector<std::int64_t> vbase, ebase, roff;
-    std::vector<double> L, U, diag;
+    std::vector<double> L, U, diag, probe_all;
+    std::vector<std::vector<int>> invs;
     std::int64_t vb = 0, ebs = 0;
     for (auto& S : subs) {
         n_rows.push_back(S.n);
@@ -901,6 +928,8 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
         append(sidx, S.sidx);
         append(roff, S.roff);
         append(diag, S.diag);
+        append(probe_all, S.probe);
+        invs.push_back(std::move(S.inv));
         append(L, S.L);
         append(U, S.U);
         S = HostSub{};
@@ -1009,9 +1038,45 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
     pc->solve_smem = static_cast<int>(sizeof(double)) * pc->max_rows;
     if (const char* e = std::getenv("CPDDG_BWD_PREFETCH")) pc->bwd_prefetch = std::atoi(e);
     if (pc->solve_smem > 200 * 1024) throw ConfigError("subdomain system too large for the shared-memory solve");
-    for (auto kern : {k_solve<0, false>, k_solve<1, false>, k_solve<2, false>, k_solve<0, true>, k_solve<1, true>,
-                      k_solve<2, true>})
+    for (auto kern : {k_solve<0, false>, k_solve<1, false>, k_solve<2, false>, k_solve<3, false>, k_solve<0, true>,
+                      k_solve<1, true>, k_solve<2, true>, k_solve<3, true>})
         CPDDG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(pc->solve_smem, 1)));
+    // factor probe (cpddg_pc_options::check_residual): solve A_j z = A_j x_probe
+    // on the device for every subdomain and check the residual on the host --
+    // the DirectSolver contract of the reference (residual ~1e-12,
+    // tests/test_transmission.cpp:307-334) made observable.
+    if (opt && opt->check_residual) {
+        DevBuf<double> pb, pz(static_cast<std::size_t>(vb));
+        pb.upload(probe_all);
+        pc_apply_mode(pc.get(), pb.get(), pz.get(), false, 3, nullptr);
+        std::vector<double> z(static_cast<std::size_t>(vb));
+        CPDDG_CUDA(cudaMemcpy(z.data(), pz.get(), z.size() * sizeof(double), cudaMemcpyDeviceToHost));
+        std::vector<double> res(static_cast<std::size_t>(n_sub), 0.0);
+        parallel_for(n_sub, opt->workers, [&](int j, int) {
+            const cpddg_local_desc& d = locals[j];
+            const std::vector<int>& inv = invs[static_cast<std::size_t>(j)];
+            const int n = n_rows[static_cast<std::size_t>(j)];
+            const std::int64_t v0 = vbase[static_cast<std::size_t>(j)];
+            double rmax = 0.0, bmax = 0.0;
+            for (int r = 0; r < n; ++r) {
+                double acc = 0.0;
+                for (std::int64_t k = d.row_ptr[r]; k < d.row_ptr[r + 1]; ++k) {
+                    const int c = d.col[k];
+                    if (c >= n) continue;
+                    acc += d.val[k] * z[static_cast<std::size_t>(v0 + inv[static_cast<std::size_t>(c)])];
+                }
+                const double b = probe_all[static_cast<std::size_t>(v0 + inv[static_cast<std::size_t>(r)])];
+                rmax = std::max(rmax, std::abs(acc - b));
+                bmax = std::max(bmax, std::abs(b));
+            }
+            res[static_cast<std::size_t>(j)] = bmax > 0 ? rmax / bmax : rmax;
+        });
+        pc->max_probe_residual = *std::max_element(res.begin(), res.end());
+        for (int j = 0; j < n_sub; ++j)
+            if (!(res[static_cast<std::size_t>(j)] <= 1e-8))
+                throw DivergenceError("inaccurate factorization of subdomain " + std::to_string(j) +
+                                      " (probe residual " + std::to_string(res[static_cast<std::size_t>(j)]) + ")");
+    }
     // bytes one apply streams: L, U, diag, first, roff per row, gather/scatter maps, r gathers, z writes
     // streamed per apply: L and reversed-U values, diagonal, and the per-row
     // tables (first + offset) of both passes
