@@ -51,11 +51,12 @@ constexpr int SB = 32;    // solve block
 struct HostSub {
     int n = 0;
     bool reduced = false;
+    std::int64_t ne = 0;       // envelope entries per triangle
     std::vector<int> inv;      // local (old) index -> factor order
     std::vector<double> probe; // b = A_sys x_probe in factor order
     std::vector<int> first, rlast, gidx, sidx;
     std::vector<std::int64_t> roff;
-    std::vector<double> L, U, diag;
+
 };
 
 /** Reverse Cuthill-McKee of a symmetric pattern (sorted, no diagonal).
@@ -179,23 +180,6 @@ HostSub analyse(const cpddg_local_desc& d, int n_global) {
         run = std::max(run, maxrow[static_cast<std::size_t>(i)]);
         S.rlast[static_cast<std::size_t>(i)] = std::max(run, i);
     }
-    const std::size_t ne = static_cast<std::size_t>(S.roff[static_cast<std::size_t>(n)]);
-    S.L.assign(ne, 0.0);
-    S.U.assign(ne, 0.0);
-    S.diag.assign(static_cast<std::size_t>(n), 0.0);
-    for (int r = 0; r < n; ++r)
-        for (std::int64_t k = rp[r]; k < rp[r + 1]; ++k) {
-            const int c = d.col[k];
-            if (c >= n) continue;  // eliminated Dirichlet closure column (z_b = 0)
-            const int pi = inv[static_cast<std::size_t>(r)], pj = inv[static_cast<std::size_t>(c)];
-            const double v = d.val[k];
-            if (pi == pj)
-                S.diag[static_cast<std::size_t>(pi)] += v;
-            else if (pj < pi)
-                S.L[static_cast<std::size_t>(S.roff[static_cast<std::size_t>(pi)] + (pj - S.first[static_cast<std::size_t>(pi)]))] += v;
-            else
-                S.U[static_cast<std::size_t>(S.roff[static_cast<std::size_t>(pj)] + (pi - S.first[static_cast<std::size_t>(pj)]))] += v;
-        }
     // factor probe: b = A_sys x with x_i = 1 + (i mod 7) / 8 in factor order
     S.probe.assign(static_cast<std::size_t>(n), 0.0);
     for (int r = 0; r < n; ++r)
@@ -218,8 +202,29 @@ HostSub analyse(const cpddg_local_desc& d, int n_global) {
         if (lo < 0 || lo >= n || g < 0 || g >= n_global) throw InternalError("scatter index out of range");
         S.sidx[static_cast<std::size_t>(inv[static_cast<std::size_t>(lo)])] = g;
     }
+    S.ne = S.roff.back();
     S.roff.pop_back();
     return S;
+}
+
+/** Scatter A_j (the factored system, Dirichlet closure eliminated) into
+ *  envelope storage: L rows, U columns, diagonal (factor order). */
+void scatter_values(const cpddg_local_desc& d, const HostSub& S, double* L, double* U, double* diag) {
+    const int n = S.n;
+    const std::int64_t* rp = d.row_ptr;
+    for (int r = 0; r < n; ++r)
+        for (std::int64_t k = rp[r]; k < rp[r + 1]; ++k) {
+            const int c = d.col[k];
+            if (c >= n) continue;  // eliminated Dirichlet closure column (z_b = 0)
+            const int pi = S.inv[static_cast<std::size_t>(r)], pj = S.inv[static_cast<std::size_t>(c)];
+            const double v = d.val[k];
+            if (pi == pj)
+                diag[pi] += v;
+            else if (pj < pi)
+                L[S.roff[static_cast<std::size_t>(pi)] + (pj - S.first[static_cast<std::size_t>(pi)])] += v;
+            else
+                U[S.roff[static_cast<std::size_t>(pj)] + (pi - S.first[static_cast<std::size_t>(pj)])] += v;
+        }
 }
 
 struct SubPtrs {
@@ -904,7 +909,7 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
     pc->n_sub = n_sub;
     std::vector<int> n_rows, first, rlast, gidx, sidx;
     std::vector<std::int64_t> vbase, ebase, roff;
-    std::vector<double> L, U, diag, probe_all;
+    std::vector<double> probe_all;
     std::vector<std::vector<int>> invs;
     std::int64_t vb = 0, ebs = 0;
     for (auto& S : subs) {
@@ -912,26 +917,39 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
         vbase.push_back(vb);
         ebase.push_back(ebs);
         vb += S.n;
-        ebs += static_cast<std::int64_t>(S.L.size());
+        ebs += S.ne;
         pc->max_rows = std::max(pc->max_rows, S.n);
         pc->n_reduced += S.reduced ? 1 : 0;
     }
     pc->rows_total = vb;
     pc->entries = 2 * ebs + vb;
+    // values: scattered per subdomain into scratch and copied straight into
+    // the device arrays (no host-side concatenation of the factor storage)
+    pc->L.alloc(static_cast<std::size_t>(std::max<std::int64_t>(ebs, 1)));
+    pc->U.alloc(static_cast<std::size_t>(std::max<std::int64_t>(ebs, 1)));
+    pc->diag.alloc(static_cast<std::size_t>(vb));
+    parallel_for(n_sub, opt ? opt->workers : 0, [&](int j, int) {
+        const HostSub& S = subs[static_cast<std::size_t>(j)];
+        std::vector<double> Lb(static_cast<std::size_t>(S.ne), 0.0), Ub(static_cast<std::size_t>(S.ne), 0.0),
+            Db(static_cast<std::size_t>(S.n), 0.0);
+        scatter_values(locals[j], S, Lb.data(), Ub.data(), Db.data());
+        const std::size_t eb = static_cast<std::size_t>(ebase[static_cast<std::size_t>(j)]);
+        const std::size_t v0 = static_cast<std::size_t>(vbase[static_cast<std::size_t>(j)]);
+        if (S.ne) {
+            CPDDG_CUDA(cudaMemcpy(pc->L.get() + eb, Lb.data(), Lb.size() * sizeof(double), cudaMemcpyHostToDevice));
+            CPDDG_CUDA(cudaMemcpy(pc->U.get() + eb, Ub.data(), Ub.size() * sizeof(double), cudaMemcpyHostToDevice));
+        }
+        CPDDG_CUDA(cudaMemcpy(pc->diag.get() + v0, Db.data(), Db.size() * sizeof(double), cudaMemcpyHostToDevice));
+    });
     first.reserve(static_cast<std::size_t>(vb));
-    L.reserve(static_cast<std::size_t>(ebs));
-    U.reserve(static_cast<std::size_t>(ebs));
     for (auto& S : subs) {
         append(first, S.first);
         append(rlast, S.rlast);
         append(gidx, S.gidx);
         append(sidx, S.sidx);
         append(roff, S.roff);
-        append(diag, S.diag);
         append(probe_all, S.probe);
         invs.push_back(std::move(S.inv));
-        append(L, S.L);
-        append(U, S.U);
         S = HostSub{};
     }
     std::vector<int> order(static_cast<std::size_t>(n_sub));
@@ -968,9 +986,7 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
     pc->rlast.upload(rlast);
     pc->gidx.upload(gidx);
     pc->sidx.upload(sidx);
-    pc->diag.upload(diag);
-    pc->L.upload(L);
-    pc->U.upload(U);
+
     const auto t1 = std::chrono::steady_clock::now();
     pc->analyse_seconds = std::chrono::duration<double>(t1 - t0).count();
 
