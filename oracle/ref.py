@@ -266,3 +266,12 @@ def solve_capped(P: RefProblem, b, max_iter: int, rel_tol: float):
     b = np.ascontiguousarray(b, np.float64)
     P._check(L.cref_solve_capped(P._h, b, int(max_iter), float(rel_tol), C.byref(it), C.byref(secs), C.byref(last)))
     return dict(iterations=it.value, seconds=secs.value, last_residual=last.value)
+
+
+def write_outputs(P: RefProblem, directory: str, u, residuals, t4, gmres_mode: bool):
+    L = lib()
+    L.cref_write_outputs.argtypes = [C.c_void_p, C.c_char_p, _f64p, _f64p, C.c_int, _f64p, C.c_int]
+    u = np.ascontiguousarray(u, np.float64)
+    res = np.ascontiguousarray(residuals, np.float64)
+    P._check(L.cref_write_outputs(P._h, directory.encode(), u, res, int(res.size),
+                                  np.ascontiguousarray(t4, np.float64), int(gmres_mode)))

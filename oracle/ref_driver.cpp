@@ -493,4 +493,25 @@ int cref_solve_capped(void* hv, const double* b, int max_iter, double rel_tol, i
     });
 }
 
+/** The reference's own writers (io.hpp:82-115) on the problem's band, a given
+ *  solution / residual history and phase times (byte-format oracle). */
+int cref_write_outputs(void* hv, const char* dir, const double* u, const double* residuals, int n_res,
+                       const double* t4, int gmres_mode) {
+    auto* H = static_cast<Handle*>(hv);
+    return visit(H, [&](auto& I) {
+        const int n = I.P->grid.n_active();
+        Eigen::VectorXd uv = Eigen::VectorXd(Eigen::Map<Eigen::VectorXd>(u, n));
+        write_solution(std::string(dir) + "/solution.csv", I.P->grid, uv);
+        IterationLog log;
+        log.residuals.assign(residuals, residuals + n_res);
+        write_iterations(std::string(dir) + "/iterations.csv", log);
+        PhaseTimings t;
+        t.mesh = t4[0];
+        t.global_matrix = t4[1];
+        t.local_operators = t4[2];
+        t.solve = t4[3];
+        write_timings(std::string(dir) + "/timings.csv", t, gmres_mode != 0);
+    });
+}
+
 }  // extern "C"

@@ -381,9 +381,15 @@ def run_solve(cfg: dict, part=None, rhs=None) -> dict:
                 minor_radius=float(cfg.get("minor_radius", 1.0 / 3.0)), obj_path=cfg.get("obj"),
                 tube_radius=float(cfg.get("tube_radius", 0.0)), workers=int(cfg.get("workers", 0)))
     t.global_matrix = time.perf_counter() - t0
+    from . import io as _io
+    if part is None and cfg.get("partition_in"):
+        part = _io.read_partition(cfg["partition_in"], P.n_active)
+    if rhs is None and str(cfg.get("rhs", "")).startswith("file:"):
+        rhs = _io.read_rhs(str(cfg["rhs"])[5:], P.n_active)
     if part is None or rhs is None:
         from .errors import ConfigError
-        raise ConfigError(_lib.ERR_CONFIG, "run_solve needs a partition and a right-hand side")
+        raise ConfigError(_lib.ERR_CONFIG, "run_solve needs a partition (partition_in) and a right-hand side "
+                                           "(rhs = file:PATH)")
     n_sub = int(cfg.get("n_subdomains", int(np.max(part)) + 1))
     if int(np.max(part)) + 1 != n_sub:
         from .errors import ConfigError
@@ -409,6 +415,16 @@ def run_solve(cfg: dict, part=None, rhs=None) -> dict:
     t.solve = res.log.device_seconds
     res.log.timings = t
     b0 = float(np.linalg.norm(rhs))
-    return dict(u=res.u.cpu().numpy(), log=res.log, part=aligned, align_moves=moves,
+    u_host = res.u.cpu().numpy()
+    if cfg.get("partition_out"):
+        _io.write_partition(cfg["partition_out"], aligned)
+    if cfg.get("output_dir"):
+        import os
+        d = cfg["output_dir"]
+        x = P.band()["ix"][: P.n_active] * P.h
+        _io.write_solution(os.path.join(d, "solution.csv"), x, u_host)
+        _io.write_iterations(os.path.join(d, "iterations.csv"), res.log.residuals)
+        _io.write_timings(os.path.join(d, "timings.csv"), t, mode == "gmres")
+    return dict(u=u_host, log=res.log, part=aligned, align_moves=moves,
                 final_relative_residual=res.log.final_true_residual / b0 if b0 > 0 else 0.0,
                 problem=P, operator=A, preconditioner=M)

@@ -192,3 +192,26 @@ def test_drop_in_band_descriptor_matches_setup():
     A2 = api.DeviceHelmholtz.from_band(3, 3, 0.1, 1.0, P.n_active, B["ix"], B["cp"])
     x = torch.from_numpy(inputs.uniform_vector(P.n_active, 9)).cuda()
     assert torch.equal(A1.apply(x), A2.apply(x))
+
+
+def test_run_solve_pipeline_with_files(tmp_path):
+    """run_solve (pipeline.hpp:183-241) fed through a partition file and an rhs
+    file, writing the reference's output files."""
+    import json
+
+    from paper_1909_08734_b200 import api, inputs, io
+    g = np.load(os.path.join(GOLDEN, "circle_oras_gmres.npz"))
+    io.write_partition(str(tmp_path / "part.txt"), g["part_in"])
+    io.write_rhs(str(tmp_path / "rhs.txt"), g["b"])
+    cfg = dict(surface="circle", h=0.0125, p=3, c=1.0, method="oras", mode="gmres", gmres_restart=50,
+               rel_tol=1e-10, max_iter=2000, n_overlap=2, n_subdomains=8, alpha=1.0,
+               partition_in=str(tmp_path / "part.txt"), rhs="file:" + str(tmp_path / "rhs.txt"),
+               partition_out=str(tmp_path / "aligned.txt"), output_dir=str(tmp_path))
+    out = api.run_solve(cfg)
+    assert out["log"].converged and abs(out["log"].iterations - int(g["iterations"])) <= 2
+    assert np.linalg.norm(out["u"] - g["u"]) <= 1e-8 * np.linalg.norm(g["u"])
+    assert np.array_equal(io.read_partition(str(tmp_path / "aligned.txt"), len(g["b"])), g["part_aligned"])
+    lines = (tmp_path / "iterations.csv").read_text().splitlines()
+    assert lines[0] == "iter,residual_2norm" and len(lines) == out["log"].iterations + 2
+    assert (tmp_path / "solution.csv").read_text().startswith("x,y,z,u\n")
+    assert (tmp_path / "timings.csv").read_text().splitlines()[-1].startswith("preconditioned_solve,")
