@@ -517,7 +517,7 @@ __device__ __noinline__ void prefetch_rows(const double* V, const int* f, const 
  *  that fall in blocks k and k+1; one barrier per block. */
 __device__ __forceinline__ void lower_solve(int n, const int* __restrict__ f, const std::int64_t* __restrict__ ro,
                                             const double* __restrict__ V, const double* __restrict__ d,
-                                            double* y, double (*part)[RB + 2], double (*tri)[RB][TS]) {
+                                            double* y, double (*part)[RB + 2], double (*tri)[RB][TS], int dbg = 0) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nblk = (n + RB - 1) / RB;
     auto panel = [&](int b0, int buf) {
@@ -573,7 +573,7 @@ __device__ __forceinline__ void lower_solve(int n, const int* __restrict__ f, co
     auto prefetch_block = [&](int k) {
         if (k < nblk) prefetch_rows(V, f, ro, k * RB, min(n, k * RB + RB));
     };
-    if (threadIdx.x == 32) {
+    if (threadIdx.x == 0) {
         prefetch_block(0);
         prefetch_block(1);
     }
@@ -582,8 +582,8 @@ __device__ __forceinline__ void lower_solve(int n, const int* __restrict__ f, co
     for (int k = 0; k < nblk; ++k) {
         const int cur = k & 1;
         const int r0 = k * RB;
-        if (threadIdx.x == 32) prefetch_block(k + 2);
-        if (warp == 0) {
+        if (threadIdx.x == 0 && !(dbg & 4)) prefetch_block(k + 2);
+        if (warp == 0 && !(dbg & 1)) {
             const int i = r0 + lane;
             const bool live = lane < RB && i < n;
             double s = 0.0;
@@ -601,7 +601,7 @@ __device__ __forceinline__ void lower_solve(int n, const int* __restrict__ f, co
                 if (lane > c && live) s = fma(-tri[cur][lane][RB + c], xc, s);
             }
             if (live) y[i] = s;
-        } else if (k + 1 < nblk) {
+        } else if (warp > 0 && k + 1 < nblk && !(dbg & 2)) {
             panel((k + 1) * RB, cur ^ 1);
         }
         __syncthreads();
@@ -716,7 +716,7 @@ __device__ __forceinline__ void upper_solve_cols(int n, const int* __restrict__ 
         const int cur = K & 1;
         const int c0 = K * RB;
         // prefetch the columns the row updates need `pf` steps from now
-        if (threadIdx.x == 32 && pf > 0) prefetch_block(K + 1 - pf);
+        if (threadIdx.x == 0 && pf > 0) prefetch_block(K + 1 - pf);
         if (warp == 0) {
             const int i = c0 + lane;
             const bool live = lane < RB && i < n;
@@ -812,7 +812,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const int* __restric
                                                             const std::int64_t* __restrict__ ubase,
                                                             const int* __restrict__ ufirst_all,
                                                             const std::int64_t* __restrict__ uroff_all,
-                                                            const double* __restrict__ drev_all) {
+                                                            const double* __restrict__ drev_all, int dbg) {
     const int j = order[blockIdx.x];
     const int n = n_rows[j];
     const std::int64_t vb = vbase[j];
@@ -831,7 +831,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const int* __restric
     }
     __syncthreads();
     // forward: L y = b (unit lower)
-    if (MODE != 2) lower_solve(n, first_all + vb, roff_all + vb, L_all + ebase[j], nullptr, y, part, tri);
+    if (MODE != 2) lower_solve(n, first_all + vb, roff_all + vb, L_all + ebase[j], nullptr, y, part, tri, dbg);
     if constexpr (UROWS) {
         // backward: U x = y as a forward solve on the reversed system
         for (int p = tid; p < n / 2; p += blockDim.x) {
@@ -841,7 +841,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const int* __restric
         }
         __syncthreads();
         if (MODE != 1)
-            lower_solve(n, ufirst_all + vb, uroff_all + vb, U_all + ubase[j], drev_all + vb, y, part, tri);
+            lower_solve(n, ufirst_all + vb, uroff_all + vb, U_all + ubase[j], drev_all + vb, y, part, tri, dbg);
         for (int p = tid; p < n; p += blockDim.x) {
             if (MODE == 3) {
                 z[vb + p] = y[n - 1 - p];
@@ -879,10 +879,19 @@ void append(std::vector<T>& dst, const std::vector<T>& src) {
 void pc_apply_mode(const cpddg_pc* pc, const double* r, double* z, bool accumulate, int mode, cudaStream_t st) {
     auto kern = pc->urows ? (mode == 1 ? k_solve<1, true> : mode == 2 ? k_solve<2, true> : mode == 3 ? k_solve<3, true> : k_solve<0, true>)
                           : (mode == 1 ? k_solve<1, false> : mode == 2 ? k_solve<2, false> : mode == 3 ? k_solve<3, false> : k_solve<0, false>);
-    kern<<<pc->n_sub, kSolveThreads, pc->solve_smem, st>>>(
+    static const int dbg_flags = [] {
+        const char* e = std::getenv("CPDDG_SOLVE_DEBUG");  // development: timing experiments only
+        return e ? std::atoi(e) : 0;
+    }();
+    static const int limit = [] {
+        const char* e = std::getenv("CPDDG_SOLVE_LIMIT");  // development: solve only the first k subdomains
+        return e ? std::atoi(e) : 0;
+    }();
+    const int grid = (limit > 0 && mode != 3) ? std::min(limit, pc->n_sub) : pc->n_sub;
+    kern<<<grid, kSolveThreads, pc->solve_smem, st>>>(
         pc->order.get(), pc->n_rows.get(), pc->vbase.get(), pc->ebase.get(), pc->first.get(), pc->roff.get(),
         pc->dinv.get(), pc->L.get(), pc->U.get(), pc->gidx.get(), pc->sidx.get(), r, z, accumulate ? 1 : 0,
-        pc->bwd_prefetch, pc->ubase.get(), pc->ufirst.get(), pc->uroff.get(), pc->drev.get());
+        pc->bwd_prefetch, pc->ubase.get(), pc->ufirst.get(), pc->uroff.get(), pc->drev.get(), mode == 3 ? 0 : dbg_flags);
     CPDDG_CUDA(cudaGetLastError());
 }
 
