@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libcpddg.so")
+LIB_PATH = os.environ.get("CPDDG_LIB") or os.path.join(_HERE, "lib", "libcpddg.so")
 
 OK, ERR_INTERNAL, ERR_CONFIG, ERR_DIVERGENCE, ERR_IO, ERR_CUDA = range(6)
 

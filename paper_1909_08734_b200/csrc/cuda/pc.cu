@@ -46,7 +46,7 @@ namespace {
 
 constexpr int NB = 32;    // factor panel width
 constexpr int TILE = 64;  // trailing-update tile
-constexpr int SB = 32;    // solve block
+
 
 struct HostSub {
     int n = 0;
@@ -480,9 +480,16 @@ __global__ void __launch_bounds__(kFactorThreads) k_factor(const int* __restrict
 
 // ---------------------------------------------------------------- solve
 
-constexpr int kSolveWarps = 16;
+#ifndef CPDDG_SOLVE_WARPS
+#define CPDDG_SOLVE_WARPS 16
+#endif
+constexpr int kSolveWarps = CPDDG_SOLVE_WARPS;
 constexpr int kSolveThreads = 32 * kSolveWarps;
-constexpr int RB = 2 * (kSolveWarps - 1);  // rows per pipelined block: 2 per panel warp
+#ifndef CPDDG_ROWS_PER_WARP
+#define CPDDG_ROWS_PER_WARP 2
+#endif
+constexpr int kRowsPerWarp = CPDDG_ROWS_PER_WARP;
+constexpr int RB = kRowsPerWarp * (kSolveWarps - 1);  // rows per pipelined block
 constexpr int TS = 2 * RB + 1;             // padded stash row (previous block + own triangle)
 
 
@@ -523,8 +530,8 @@ __device__ __forceinline__ void lower_solve(int n, const int* __restrict__ f, co
     auto panel = [&](int b0, int buf) {
         const int lim = b0 - RB;  // columns < lim are final
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-            const int rr = 2 * (warp - 1) + q;
+        for (int q = 0; q < kRowsPerWarp; ++q) {
+            const int rr = kRowsPerWarp * (warp - 1) + q;
             const int i = b0 + rr;
             double s = 0.0;
             if (i < n) {
@@ -532,7 +539,7 @@ __device__ __forceinline__ void lower_solve(int n, const int* __restrict__ f, co
                 const double* Li = V + (__ldg(ro + i) - fi);
                 // stash loads first: they share the round trip of the partial loads
                 const int col0 = lim + lane, col1 = lim + lane + 32;
-                const double t0 = (col0 >= fi && col0 < i) ? __ldcs(Li + col0) : 0.0;
+                const double t0 = (lane < 2 * RB && col0 >= fi && col0 < i) ? __ldcs(Li + col0) : 0.0;
                 const double t1 = (lane + 32 < 2 * RB && col1 >= fi && col1 < i) ? __ldcs(Li + col1) : 0.0;
                 double s1 = 0.0, s2 = 0.0, s3 = 0.0;
                 const double2* Li2 = reinterpret_cast<const double2*>(Li + fi);  // fi even, row 16B-aligned
@@ -560,7 +567,7 @@ __device__ __forceinline__ void lower_solve(int n, const int* __restrict__ f, co
                     }
                 }
                 s = (s + s1) + (s2 + s3);
-                tri[buf][rr][lane] = t0;
+                if (lane < 2 * RB) tri[buf][rr][lane] = t0;
                 if (lane + 32 < 2 * RB) tri[buf][rr][lane + 32] = t1;
             } else {
                 for (int cc = lane; cc < 2 * RB; cc += 32) tri[buf][rr][cc] = 0.0;
