@@ -68,6 +68,7 @@ struct cpddg_pc {
     int solve_smem = 0;
     int bwd_prefetch = 1;  // backward L2 prefetch distance in blocks (0 = off)
     bool urows = true;     // backward layout: reversed U rows (true) or U columns (false)
+    int shape = 1;         // solve block shape: 0 big (1 CTA/SM), 1 mid (2/SM), 2 small (4/SM)
 };
 
 namespace cpddg {

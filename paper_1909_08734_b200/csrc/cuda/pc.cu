@@ -37,6 +37,7 @@
 #include <climits>
 #include <cstdlib>
 #include <string>
+#include <type_traits>
 #include <cmath>
 #include <numeric>
 
@@ -480,18 +481,24 @@ __global__ void __launch_bounds__(kFactorThreads) k_factor(const int* __restrict
 
 // ---------------------------------------------------------------- solve
 
-#ifndef CPDDG_SOLVE_WARPS
-#define CPDDG_SOLVE_WARPS 16
-#endif
-constexpr int kSolveWarps = CPDDG_SOLVE_WARPS;
-constexpr int kSolveThreads = 32 * kSolveWarps;
-#ifndef CPDDG_ROWS_PER_WARP
-#define CPDDG_ROWS_PER_WARP 2
-#endif
-constexpr int kRowsPerWarp = CPDDG_ROWS_PER_WARP;
-constexpr int RB = kRowsPerWarp * (kSolveWarps - 1);  // rows per pipelined block
-constexpr int TS = 2 * RB + 1;             // padded stash row (previous block + own triangle)
-
+/** Block shape of the pipelined triangular solves: NW warps per CTA (warp 0
+ *  solves triangles, NW-1 stream panel rows), RPW rows per panel warp, so a
+ *  block has RB = RPW (NW-1) rows (even: 16-byte vector loads never straddle
+ *  the partial/stash boundary).  Chosen per launch from the subdomain count:
+ *  one CTA per subdomain and every CTA resident in a single wave. */
+template <int NW, int RPW, int MINB>
+struct SolveShape {
+    static constexpr int kWarps = NW, kThreads = 32 * NW, kRows = RPW, kMinBlocks = MINB;
+    static constexpr int RB = RPW * (NW - 1);
+    static constexpr int TS = 2 * RB + 1;  // padded stash row (previous block + own triangle)
+    static_assert(RB % 2 == 0 && RB <= 32, "block rows must be even and fit one warp");
+};
+using ShapeBig = SolveShape<31, 1, 1>;    // n_sub <= #SMs: 992 threads, one CTA per SM
+using ShapeMid = SolveShape<16, 2, 2>;    // n_sub <= 2 #SMs: 512 threads, two per SM
+using ShapeSmall = SolveShape<8, 2, 4>;   // more subdomains: 256 threads, up to four per SM
+constexpr int RB = ShapeMid::RB;  // the column-layout backward (upper_solve_cols) uses ShapeMid
+constexpr int TS = ShapeMid::TS;
+constexpr int kSolveThreads = ShapeMid::kThreads;
 
 /** Prefetch [p, p + bytes) into L2 with the bulk-copy engine
  *  (cp.async.bulk.prefetch.L2; p and bytes 16-byte aligned). */
@@ -522,9 +529,13 @@ __device__ __noinline__ void prefetch_rows(const double* V, const int* f, const 
  *  rows (two rows each, 8 loads in flight per lane, streaming cache hints)
  *  into a partial dot over the already-final columns and stash the entries
  *  that fall in blocks k and k+1; one barrier per block. */
+template <class SH>
 __device__ __forceinline__ void lower_solve(int n, const int* __restrict__ f, const std::int64_t* __restrict__ ro,
                                             const double* __restrict__ V, const double* __restrict__ d,
-                                            double* y, double (*part)[RB + 2], double (*tri)[RB][TS], int dbg = 0) {
+                                            double* y, double (*part)[SH::RB + 2], double (*tri)[SH::RB][SH::TS],
+                                            int dbg = 0) {
+    constexpr int RB = SH::RB;
+    constexpr int kRowsPerWarp = SH::kRows;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nblk = (n + RB - 1) / RB;
     auto panel = [&](int b0, int buf) {
@@ -802,8 +813,8 @@ __device__ __forceinline__ void upper_solve_cols(int n, const int* __restrict__ 
 // 3: factor probe -- r / z are per-row arrays in factor order (vbase
 //    indexing) instead of global vectors, no gather / scatter.
 // UROWS: backward on reversed U rows (k_reverse_u) instead of U columns.
-template <int MODE, bool UROWS>
-__global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const int* __restrict__ order,
+template <int MODE, bool UROWS, class SH>
+__global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) k_solve(const int* __restrict__ order,
                                                             const int* __restrict__ n_rows,
                                                             const std::int64_t* __restrict__ vbase,
                                                             const std::int64_t* __restrict__ ebase,
@@ -824,8 +835,8 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const int* __restric
     const int n = n_rows[j];
     const std::int64_t vb = vbase[j];
     extern __shared__ double y[];
-    __shared__ double part[2][RB + 2];
-    __shared__ double tri[2][RB][TS];
+    __shared__ double part[2][SH::RB + 2];
+    __shared__ double tri[2][SH::RB][SH::TS];
     const int tid = threadIdx.x;
 
     for (int p = tid; p < n; p += blockDim.x) {
@@ -838,7 +849,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const int* __restric
     }
     __syncthreads();
     // forward: L y = b (unit lower)
-    if (MODE != 2) lower_solve(n, first_all + vb, roff_all + vb, L_all + ebase[j], nullptr, y, part, tri, dbg);
+    if (MODE != 2) lower_solve<SH>(n, first_all + vb, roff_all + vb, L_all + ebase[j], nullptr, y, part, tri, dbg);
     if constexpr (UROWS) {
         // backward: U x = y as a forward solve on the reversed system
         for (int p = tid; p < n / 2; p += blockDim.x) {
@@ -848,7 +859,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const int* __restric
         }
         __syncthreads();
         if (MODE != 1)
-            lower_solve(n, ufirst_all + vb, uroff_all + vb, U_all + ubase[j], drev_all + vb, y, part, tri, dbg);
+            lower_solve<SH>(n, ufirst_all + vb, uroff_all + vb, U_all + ubase[j], drev_all + vb, y, part, tri, dbg);
         for (int p = tid; p < n; p += blockDim.x) {
             if (MODE == 3) {
                 z[vb + p] = y[n - 1 - p];
@@ -861,6 +872,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const int* __restric
             }
         }
     } else {
+        static_assert(std::is_same_v<SH, ShapeMid>, "the column-layout backward is built for ShapeMid");
         // backward: U x = y, column-oriented on the factorisation's U layout
         __shared__ int cf[3][RB];
         __shared__ long long cro[3][RB];
@@ -883,9 +895,25 @@ void append(std::vector<T>& dst, const std::vector<T>& src) {
 
 }  // namespace
 
+template <bool UROWS, class SH>
+static void launch_solve(const cpddg_pc* pc, int grid, const double* r, double* z, bool accumulate, int mode,
+                         int dbg, cudaStream_t st) {
+    auto kern = mode == 1 ? k_solve<1, UROWS, SH> : mode == 2 ? k_solve<2, UROWS, SH>
+              : mode == 3 ? k_solve<3, UROWS, SH> : k_solve<0, UROWS, SH>;
+    kern<<<grid, SH::kThreads, pc->solve_smem, st>>>(
+        pc->order.get(), pc->n_rows.get(), pc->vbase.get(), pc->ebase.get(), pc->first.get(), pc->roff.get(),
+        pc->dinv.get(), pc->L.get(), pc->U.get(), pc->gidx.get(), pc->sidx.get(), r, z, accumulate ? 1 : 0,
+        pc->bwd_prefetch, pc->ubase.get(), pc->ufirst.get(), pc->uroff.get(), pc->drev.get(), dbg);
+    CPDDG_CUDA(cudaGetLastError());
+}
+
+template <bool UROWS, class SH>
+static void set_solve_smem(int bytes) {
+    for (auto kern : {k_solve<0, UROWS, SH>, k_solve<1, UROWS, SH>, k_solve<2, UROWS, SH>, k_solve<3, UROWS, SH>})
+        CPDDG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(bytes, 1)));
+}
+
 void pc_apply_mode(const cpddg_pc* pc, const double* r, double* z, bool accumulate, int mode, cudaStream_t st) {
-    auto kern = pc->urows ? (mode == 1 ? k_solve<1, true> : mode == 2 ? k_solve<2, true> : mode == 3 ? k_solve<3, true> : k_solve<0, true>)
-                          : (mode == 1 ? k_solve<1, false> : mode == 2 ? k_solve<2, false> : mode == 3 ? k_solve<3, false> : k_solve<0, false>);
     static const int dbg_flags = [] {
         const char* e = std::getenv("CPDDG_SOLVE_DEBUG");  // development: timing experiments only
         return e ? std::atoi(e) : 0;
@@ -895,11 +923,15 @@ void pc_apply_mode(const cpddg_pc* pc, const double* r, double* z, bool accumula
         return e ? std::atoi(e) : 0;
     }();
     const int grid = (limit > 0 && mode != 3) ? std::min(limit, pc->n_sub) : pc->n_sub;
-    kern<<<grid, kSolveThreads, pc->solve_smem, st>>>(
-        pc->order.get(), pc->n_rows.get(), pc->vbase.get(), pc->ebase.get(), pc->first.get(), pc->roff.get(),
-        pc->dinv.get(), pc->L.get(), pc->U.get(), pc->gidx.get(), pc->sidx.get(), r, z, accumulate ? 1 : 0,
-        pc->bwd_prefetch, pc->ubase.get(), pc->ufirst.get(), pc->uroff.get(), pc->drev.get(), mode == 3 ? 0 : dbg_flags);
-    CPDDG_CUDA(cudaGetLastError());
+    const int dbg = mode == 3 ? 0 : dbg_flags;
+    if (!pc->urows)
+        launch_solve<false, ShapeMid>(pc, grid, r, z, accumulate, mode, dbg, st);
+    else if (pc->shape == 0)
+        launch_solve<true, ShapeBig>(pc, grid, r, z, accumulate, mode, dbg, st);
+    else if (pc->shape == 1)
+        launch_solve<true, ShapeMid>(pc, grid, r, z, accumulate, mode, dbg, st);
+    else
+        launch_solve<true, ShapeSmall>(pc, grid, r, z, accumulate, mode, dbg, st);
 }
 
 void pc_apply(const cpddg_pc* pc, const double* r, double* z, bool accumulate, cudaStream_t st) {
@@ -1070,9 +1102,19 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
     pc->solve_smem = static_cast<int>(sizeof(double)) * pc->max_rows;
     if (const char* e = std::getenv("CPDDG_BWD_PREFETCH")) pc->bwd_prefetch = std::atoi(e);
     if (pc->solve_smem > 200 * 1024) throw ConfigError("subdomain system too large for the shared-memory solve");
-    for (auto kern : {k_solve<0, false>, k_solve<1, false>, k_solve<2, false>, k_solve<3, false>, k_solve<0, true>,
-                      k_solve<1, true>, k_solve<2, true>, k_solve<3, true>})
-        CPDDG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(pc->solve_smem, 1)));
+    set_solve_smem<false, ShapeMid>(pc->solve_smem);
+    set_solve_smem<true, ShapeBig>(pc->solve_smem);
+    set_solve_smem<true, ShapeMid>(pc->solve_smem);
+    set_solve_smem<true, ShapeSmall>(pc->solve_smem);
+    // block shape: one CTA per subdomain, all resident in one wave
+    {
+        const int S = sm_count();
+        pc->shape = n_sub <= S ? 0 : n_sub <= 2 * S ? 1 : 2;
+        if (const char* e = std::getenv("CPDDG_SOLVE_SHAPE")) {
+            const std::string v(e);
+            pc->shape = v == "big" ? 0 : v == "mid" ? 1 : v == "small" ? 2 : pc->shape;
+        }
+    }
     // factor probe (cpddg_pc_options::check_residual): solve A_j z = A_j x_probe
     // on the device for every subdomain and check the residual on the host --
     // the DirectSolver contract of the reference (residual ~1e-12,
