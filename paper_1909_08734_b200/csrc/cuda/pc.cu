@@ -1109,7 +1109,7 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
     // block shape: one CTA per subdomain, all resident in one wave
     {
         const int S = sm_count();
-        pc->shape = n_sub <= S ? 0 : n_sub <= 2 * S ? 1 : 2;
+        pc->shape = n_sub <= S ? 0 : 1;  // measured: two waves of ShapeMid beat one wave of ShapeSmall
         if (const char* e = std::getenv("CPDDG_SOLVE_SHAPE")) {
             const std::string v(e);
             pc->shape = v == "big" ? 0 : v == "mid" ? 1 : v == "small" ? 2 : pc->shape;
