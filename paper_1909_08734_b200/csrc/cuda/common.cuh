@@ -79,6 +79,11 @@ int sm_count();
 int reduction_blocks();
 
 constexpr int kRedThreads = 256;
+constexpr int kExtTile = 256;      // max band nodes per staged-extension tile (one per thread)
+#ifndef CPDDG_EXT_CAP
+#define CPDDG_EXT_CAP 4096
+#endif
+constexpr int kExtStageCap = CPDDG_EXT_CAP; // max staged x entries per tile (8 B of shared memory each)
 
 // Fixed-order block sum: warp shuffles (xor tree) then warp 0 over the 8
 // warp partials.  Deterministic for a fixed blockDim.

@@ -181,6 +181,74 @@ __global__ void __launch_bounds__(256) k_extend_p3(int nb, const double* __restr
     if (k < nb && a == 0) v[k] = acc;
 }
 
+#ifndef CPDDG_EXT_UNROLL
+#define CPDDG_EXT_UNROLL 8
+#endif
+#ifndef CPDDG_EXT_MINB
+#define CPDDG_EXT_MINB 5
+#endif
+/** v = E x for d = 3, p = 3, staged: one CTA per tile of kExtTile
+ *  consecutive band nodes, one thread per node.  The CTA first copies the
+ *  x entries its 16 x 256 stencil runs touch (sorted unique active
+ *  ordinals, ~9 per node at the headline) into shared memory with coalesced
+ *  loads, then every thread reads its 64 stencil values from the stage at
+ *  16-bit tile-local run starts.  Consecutive band nodes share most of their
+ *  runs, so the L2 gather of 64 values per node (the bound of k_extend_p3:
+ *  L1 wavefronts) becomes ~9 streamed loads per node.  The summation order
+ *  is k_extend_p3's ((a0 + a1) + (a2 + a3)), so v is bit-identical. */
+__global__ void __launch_bounds__(kExtTile, CPDDG_EXT_MINB) k_extend_staged(int nb, const double* __restrict__ t,
+                                                           const std::uint16_t* __restrict__ lines16,
+                                                           const int* __restrict__ tile_k0,
+                                                           const int* __restrict__ stage_base,
+                                                           const int* __restrict__ stage_idx,
+                                                           const double* __restrict__ x,
+                                                           double* __restrict__ v) {
+    extern __shared__ double xs[];
+    const int k = __ldg(tile_k0 + blockIdx.x) + threadIdx.x;
+    const bool live = k < __ldg(tile_k0 + blockIdx.x + 1);
+    // the node's offsets first: their latency overlaps the stage copy
+    double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+    if (live) {
+        t0 = __ldg(t + k);
+        t1 = __ldg(t + static_cast<std::size_t>(nb) + k);
+        t2 = __ldg(t + 2 * static_cast<std::size_t>(nb) + k);
+    }
+    const int s0 = __ldg(stage_base + blockIdx.x), s1 = __ldg(stage_base + blockIdx.x + 1);
+    constexpr int U = CPDDG_EXT_UNROLL;  // one round covers U * kExtTile staged entries
+    for (int j = s0 + threadIdx.x; j < s1; j += U * kExtTile) {
+        int src[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) src[u] = j + u * kExtTile < s1 ? __ldg(stage_idx + j + u * kExtTile) : -1;
+        double val[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) val[u] = src[u] >= 0 ? __ldg(x + src[u]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (src[u] >= 0) xs[j - s0 + u * kExtTile] = val[u];
+    }
+    double wl[4], w0[4], w1[4];
+    weights_p3(t2, wl);
+    weights_p3(t0, w0);
+    weights_p3(t1, w1);
+    __syncthreads();
+    if (!live) return;
+    double part[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        double sa = 0.0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const double* r = xs + __ldg(lines16 + static_cast<std::size_t>(a * 4 + b) * nb + k);
+            double s = 0.0;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) s = fma(wl[c], r[c], s);
+            sa = fma(w1[b], s, sa);
+        }
+        part[a] = __dmul_rn(w0[a], sa);
+    }
+    v[k] = (part[0] + part[1]) + (part[2] + part[3]);
+}
+
 /** y = cg x - ih2 sum v[nbr]; if b != nullptr: y <- b - y and partial ||y||^2. */
 template <int D, bool RESID>
 __global__ void __launch_bounds__(kRedThreads) k_helm(int na, double cg, double ih2,
@@ -229,6 +297,79 @@ __global__ void __launch_bounds__(kRedThreads) k_helm(int na, double cg, double 
 
 // ---------------------------------------------------------------- host side
 
+/** Stage lists of the staged extension (k_extend_staged): band nodes are cut
+ *  into tiles of at most kExtTile consecutive nodes (halved until a tile's
+ *  stage fits kExtStageCap entries, so several CTAs fit one SM); per tile, the
+ *  sorted unique active ordinals its runs cover and every run's 16-bit start
+ *  inside that list.  Left empty (gather kernel) if even a 32-node tile
+ *  overflows the cap. */
+static void build_stage(cpddg_op* op, const std::vector<int>& lines, int nb) {
+    constexpr int R = 16, Q = 4;
+    const int groups = (nb + kExtTile - 1) / kExtTile;
+    struct Tile {
+        int k0, k1;
+        std::vector<int> u;
+    };
+    std::vector<std::vector<Tile>> parts(static_cast<std::size_t>(groups));
+    std::vector<int> fail(static_cast<std::size_t>(groups), 0);
+    std::vector<std::uint16_t> l16(static_cast<std::size_t>(R) * nb);
+    auto stage_of = [&](int k0, int k1) {
+        std::vector<int> st;
+        st.reserve(static_cast<std::size_t>(R) * (k1 - k0));
+        for (int l = 0; l < R; ++l)
+            for (int k = k0; k < k1; ++k) st.push_back(lines[static_cast<std::size_t>(l) * nb + k]);
+        std::sort(st.begin(), st.end());
+        st.erase(std::unique(st.begin(), st.end()), st.end());
+        std::vector<int> u;
+        for (int o : st)  // union of [o, o + Q), runs sorted by start
+            for (int c = (u.empty() ? 0 : std::max(0, u.back() - o + 1)); c < Q; ++c) u.push_back(o + c);
+        return u;
+    };
+    parallel_for(groups, 0, [&](int g, int) {
+        std::vector<std::pair<int, int>> todo{{g * kExtTile, std::min(nb, (g + 1) * kExtTile)}};
+        auto& out = parts[static_cast<std::size_t>(g)];
+        while (!todo.empty()) {
+            const auto [k0, k1] = todo.back();
+            todo.pop_back();
+            std::vector<int> u = stage_of(k0, k1);
+            if (static_cast<int>(u.size()) > kExtStageCap) {
+                if (k1 - k0 <= 32) {
+                    fail[static_cast<std::size_t>(g)] = 1;
+                    return;
+                }
+                const int mid = k0 + (k1 - k0) / 2;
+                todo.push_back({mid, k1});  // popped after [k0, mid): tiles stay in order
+                todo.push_back({k0, mid});
+                continue;
+            }
+            for (int l = 0; l < R; ++l)
+                for (int k = k0; k < k1; ++k) {
+                    const int o = lines[static_cast<std::size_t>(l) * nb + k];
+                    l16[static_cast<std::size_t>(l) * nb + k] =
+                        static_cast<std::uint16_t>(std::lower_bound(u.begin(), u.end(), o) - u.begin());
+                }
+            out.push_back({k0, k1, std::move(u)});
+        }
+    });
+    for (int f : fail)
+        if (f) return;
+    std::vector<int> k0s, base{0}, idx;
+    for (auto& ts : parts)
+        for (auto& tl : ts) {
+            k0s.push_back(tl.k0);
+            idx.insert(idx.end(), tl.u.begin(), tl.u.end());
+            base.push_back(static_cast<int>(idx.size()));
+        }
+    k0s.push_back(nb);
+    op->lines16.upload(l16);
+    op->tile_k0.upload(k0s);
+    op->stage_base.upload(base);
+    op->stage_idx.upload(idx);
+    op->ext_tiles = static_cast<int>(k0s.size()) - 1;
+    op->ext_smem = kExtStageCap * static_cast<int>(sizeof(double));
+    CPDDG_CUDA(cudaFuncSetAttribute(k_extend_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, op->ext_smem));
+}
+
 template <int D>
 static void build_tables(cpddg_op* op, const Ix<D>* ix, const Vec<D>* cp, const LatticeMap& map) {
     const int nb = op->na + op->ng, p = op->p, Q = p + 1;
@@ -276,6 +417,9 @@ static void build_tables(cpddg_op* op, const Ix<D>* ix, const Vec<D>* cp, const 
             nbr[static_cast<std::size_t>(k) * op->na + i] = static_cast<int>(c);
         }
     }
+    if constexpr (D == 3) {
+        if (p == 3 && !std::getenv("CPDDG_EXT_GATHER")) build_stage(op, lines, nb);
+    }
     op->t.upload(t);
     op->lines.upload(lines);
     op->nbr.upload(nbr);
@@ -285,6 +429,8 @@ static void build_tables(cpddg_op* op, const Ix<D>* ix, const Vec<D>* cp, const 
     op->alg_bytes = 16LL * op->na + (8LL * D + 4LL * nlines) * nb + 8LL * D * op->na;
     // streamed: x read + y write, t + lines per band node, v write+read, nbr
     op->streamed_bytes = 16LL * op->na + (8LL * D + 4LL * nlines) * nb + 16LL * nb + 8LL * D * op->na;
+    if (op->ext_tiles)  // staged: 16-bit run starts + one int per staged x
+        op->streamed_bytes += (2LL - 4LL) * nlines * nb + 4LL * static_cast<long long>(op->stage_idx.size());
 }
 
 template <int D>
@@ -292,7 +438,12 @@ static void launch_apply(const cpddg_op* op, const double* x, const double* b, d
                          cudaStream_t st) {
     const int nb = op->na + op->ng;
     const int thr = 256;
-    if (op->p == 3) {
+    if (op->ext_tiles) {
+        k_extend_staged<<<op->ext_tiles, kExtTile, op->ext_smem, st>>>(nb, op->t.get(), op->lines16.get(),
+                                                                       op->tile_k0.get(),
+                                                                       op->stage_base.get(), op->stage_idx.get(), x,
+                                                                       op->v.get());
+    } else if (op->p == 3) {
         const long long threads = 4LL * nb;
         k_extend_p3<D><<<static_cast<int>((threads + thr - 1) / thr), thr, 0, st>>>(nb, op->t.get(), op->lines.get(), x,
                                                                                   op->v.get());

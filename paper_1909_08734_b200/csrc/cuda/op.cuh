@@ -29,6 +29,14 @@ struct cpddg_op {
     cpddg::DevBuf<int> lines;   // [(p+1)^(d-1)][N_B] first ordinal of each contiguous run
     cpddg::DevBuf<int> nbr;     // [2d][N_A] band codes of the axis neighbours
     cpddg::DevBuf<double> v;    // [N_B] extension values E x
+    // staged extension (d = 3, p = 3): tiles of <= kExtTile consecutive band
+    // nodes; each tile stages the x entries its stencils touch into shared
+    // memory and addresses them with 16-bit tile-local run starts.
+    int ext_tiles = 0, ext_smem = 0;                // 0 tiles: gather kernel
+    cpddg::DevBuf<std::uint16_t> lines16;          // [16][N_B] run start in the tile's stage
+    cpddg::DevBuf<int> tile_k0;                     // [tiles+1] first band node of each tile
+    cpddg::DevBuf<int> stage_base;                  // [tiles+1] first entry of each tile's stage list
+    cpddg::DevBuf<int> stage_idx;                   // stage list: active ordinal of each staged x
     cpddg::DevBuf<double> rn2;  // scalar slot for ||b - A x||^2
     cpddg::ReduceWork red;
     std::int64_t alg_bytes = 0, streamed_bytes = 0;

@@ -194,6 +194,23 @@ def test_drop_in_band_descriptor_matches_setup():
     assert torch.equal(A1.apply(x), A2.apply(x))
 
 
+@pytest.mark.parametrize("h", [0.1, 0.025])
+def test_staged_extension_matches_gather_kernel(h, monkeypatch):
+    """The staged extension kernel (d = 3, p = 3 default) and the plain
+    gather kernel (CPDDG_EXT_GATHER=1 at create time) give bitwise equal
+    A x: same weights, same summation order."""
+    import torch
+
+    from paper_1909_08734_b200 import api, inputs
+    P = api.Problem("sphere", h=h, p=3, c=1.0)
+    staged = api.DeviceHelmholtz.from_problem(P)
+    monkeypatch.setenv("CPDDG_EXT_GATHER", "1")
+    gather = api.DeviceHelmholtz.from_problem(P)
+    x = torch.from_numpy(inputs.uniform_vector(P.n_active, 5)).cuda()
+    assert torch.equal(staged.apply(x), gather.apply(x))
+    assert staged.bytes()[1] != gather.bytes()[1]  # the staged tables were really built
+
+
 def test_run_solve_pipeline_with_files(tmp_path):
     """run_solve (pipeline.hpp:183-241) fed through a partition file and an rhs
     file, writing the reference's output files."""
