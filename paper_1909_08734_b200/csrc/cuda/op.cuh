@@ -54,8 +54,11 @@ struct cpddg_pc {
     cpddg::DevBuf<std::int64_t> ebase; // [n_sub] first entry in the concatenated L / U arrays
     cpddg::DevBuf<int> order;          // [n_sub] launch order (largest first)
     // per row (device, concatenated over subdomains, in factor order)
-    cpddg::DevBuf<int> first;          // envelope start column f_i (local index)
-    cpddg::DevBuf<std::int64_t> roff;  // offset of row i inside its subdomain's L/U arrays
+    cpddg::DevBuf<int> first;          // L row i: envelope start column fL_i (local index)
+    cpddg::DevBuf<std::int64_t> roff;  // offset of row i inside its subdomain's L array
+    cpddg::DevBuf<std::int64_t> ebaseU; // [n_sub] first entry of each subdomain in U (column storage)
+    cpddg::DevBuf<int> firstU;         // U column i: first stored row fU_i
+    cpddg::DevBuf<std::int64_t> roffU; // offset of column i inside its subdomain's U array
     cpddg::DevBuf<int> rlast;          // largest row whose envelope starts at or before i
     cpddg::DevBuf<int> gidx;           // global index gathered into row i (R_j), or -1
     cpddg::DevBuf<int> sidx;           // global index row i scatters to (owned), or -1

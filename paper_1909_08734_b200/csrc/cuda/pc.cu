@@ -52,11 +52,11 @@ constexpr int TILE = 64;  // trailing-update tile
 struct HostSub {
     int n = 0;
     bool reduced = false;
-    std::int64_t ne = 0;       // envelope entries per triangle
+    std::int64_t ne = 0, neU = 0;  // envelope entries of L (rows) and U (columns)
     std::vector<int> inv;      // local (old) index -> factor order
     std::vector<double> probe; // b = A_sys x_probe in factor order
-    std::vector<int> first, rlast, gidx, sidx;
-    std::vector<std::int64_t> roff;
+    std::vector<int> first, firstU, rlast, urlast, gidx, sidx;
+    std::vector<std::int64_t> roff, roffU;
 
 };
 
@@ -156,31 +156,71 @@ HostSub analyse(const cpddg_local_desc& d, int n_global) {
     const std::vector<int> perm = rcm(adj);
     std::vector<int> inv(static_cast<std::size_t>(n));
     for (int k = 0; k < n; ++k) inv[static_cast<std::size_t>(perm[static_cast<std::size_t>(k)])] = k;
-    S.first.assign(static_cast<std::size_t>(n), 0);
-    for (int o = 0; o < n; ++o) {
-        const int i = inv[static_cast<std::size_t>(o)];
-        int f = i;
-        for (int w : adj[static_cast<std::size_t>(o)]) f = std::min(f, inv[static_cast<std::size_t>(w)]);
-        S.first[static_cast<std::size_t>(i)] = f;
-    }
+    // envelopes of the actual (nonsymmetric) pattern in factor order: L row i
+    // starts at fL_i (first nonzero left of the diagonal), U column c at fU_c
+    // (first nonzero above it).  LU without pivoting keeps its fill inside
+    // both: l_ij = 0 for j < fL_i and u_ic = 0 for i < fU_c by induction on
+    // the elimination, so L is stored by rows over [fL_i, i) and U by
+    // columns over [fU_c, c).  (CPDDG_ENVELOPE=sym: the symmetric profile
+    // min(fL, fU) for both, the previous layout.)
+    S.first.resize(static_cast<std::size_t>(n));
+    S.firstU.resize(static_cast<std::size_t>(n));
+    std::iota(S.first.begin(), S.first.end(), 0);
+    std::iota(S.firstU.begin(), S.firstU.end(), 0);
+    for (int r = 0; r < n; ++r)
+        for (std::int64_t k = rp[r]; k < rp[r + 1]; ++k) {
+            const int c = d.col[k];
+            if (c >= n || c == r) continue;
+            const int pi = inv[static_cast<std::size_t>(r)], pj = inv[static_cast<std::size_t>(c)];
+            if (pj < pi)
+                S.first[static_cast<std::size_t>(pi)] = std::min(S.first[static_cast<std::size_t>(pi)], pj);
+            else
+                S.firstU[static_cast<std::size_t>(pj)] = std::min(S.firstU[static_cast<std::size_t>(pj)], pi);
+        }
+    static const bool sym_env = [] {
+        const char* e = std::getenv("CPDDG_ENVELOPE");
+        return e && std::string(e) == "sym";
+    }();
+    if (sym_env)
+        for (int i = 0; i < n; ++i)
+            S.first[static_cast<std::size_t>(i)] = S.firstU[static_cast<std::size_t>(i)] =
+                std::min(S.first[static_cast<std::size_t>(i)], S.firstU[static_cast<std::size_t>(i)]);
     // 16-byte alignment for vector loads: every row (of L) / column (of U)
     // starts at an even column and has even length, so column pairs
     // (2m, 2m+1) are double2-aligned.  The extra slots are structural zeros
     // that the no-pivot factorisation never fills (they lie outside the
-    // profile), so they cost at most two stored zeros per row.
-    for (int i = 0; i < n; ++i) S.first[static_cast<std::size_t>(i)] &= ~1;
-    S.roff.assign(static_cast<std::size_t>(n) + 1, 0);
-    for (int i = 0; i < n; ++i)
-        S.roff[static_cast<std::size_t>(i) + 1] =
-            S.roff[static_cast<std::size_t>(i)] + ((i + (i & 1)) - S.first[static_cast<std::size_t>(i)]);
-    std::vector<int> maxrow(static_cast<std::size_t>(n), -1);
-    for (int i = 0; i < n; ++i) maxrow[static_cast<std::size_t>(S.first[static_cast<std::size_t>(i)])] = std::max(maxrow[static_cast<std::size_t>(S.first[static_cast<std::size_t>(i)])], i);
-    S.rlast.assign(static_cast<std::size_t>(n), 0);
-    int run = -1;
+    // envelope), so they cost at most two stored zeros per row.
     for (int i = 0; i < n; ++i) {
-        run = std::max(run, maxrow[static_cast<std::size_t>(i)]);
-        S.rlast[static_cast<std::size_t>(i)] = std::max(run, i);
+        S.first[static_cast<std::size_t>(i)] &= ~1;
+        S.firstU[static_cast<std::size_t>(i)] &= ~1;
     }
+    auto offsets = [&](const std::vector<int>& f, std::vector<std::int64_t>& ro) {
+        ro.assign(static_cast<std::size_t>(n) + 1, 0);
+        for (int i = 0; i < n; ++i)
+            ro[static_cast<std::size_t>(i) + 1] = ro[static_cast<std::size_t>(i)] + ((i + (i & 1)) - f[static_cast<std::size_t>(i)]);
+        const std::int64_t total = ro.back();
+        ro.pop_back();
+        return total;
+    };
+    S.ne = offsets(S.first, S.roff);
+    S.neU = offsets(S.firstU, S.roffU);
+    // rlast_i: largest row whose L row or U column starts at or before i (the
+    // factorisation's panel reach); urlast_i: U columns only (reversed U rows)
+    auto reach = [&](std::initializer_list<const std::vector<int>*> fs) {
+        std::vector<int> maxrow(static_cast<std::size_t>(n), -1), out(static_cast<std::size_t>(n));
+        for (const auto* f : fs)
+            for (int i = 0; i < n; ++i)
+                maxrow[static_cast<std::size_t>((*f)[static_cast<std::size_t>(i)])] =
+                    std::max(maxrow[static_cast<std::size_t>((*f)[static_cast<std::size_t>(i)])], i);
+        int run = -1;
+        for (int i = 0; i < n; ++i) {
+            run = std::max(run, maxrow[static_cast<std::size_t>(i)]);
+            out[static_cast<std::size_t>(i)] = std::max(run, i);
+        }
+        return out;
+    };
+    S.rlast = reach({&S.first, &S.firstU});
+    S.urlast = reach({&S.firstU});
     // factor probe: b = A_sys x with x_i = 1 + (i mod 7) / 8 in factor order
     S.probe.assign(static_cast<std::size_t>(n), 0.0);
     for (int r = 0; r < n; ++r)
@@ -203,8 +243,6 @@ HostSub analyse(const cpddg_local_desc& d, int n_global) {
         if (lo < 0 || lo >= n || g < 0 || g >= n_global) throw InternalError("scatter index out of range");
         S.sidx[static_cast<std::size_t>(inv[static_cast<std::size_t>(lo)])] = g;
     }
-    S.ne = S.roff.back();
-    S.roff.pop_back();
     return S;
 }
 
@@ -224,14 +262,16 @@ void scatter_values(const cpddg_local_desc& d, const HostSub& S, double* L, doub
             else if (pj < pi)
                 L[S.roff[static_cast<std::size_t>(pi)] + (pj - S.first[static_cast<std::size_t>(pi)])] += v;
             else
-                U[S.roff[static_cast<std::size_t>(pj)] + (pi - S.first[static_cast<std::size_t>(pj)])] += v;
+                U[S.roffU[static_cast<std::size_t>(pj)] + (pi - S.firstU[static_cast<std::size_t>(pj)])] += v;
         }
 }
 
 struct SubPtrs {
     int n;
-    const int* first;
+    const int* first;          // L rows
     const std::int64_t* roff;
+    const int* firstU;         // U columns
+    const std::int64_t* roffU;
     const int* rlast;
     double* diag;
     double* L;
@@ -239,11 +279,13 @@ struct SubPtrs {
 };
 
 __device__ __forceinline__ SubPtrs sub_ptrs(int j, const int* n_rows, const std::int64_t* vbase,
-                                            const std::int64_t* ebase, const int* first,
-                                            const std::int64_t* roff, const int* rlast, double* diag,
+                                            const std::int64_t* ebase, const std::int64_t* ebaseU,
+                                            const int* first, const std::int64_t* roff, const int* firstU,
+                                            const std::int64_t* roffU, const int* rlast, double* diag,
                                             double* L, double* U) {
-    const std::int64_t vb = vbase[j], eb = ebase[j];
-    return {n_rows[j], first + vb, roff + vb, rlast + vb, diag + vb, L + eb, U + eb};
+    const std::int64_t vb = vbase[j];
+    return {n_rows[j], first + vb, roff + vb, firstU + vb, roffU + vb, rlast + vb, diag + vb, L + ebase[j],
+            U + ebaseU[j]};
 }
 
 // ------------------------------------------------------------ factorisation
@@ -255,13 +297,17 @@ __global__ void __launch_bounds__(kFactorThreads) k_factor(const int* __restrict
                                                            const int* __restrict__ n_rows,
                                                            const std::int64_t* __restrict__ vbase,
                                                            const std::int64_t* __restrict__ ebase,
+                                                           const std::int64_t* __restrict__ ebaseU,
                                                            const int* __restrict__ first_all,
                                                            const std::int64_t* __restrict__ roff_all,
+                                                           const int* __restrict__ firstU_all,
+                                                           const std::int64_t* __restrict__ roffU_all,
                                                            const int* __restrict__ rlast_all,
                                                            double* diag_all, double* L_all, double* U_all,
                                                            double* dinv_all, int* status) {
     const int j = order[blockIdx.x];
-    const SubPtrs S = sub_ptrs(j, n_rows, vbase, ebase, first_all, roff_all, rlast_all, diag_all, L_all, U_all);
+    const SubPtrs S = sub_ptrs(j, n_rows, vbase, ebase, ebaseU, first_all, roff_all, firstU_all, roffU_all,
+                               rlast_all, diag_all, L_all, U_all);
     extern __shared__ double sm[];
     double* A11 = sm;                            // [NB][NB+1]
     double* Xi = A11 + NB * (NB + 1);            // [NB][TILE+1]: X rows of tile i, transposed (p-major)
@@ -287,8 +333,8 @@ __global__ void __launch_bounds__(kFactorThreads) k_factor(const int* __restrict
                     const int f = S.first[gr];
                     if (gc >= f) v = S.L[S.roff[gr] + gc - f];
                 } else {
-                    const int f = S.first[gc];
-                    if (gr >= f) v = S.U[S.roff[gc] + gr - f];
+                    const int f = S.firstU[gc];
+                    if (gr >= f) v = S.U[S.roffU[gc] + gr - f];
                 }
             }
             A11[r * (NB + 1) + c] = v;
@@ -315,22 +361,21 @@ __global__ void __launch_bounds__(kFactorThreads) k_factor(const int* __restrict
                 const int f = S.first[gr];
                 if (gc >= f) S.L[S.roff[gr] + gc - f] = v;
             } else {
-                const int f = S.first[gc];
-                if (gr >= f) S.U[S.roff[gc] + gr - f] = v;
+                const int f = S.firstU[gc];
+                if (gr >= f) S.U[S.roffU[gc] + gr - f] = v;
             }
         }
         // (3)+(4) panels: rows i in [k1, R]
         for (int i = k1 + tid; i <= R; i += blockDim.x) {
-            const int f = S.first[i];
-            if (f >= k1) continue;  // no entries in the panel columns
-            const std::int64_t ro = S.roff[i] - f;
+            const int f = S.first[i], fu = S.firstU[i];
+            if (f >= k1 && fu >= k1) continue;  // no entries in the panel columns
+            const std::int64_t ro = S.roff[i] - f, rou = S.roffU[i] - fu;
             double x[NB], u[NB];
 #pragma unroll
             for (int p = 0; p < NB; ++p) {
                 const int gc = k0 + p;
-                const bool in = p < kb && gc >= f;
-                x[p] = in ? S.L[ro + gc] : 0.0;
-                u[p] = in ? S.U[ro + gc] : 0.0;
+                x[p] = p < kb && gc >= f ? S.L[ro + gc] : 0.0;
+                u[p] = p < kb && gc >= fu ? S.U[rou + gc] : 0.0;
             }
             // L21: x U11 = a  (forward over columns)
 #pragma unroll
@@ -355,10 +400,8 @@ __global__ void __launch_bounds__(kFactorThreads) k_factor(const int* __restrict
 #pragma unroll
             for (int p = 0; p < NB; ++p) {
                 const int gc = k0 + p;
-                if (p < kb && gc >= f) {
-                    S.L[ro + gc] = x[p];
-                    S.U[ro + gc] = u[p];
-                }
+                if (p < kb && gc >= f) S.L[ro + gc] = x[p];
+                if (p < kb && gc >= fu) S.U[rou + gc] = u[p];
             }
         }
         __syncthreads();
@@ -379,8 +422,8 @@ __global__ void __launch_bounds__(kFactorThreads) k_factor(const int* __restrict
                 if (tid < 32) {
                     int mi = INT_MAX, mj = INT_MAX;
                     for (int q = tid; q < TILE; q += 32) {
-                        if (i0 + q <= R) mi = min(mi, S.first[i0 + q]);
-                        if (j0 + q <= R) mj = min(mj, S.first[j0 + q]);
+                        if (i0 + q <= R) mi = min(mi, min(S.first[i0 + q], S.firstU[i0 + q]));
+                        if (j0 + q <= R) mj = min(mj, min(S.first[j0 + q], S.firstU[j0 + q]));
                     }
 #pragma unroll
                     for (int o = 16; o > 0; o >>= 1) {
@@ -397,18 +440,14 @@ __global__ void __launch_bounds__(kFactorThreads) k_factor(const int* __restrict
                     double xi = 0, yi = 0, xj = 0, yj = 0;
                     if (p < kb) {
                         if (gi <= R) {
-                            const int f = S.first[gi];
-                            if (gc >= f) {
-                                xi = S.L[S.roff[gi] + gc - f];
-                                yi = S.U[S.roff[gi] + gc - f];
-                            }
+                            const int f = S.first[gi], fu = S.firstU[gi];
+                            if (gc >= f) xi = S.L[S.roff[gi] + gc - f];
+                            if (gc >= fu) yi = S.U[S.roffU[gi] + gc - fu];
                         }
                         if (gj <= R) {
-                            const int f = S.first[gj];
-                            if (gc >= f) {
-                                xj = S.L[S.roff[gj] + gc - f];
-                                yj = S.U[S.roff[gj] + gc - f];
-                            }
+                            const int f = S.first[gj], fu = S.firstU[gj];
+                            if (gc >= f) xj = S.L[S.roff[gj] + gc - f];
+                            if (gc >= fu) yj = S.U[S.roffU[gj] + gc - fu];
                         }
                     }
                     Xi[p * kTS + r] = xi;
@@ -444,8 +483,8 @@ __global__ void __launch_bounds__(kFactorThreads) k_factor(const int* __restrict
                 {
                     const int gi = i0 + warp * 8 + lr;
                     if (gi <= R) {
-                        const int f = S.first[gi];
-                        const std::int64_t ro = S.roff[gi] - f;
+                        const int f = S.first[gi], fu = S.firstU[gi];
+                        const std::int64_t ro = S.roff[gi] - f, rou = S.roffU[gi] - fu;
 #pragma unroll
                         for (int cb = 0; cb < 8; ++cb)
 #pragma unroll
@@ -453,10 +492,8 @@ __global__ void __launch_bounds__(kFactorThreads) k_factor(const int* __restrict
                                 const int gc = j0 + cb * 8 + 2 * lk + e;
                                 if (gc > R) continue;
                                 if (gc < gi) {
-                                    if (gc >= f) {
-                                        S.L[ro + gc] -= cL[cb][e];
-                                        S.U[ro + gc] -= cU[cb][e];
-                                    }
+                                    if (gc >= f) S.L[ro + gc] -= cL[cb][e];
+                                    if (gc >= fu) S.U[rou + gc] -= cU[cb][e];
                                 } else if (gc == gi) {
                                     S.diag[gi] -= cL[cb][e];
                                 }
@@ -500,6 +537,10 @@ constexpr int RB = ShapeMid::RB;  // the column-layout backward (upper_solve_col
 constexpr int TS = ShapeMid::TS;
 constexpr int kSolveThreads = ShapeMid::kThreads;
 
+// development timing trace (CPDDG_SOLVE_DEBUG & 16): per block of CTA 0,
+// [k][0] step start, [k][1] warp 0 done, [k][2 + w] panel warp w done
+__device__ long long g_trace[1024][20];
+
 /** Prefetch [p, p + bytes) into L2 with the bulk-copy engine
  *  (cp.async.bulk.prefetch.L2; p and bytes 16-byte aligned). */
 __device__ __forceinline__ void prefetch_l2(const void* p, long long bytes) {
@@ -540,6 +581,8 @@ __device__ __forceinline__ void lower_solve(int n, const int* __restrict__ f, co
     const int nblk = (n + RB - 1) / RB;
     auto panel = [&](int b0, int buf) {
         const int lim = b0 - RB;  // columns < lim are final
+        const bool trp = (dbg & 16) && blockIdx.x == 0 && warp == 1 && lane == 0 && b0 / RB - 1 < 1024 && b0 >= RB;
+        if (trp) g_trace[b0 / RB - 1][17] = clock64();
 #pragma unroll
         for (int q = 0; q < kRowsPerWarp; ++q) {
             const int rr = kRowsPerWarp * (warp - 1) + q;
@@ -578,12 +621,14 @@ __device__ __forceinline__ void lower_solve(int n, const int* __restrict__ f, co
                     }
                 }
                 s = (s + s1) + (s2 + s3);
+                if (trp && q == 0) g_trace[b0 / RB - 1][18] = clock64();
                 if (lane < 2 * RB) tri[buf][rr][lane] = t0;
                 if (lane + 32 < 2 * RB) tri[buf][rr][lane + 32] = t1;
             } else {
                 for (int cc = lane; cc < 2 * RB; cc += 32) tri[buf][rr][cc] = 0.0;
             }
             s = warp_sum(s);
+            if (trp && q == 0) g_trace[b0 / RB - 1][19] = clock64();
             if (lane == 0) part[buf][rr] = s;
         }
     };
@@ -592,15 +637,16 @@ __device__ __forceinline__ void lower_solve(int n, const int* __restrict__ f, co
         if (k < nblk) prefetch_rows(V, f, ro, k * RB, min(n, k * RB + RB));
     };
     if (threadIdx.x == 0) {
-        prefetch_block(0);
-        prefetch_block(1);
+        for (int q = 0; q < 2 + (dbg >> 8); ++q) prefetch_block(q);
     }
     if (warp > 0) panel(0, 0);
     __syncthreads();
     for (int k = 0; k < nblk; ++k) {
         const int cur = k & 1;
         const int r0 = k * RB;
-        if (threadIdx.x == 0 && !(dbg & 4)) prefetch_block(k + 2);
+        const bool tr = (dbg & 16) && blockIdx.x == 0 && k < 1024;
+        if (tr && threadIdx.x == 0) g_trace[k][0] = clock64();
+        if (threadIdx.x == 0 && !(dbg & 4)) prefetch_block(k + 2 + (dbg >> 8));
         if (warp == 0 && !(dbg & 1)) {
             const int i = r0 + lane;
             const bool live = lane < RB && i < n;
@@ -619,8 +665,10 @@ __device__ __forceinline__ void lower_solve(int n, const int* __restrict__ f, co
                 if (lane > c && live) s = fma(-tri[cur][lane][RB + c], xc, s);
             }
             if (live) y[i] = s;
+            if (tr && lane == 0) g_trace[k][1] = clock64();
         } else if (warp > 0 && k + 1 < nblk && !(dbg & 2)) {
             panel((k + 1) * RB, cur ^ 1);
+            if (tr && lane == 0 && warp < 18) g_trace[k][1 + warp] = clock64();
         }
         __syncthreads();
     }
@@ -670,71 +718,91 @@ __global__ void __launch_bounds__(256) k_reverse_u(const int* __restrict__ order
 }
 
 /** Pipelined blocked backward substitution U x = y with U stored by columns
- *  (column c holds rows [f_c, c) contiguously at V + ro[c]; diagonal d).
- *  Blocks of RB columns from the last: while warp 0 applies block K+1's
- *  columns to block K's rows and solves block K's triangle, warps 1..15
- *  apply block K+1's columns to every row below block K (thread per row,
- *  RB independent coalesced loads each) and stash the U entries block K-1's
- *  triangle step will need; one barrier per block.  Streams each stored
- *  entry of U exactly once. */
+ *  (column c holds rows [f_c, c) contiguously at V + ro[c]; reciprocal
+ *  pivots d).  Blocks of RB columns from the last.  Step K: warp 0 applies
+ *  block K+1's columns to block K's rows and solves block K's triangle, both
+ *  from a shared-memory stash; warps 1..15 apply block K+1's columns to every
+ *  row above block K (thread per row pair, coalesced 16-byte loads down the
+ *  columns), load the stash for block K-1 and the column tables (f, ro) of
+ *  block K-2.  Every load of a step is independent of the step's other loads
+ *  (tables come from shared memory, loaded a step ahead), so a step costs
+ *  the round trips of its update batches only; one barrier per block.
+ *  Streams each stored entry of U exactly once.  cf, cro: [4][RB] ring of
+ *  column tables indexed by block % 4. */
 __device__ __forceinline__ void upper_solve_cols(int n, const int* __restrict__ f,
                                                  const std::int64_t* __restrict__ ro,
                                                  const double* __restrict__ V, const double* __restrict__ d,
                                                  double* y, double (*tri)[RB][TS], int (*cf)[RB],
-                                                 long long (*cro)[RB], int pf) {  // cf, cro: [3][RB]
+                                                 long long (*cro)[RB], int pf) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nblk = (n + RB - 1) / RB;
     const int ptid = threadIdx.x - 32, pthreads = blockDim.x - 32;
-    // stash for block K: tri[buf][i][c] = U(c0+i, c0+c) for c in [0, 2RB) (block K, then K+1 columns)
-    // stash = load (into registers, 2 per thread since RB * 2RB <= 2 * 480)
-    // then store (after the row updates, so both share a round trip)
+    constexpr int kStash = (RB * 2 * RB + 479) / 480;  // stash entries per panel thread
+    // column table of block K into ring slot K % 4 (panel threads < RB)
+    auto table_load = [&](int K, int& tf, long long& tro) {
+        const int col = K * RB + ptid;
+        tf = n;
+        tro = 0;
+        if (K >= 0 && ptid < RB && col < n) {
+            tf = __ldg(f + col);
+            tro = __ldg(ro + col);
+        }
+    };
+    auto table_store = [&](int K, int tf, long long tro) {
+        if (K >= 0 && ptid < RB) {
+            cf[K & 3][ptid] = tf;
+            cro[K & 3][ptid] = tro;
+        }
+    };
+    // stash for block K: tri[buf][i][c] = U(c0+i, c0+c), c in [0, 2RB): block
+    // K's columns then block K+1's; tables of blocks K, K+1 in shared memory
     auto stash_load = [&](int K, double* v) {
         const int c0 = K * RB;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < kStash; ++q) {
             const int e = ptid + q * pthreads;
             v[q] = 0.0;
             if (e < RB * 2 * RB) {
                 const int il = e / (2 * RB), cl = e % (2 * RB);
                 const int i = c0 + il, col = c0 + cl;
                 if (col < n && i < col) {
-                    const int fc = __ldg(f + col);
-                    if (i >= fc) v[q] = __ldcs(V + __ldg(ro + col) + (i - fc));
+                    const int slot = (cl < RB ? K : K + 1) & 3, cc = cl < RB ? cl : cl - RB;
+                    const int fc = cf[slot][cc];
+                    if (i >= fc) v[q] = __ldcs(V + cro[slot][cc] + (i - fc));
                 }
             }
         }
     };
     auto stash_store = [&](const double* v, int buf) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < kStash; ++q) {
             const int e = ptid + q * pthreads;
             if (e < RB * 2 * RB) tri[buf][e / (2 * RB)][e % (2 * RB)] = v[q];
-        }
-    };
-    auto stash = [&](int K, int buf) {
-        const int c0 = K * RB;
-        double v[4];
-        stash_load(K, v);
-        stash_store(v, buf);
-        // column tables use a third buffer: block K+1's are still being read
-        // by the row updates of the step that stashes block K
-        const int cb = K % 3;
-        for (int e = ptid; e < RB; e += pthreads) {
-            const int col = c0 + e;
-            cf[cb][e] = col < n ? __ldg(f + col) : n;
-            cro[cb][e] = col < n ? __ldg(ro + col) : 0;
         }
     };
     auto prefetch_block = [&](int K) {
         if (K >= 0) prefetch_rows(V, f, ro, K * RB, min(n, K * RB + RB));
     };
-    if (warp > 0) stash(nblk - 1, (nblk - 1) & 1);
+    if (warp > 0) {
+        int tf;
+        long long tro;
+        table_load(nblk - 1, tf, tro);
+        table_store(nblk - 1, tf, tro);
+        table_load(nblk - 2, tf, tro);
+        table_store(nblk - 2, tf, tro);
+        if (ptid == 0)
+            for (int q = 1; q <= pf; ++q) prefetch_block(nblk - q);
+    }
+    __syncthreads();
+    if (warp > 0) {
+        double sv[kStash];
+        stash_load(nblk - 1, sv);
+        stash_store(sv, (nblk - 1) & 1);
+    }
     __syncthreads();
     for (int K = nblk - 1; K >= 0; --K) {
         const int cur = K & 1;
         const int c0 = K * RB;
-        // prefetch the columns the row updates need `pf` steps from now
-        if (threadIdx.x == 0 && pf > 0) prefetch_block(K + 1 - pf);
         if (warp == 0) {
             const int i = c0 + lane;
             const bool live = lane < RB && i < n;
@@ -753,11 +821,17 @@ __device__ __forceinline__ void upper_solve_cols(int n, const int* __restrict__ 
             }
             if (live) y[i] = s;
         } else {
-            double sv[4];
+            // the columns the row updates need pf steps from now (bulk L2 prefetch
+            // from a panel thread: warp 0 is on the critical path)
+            if (ptid == 0 && pf > 0) prefetch_block(K - pf);
+            int tf;
+            long long tro;
+            table_load(K - 2, tf, tro);
+            double sv[kStash];
             if (K >= 1) stash_load(K - 1, sv);
             if (K + 1 < nblk) {
-                // rows below block K from block K+1's columns
-                const int nxt = (K + 1) % 3;
+                // rows above block K from block K+1's columns
+                const int nxt = (K + 1) & 3;
                 const int cb1 = min(RB, n - (c0 + RB));
                 int jmin = c0;
                 for (int c = 0; c < cb1; ++c) jmin = min(jmin, cf[nxt][c]);
@@ -794,16 +868,8 @@ __device__ __forceinline__ void upper_solve_cols(int n, const int* __restrict__ 
                     }
                 }
             }
-            if (K >= 1) {
-                stash_store(sv, cur ^ 1);
-                // column tables of block K-1 (third buffer, see stash())
-                const int cb = (K - 1) % 3;
-                for (int e = ptid; e < RB; e += pthreads) {
-                    const int col = (K - 1) * RB + e;
-                    cf[cb][e] = col < n ? __ldg(f + col) : n;
-                    cro[cb][e] = col < n ? __ldg(ro + col) : 0;
-                }
-            }
+            if (K >= 1) stash_store(sv, cur ^ 1);
+            table_store(K - 2, tf, tro);  // slot (K-2) & 3 == (K+2) & 3: no longer read
         }
         __syncthreads();
     }
@@ -820,6 +886,9 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) k_solve(const in
                                                             const std::int64_t* __restrict__ ebase,
                                                             const int* __restrict__ first_all,
                                                             const std::int64_t* __restrict__ roff_all,
+                                                            const std::int64_t* __restrict__ ebaseU,
+                                                            const int* __restrict__ firstU_all,
+                                                            const std::int64_t* __restrict__ roffU_all,
                                                             const double* __restrict__ diag_all,
                                                             const double* __restrict__ L_all,
                                                             const double* __restrict__ U_all,
@@ -874,9 +943,10 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) k_solve(const in
     } else {
         static_assert(std::is_same_v<SH, ShapeMid>, "the column-layout backward is built for ShapeMid");
         // backward: U x = y, column-oriented on the factorisation's U layout
-        __shared__ int cf[3][RB];
-        __shared__ long long cro[3][RB];
-        if (MODE != 1) upper_solve_cols(n, first_all + vb, roff_all + vb, U_all + ebase[j], diag_all + vb, y, tri, cf, cro, pf);
+        __shared__ int cf[4][RB];
+        __shared__ long long cro[4][RB];
+        if (MODE != 1)
+            upper_solve_cols(n, firstU_all + vb, roffU_all + vb, U_all + ebaseU[j], diag_all + vb, y, tri, cf, cro, pf);
         for (int p = tid; p < n; p += blockDim.x) {
             if (MODE == 3) {
                 z[vb + p] = y[p];
@@ -902,6 +972,7 @@ static void launch_solve(const cpddg_pc* pc, int grid, const double* r, double* 
               : mode == 3 ? k_solve<3, UROWS, SH> : k_solve<0, UROWS, SH>;
     kern<<<grid, SH::kThreads, pc->solve_smem, st>>>(
         pc->order.get(), pc->n_rows.get(), pc->vbase.get(), pc->ebase.get(), pc->first.get(), pc->roff.get(),
+        pc->ebaseU.get(), pc->firstU.get(), pc->roffU.get(),
         pc->dinv.get(), pc->L.get(), pc->U.get(), pc->gidx.get(), pc->sidx.get(), r, z, accumulate ? 1 : 0,
         pc->bwd_prefetch, pc->ubase.get(), pc->ufirst.get(), pc->uroff.get(), pc->drev.get(), dbg);
     CPDDG_CUDA(cudaGetLastError());
@@ -955,44 +1026,49 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
     auto pc = std::make_unique<cpddg_pc>();
     pc->n_global = n_global;
     pc->n_sub = n_sub;
-    std::vector<int> n_rows, first, rlast, gidx, sidx;
-    std::vector<std::int64_t> vbase, ebase, roff;
+    std::vector<int> n_rows, first, firstU, rlast, urlast, gidx, sidx;
+    std::vector<std::int64_t> vbase, ebase, ebaseU, roff, roffU;
     std::vector<double> probe_all;
     std::vector<std::vector<int>> invs;
-    std::int64_t vb = 0, ebs = 0;
+    std::int64_t vb = 0, ebs = 0, ebsU = 0;
     for (auto& S : subs) {
         n_rows.push_back(S.n);
         vbase.push_back(vb);
         ebase.push_back(ebs);
+        ebaseU.push_back(ebsU);
         vb += S.n;
         ebs += S.ne;
+        ebsU += S.neU;
         pc->max_rows = std::max(pc->max_rows, S.n);
         pc->n_reduced += S.reduced ? 1 : 0;
     }
     pc->rows_total = vb;
-    pc->entries = 2 * ebs + vb;
     // values: scattered per subdomain into scratch and copied straight into
     // the device arrays (no host-side concatenation of the factor storage)
     pc->L.alloc(static_cast<std::size_t>(std::max<std::int64_t>(ebs, 1)));
-    pc->U.alloc(static_cast<std::size_t>(std::max<std::int64_t>(ebs, 1)));
+    pc->U.alloc(static_cast<std::size_t>(std::max<std::int64_t>(ebsU, 1)));
     pc->diag.alloc(static_cast<std::size_t>(vb));
     parallel_for(n_sub, opt ? opt->workers : 0, [&](int j, int) {
         const HostSub& S = subs[static_cast<std::size_t>(j)];
-        std::vector<double> Lb(static_cast<std::size_t>(S.ne), 0.0), Ub(static_cast<std::size_t>(S.ne), 0.0),
+        std::vector<double> Lb(static_cast<std::size_t>(S.ne), 0.0), Ub(static_cast<std::size_t>(S.neU), 0.0),
             Db(static_cast<std::size_t>(S.n), 0.0);
         scatter_values(locals[j], S, Lb.data(), Ub.data(), Db.data());
         const std::size_t eb = static_cast<std::size_t>(ebase[static_cast<std::size_t>(j)]);
+        const std::size_t ebu = static_cast<std::size_t>(ebaseU[static_cast<std::size_t>(j)]);
         const std::size_t v0 = static_cast<std::size_t>(vbase[static_cast<std::size_t>(j)]);
-        if (S.ne) {
+        if (S.ne)
             CPDDG_CUDA(cudaMemcpy(pc->L.get() + eb, Lb.data(), Lb.size() * sizeof(double), cudaMemcpyHostToDevice));
-            CPDDG_CUDA(cudaMemcpy(pc->U.get() + eb, Ub.data(), Ub.size() * sizeof(double), cudaMemcpyHostToDevice));
-        }
+        if (S.neU)
+            CPDDG_CUDA(cudaMemcpy(pc->U.get() + ebu, Ub.data(), Ub.size() * sizeof(double), cudaMemcpyHostToDevice));
         CPDDG_CUDA(cudaMemcpy(pc->diag.get() + v0, Db.data(), Db.size() * sizeof(double), cudaMemcpyHostToDevice));
     });
     first.reserve(static_cast<std::size_t>(vb));
     for (auto& S : subs) {
         append(first, S.first);
+        append(firstU, S.firstU);
         append(rlast, S.rlast);
+        append(urlast, S.urlast);
+        append(roffU, S.roffU);
         append(gidx, S.gidx);
         append(sidx, S.sidx);
         append(roff, S.roff);
@@ -1003,9 +1079,14 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
     std::vector<int> order(static_cast<std::size_t>(n_sub));
     std::iota(order.begin(), order.end(), 0);
     {
+        std::vector<std::int64_t> subs_cost(static_cast<std::size_t>(n_sub));
+        for (int j = 0; j < n_sub; ++j)
+            subs_cost[static_cast<std::size_t>(j)] =
+                (j + 1 < n_sub ? ebase[static_cast<std::size_t>(j) + 1] : ebs) - ebase[static_cast<std::size_t>(j)] +
+                (j + 1 < n_sub ? ebaseU[static_cast<std::size_t>(j) + 1] : ebsU) - ebaseU[static_cast<std::size_t>(j)];
         std::vector<std::int64_t> cost(static_cast<std::size_t>(n_sub));
         for (int j = 0; j < n_sub; ++j)
-            cost[static_cast<std::size_t>(j)] = (j + 1 < n_sub ? ebase[static_cast<std::size_t>(j) + 1] : ebs) - ebase[static_cast<std::size_t>(j)];
+            cost[static_cast<std::size_t>(j)] = subs_cost[static_cast<std::size_t>(j)];
         std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[static_cast<std::size_t>(a)] > cost[static_cast<std::size_t>(b)]; });
         // SM balance for the solve (2 resident CTAs per SM, blocks dealt to SMs
         // round-robin): with n_sub = S + P subdomains on S SMs, the S - P SMs that
@@ -1031,6 +1112,9 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
     pc->order.upload(order);
     pc->first.upload(first);
     pc->roff.upload(roff);
+    pc->ebaseU.upload(ebaseU);
+    pc->firstU.upload(firstU);
+    pc->roffU.upload(roffU);
     pc->rlast.upload(rlast);
     pc->gidx.upload(gidx);
     pc->sidx.upload(sidx);
@@ -1049,7 +1133,8 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
     CPDDG_CUDA(cudaEventCreate(&e1));
     CPDDG_CUDA(cudaEventRecord(e0));
     k_factor<<<n_sub, kFactorThreads, fsm>>>(pc->order.get(), pc->n_rows.get(), pc->vbase.get(), pc->ebase.get(),
-                                           pc->first.get(), pc->roff.get(), pc->rlast.get(), pc->diag.get(),
+                                           pc->ebaseU.get(), pc->first.get(), pc->roff.get(), pc->firstU.get(),
+                                           pc->roffU.get(), pc->rlast.get(), pc->diag.get(),
                                            pc->L.get(), pc->U.get(), pc->dinv.get(), status.get());
     CPDDG_CUDA(cudaGetLastError());
     CPDDG_CUDA(cudaEventRecord(e1));
@@ -1064,7 +1149,7 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
     for (int j = 0; j < n_sub; ++j)
         if (st[static_cast<std::size_t>(j)]) throw DivergenceError("singular factorization of subdomain " + std::to_string(j));
 
-    pc->u_entries = ebs;
+    pc->u_entries = ebsU;
     if (const char* e = std::getenv("CPDDG_BWD_LAYOUT")) pc->urows = std::string(e) != "cols";
     if (pc->urows) {
         std::vector<int> ufirst(static_cast<std::size_t>(vb));
@@ -1077,7 +1162,7 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
             std::int64_t off = 0;
             for (int ip = 0; ip < nj; ++ip) {
                 const int i = nj - 1 - ip;
-                const int fpr = (nj - 1 - rlast[static_cast<std::size_t>(v0 + i)]) & ~1;
+                const int fpr = (nj - 1 - urlast[static_cast<std::size_t>(v0 + i)]) & ~1;
                 ufirst[static_cast<std::size_t>(v0 + ip)] = fpr;
                 uroff[static_cast<std::size_t>(v0 + ip)] = off;
                 off += (ip + (ip & 1)) - fpr;
@@ -1090,15 +1175,15 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
         pc->ubase.upload(ubase);
         DevBuf<double> urev(static_cast<std::size_t>(std::max<std::int64_t>(ub, 1)));
         pc->drev.alloc(static_cast<std::size_t>(vb));
-        k_reverse_u<<<n_sub, 256>>>(pc->order.get(), pc->n_rows.get(), pc->vbase.get(), pc->ebase.get(),
-                                    pc->ubase.get(), pc->first.get(), pc->roff.get(), pc->ufirst.get(),
+        k_reverse_u<<<n_sub, 256>>>(pc->order.get(), pc->n_rows.get(), pc->vbase.get(), pc->ebaseU.get(),
+                                    pc->ubase.get(), pc->firstU.get(), pc->roffU.get(), pc->ufirst.get(),
                                     pc->uroff.get(), pc->dinv.get(), pc->U.get(), urev.get(), pc->drev.get());
         CPDDG_CUDA(cudaGetLastError());
         CPDDG_CUDA(cudaDeviceSynchronize());
         pc->U = std::move(urev);
     }
     pc->entries = ebs + pc->u_entries + vb;
-    pc->profile_entries = 2 * ebs + vb;
+    pc->profile_entries = ebs + ebsU + vb;
     pc->solve_smem = static_cast<int>(sizeof(double)) * pc->max_rows;
     if (const char* e = std::getenv("CPDDG_BWD_PREFETCH")) pc->bwd_prefetch = std::atoi(e);
     if (pc->solve_smem > 200 * 1024) throw ConfigError("subdomain system too large for the shared-memory solve");
@@ -1226,6 +1311,10 @@ int cpddg_pc_stats_get(const cpddg_pc* pc, cpddg_pc_stats* st) {
 
 /** Development hook: time one pass of the preconditioner (mode 1 forward,
  *  2 backward, 0 both).  Not part of include/cpddg.h. */
+int cpddg_dev_trace(long long* out) {  // development: copy g_trace
+    return guarded([&] { CPDDG_CUDA(cudaMemcpyFromSymbol(out, g_trace, sizeof(long long) * 1024 * 20)); });
+}
+
 int cpddg_pc_apply_mode(cpddg_pc* pc, const double* r, double* z, int mode, void* stream) {
     return guarded([&] {
         if (!pc || !r || !z) throw InternalError("null argument");
