@@ -17,6 +17,8 @@
 #include <cooperative_groups.h>
 
 #include <cmath>
+#include <cstdlib>
+#include <string>
 #include <vector>
 
 namespace cpddg {
@@ -131,6 +133,84 @@ __global__ void __launch_bounds__(kRedThreads) k_mgs_all(int n, int m, const dou
     const double sub = sqrt(hprev);
     if (vnext)
         for (int i = i0; i < n; i += stride) vnext[i] = w[i] / sub;
+}
+
+/** k_mgs_all with the thread's slice of w and of the previous basis vector
+ *  held in registers across passes (EPT elements per thread, same index
+ *  mapping, same summation order -- bit-identical results): a pass streams
+ *  one basis vector (8n bytes) instead of w twice and two basis vectors
+ *  (32n bytes). */
+template <int EPT>
+__global__ void __launch_bounds__(kRedThreads) k_mgs_reg(int n, int m, const double* const* __restrict__ V,
+                                                         double* __restrict__ w, double* __restrict__ vnext,
+                                                         double* partials, double* hout, double* wn0) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double sh[kRedThreads / 32];
+    __shared__ double hb;
+    const int nb = gridDim.x;
+    const int stride = gridDim.x * blockDim.x;
+    const int i0 = blockIdx.x * blockDim.x + threadIdx.x;
+    double wr[EPT], vr[EPT];
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) {
+        const int i = i0 + k * stride;
+        wr[k] = i < n ? w[i] : 0.0;
+        vr[k] = 0.0;
+    }
+    double hprev = 0.0;
+    for (int pass = 0; pass <= m + 1; ++pass) {
+        const double* vn = pass <= m ? V[pass] : nullptr;
+        double a1 = 0.0, a2 = 0.0;
+#pragma unroll
+        for (int k = 0; k < EPT; ++k) {
+            const int i = i0 + k * stride;
+            if (i < n) {
+                double wi = wr[k];
+                if (pass > 0) {
+                    wi -= hprev * vr[k];
+                    wr[k] = wi;
+                }
+                const double vi = vn ? __ldcg(vn + i) : wi;
+                vr[k] = vi;
+                a1 = fma(vi, wi, a1);
+                if (pass == 0) a2 = fma(wi, wi, a2);
+            }
+        }
+        const double b1 = block_sum<kRedThreads>(a1, sh);
+        const double b2 = pass == 0 ? block_sum<kRedThreads>(a2, sh) : 0.0;
+        double* slot = partials + static_cast<std::size_t>(pass) * 2 * nb;
+        if (threadIdx.x == 0) {
+            slot[blockIdx.x] = b1;
+            slot[nb + blockIdx.x] = b2;
+        }
+        grid.sync();
+        double s1 = 0.0, s2 = 0.0;
+        for (int q = threadIdx.x; q < nb; q += blockDim.x) {
+            s1 += slot[q];
+            if (pass == 0) s2 += slot[nb + q];
+        }
+        const double t1 = block_sum<kRedThreads>(s1, sh);
+        const double t2 = pass == 0 ? block_sum<kRedThreads>(s2, sh) : 0.0;
+        if (threadIdx.x == 0) {
+            hb = t1;
+            if (blockIdx.x == 0) {
+                hout[pass] = t1;
+                if (pass == 0) *wn0 = t2;
+            }
+        }
+        __syncthreads();
+        hprev = hb;
+    }
+    const double sub = sqrt(hprev);
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) {
+        const int i = i0 + k * stride;
+        if (i < n) {
+            w[i] = wr[k];
+            if (vnext) vnext[i] = wr[k] / sub;
+        }
+    }
 }
 
 /** Single-CTA variant of k_mgs_all for small systems (n below a few 10^4):
@@ -305,10 +385,12 @@ struct Workspace {
             kc.vptr.alloc(static_cast<std::size_t>(cap) + 64);
             kc.vptr_valid = 0;
         }
-        if (kc.host_cap < cap + 4) {
+        // three regions: two alternating Hessenberg columns (pipelined
+        // Arnoldi steps) and the update coefficients y
+        if (kc.host_cap < 3 * (cap + 4)) {
             if (kc.host) cudaFreeHost(kc.host);
-            CPDDG_CUDA(cudaMallocHost(&kc.host, sizeof(double) * (cap + 4)));
-            kc.host_cap = cap + 4;
+            CPDDG_CUDA(cudaMallocHost(&kc.host, sizeof(double) * 3 * (cap + 4)));
+            kc.host_cap = 3 * (cap + 4);
         }
     }
     double* basis(int k) {
@@ -352,8 +434,25 @@ struct Workspace {
         }
         double* part = mgs_partials.get();
         void* args[] = {&nn, &mm, &vpd, &w, &vnext, &part, &hout, &wn0};
-        CPDDG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_mgs_all), dim3(coop_grid), dim3(kRedThreads),
-                                               args, 0, st));
+        // register-resident w: up to 8 elements per thread of the cooperative grid
+        static const bool streamed = [] {
+            const char* e = std::getenv("CPDDG_MGS");  // development: "stream" = k_mgs_all
+            return e && std::string(e) == "stream";
+        }();
+        const long long threads = static_cast<long long>(coop_grid) * kRedThreads;
+        const int ept = static_cast<int>((n + threads - 1) / threads);
+        const void* kern = reinterpret_cast<const void*>(k_mgs_all);
+        if (!streamed && ept <= 8)
+            kern = ept <= 1   ? reinterpret_cast<const void*>(k_mgs_reg<1>)
+                   : ept <= 2 ? reinterpret_cast<const void*>(k_mgs_reg<2>)
+                   : ept <= 4 ? reinterpret_cast<const void*>(k_mgs_reg<4>)
+                              : reinterpret_cast<const void*>(k_mgs_reg<8>);
+        if (kern != reinterpret_cast<const void*>(k_mgs_all)) {
+            int per_sm = 0;  // the whole grid must be resident
+            CPDDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRedThreads, 0));
+            if (per_sm * sm_count() < coop_grid) kern = reinterpret_cast<const void*>(k_mgs_all);
+        }
+        CPDDG_CUDA(cudaLaunchCooperativeKernel(kern, dim3(coop_grid), dim3(kRedThreads), args, 0, st));
         ++launches;
     }
     void scale(const double* src, double s, double* dst) {
@@ -399,6 +498,17 @@ static void gmres(cpddg_op* op, cpddg_pc* pc, const double* b, double* u, const 
     struct {
         double* p;
     } hh{ws.kc.host};
+    double* hslot[2] = {hh.p, hh.p + (cap + 4)};
+    struct Events {
+        cudaEvent_t e[2];
+        Events() {
+            for (auto& x : e) CPDDG_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+        }
+        ~Events() {
+            for (auto& x : e) cudaEventDestroy(x);
+        }
+    } hevs;
+    cudaEvent_t* hev = hevs.e;
     DevBuf<double>& w = ws.kc.w;
     DevBuf<double>& r = ws.kc.r;
     DevBuf<double>& tmp = ws.kc.tmp;
@@ -441,24 +551,46 @@ static void gmres(cpddg_op* op, cpddg_pc* pc, const double* b, double* u, const 
         std::vector<double> cs, sn, g{beta};
         int m = 0;
         bool breakdown = false;
-        while (m < cycle && total < max_iter) {
-            const double* z = basis(m);
+        // Arnoldi step mm on the device: z = M^-1 V_mm, w = A z, MGS (all
+        // mm+2 passes and the next basis vector in one cooperative launch),
+        // the Hessenberg column to pinned host slot `slot`, event.
+        auto enqueue = [&](int mm, int slot) {
+            const double* z = basis(mm);
             if (pc) {
-                kt.time(true, [&] { pc_apply(pc, basis(m), tmp.get(), false, st); });
+                kt.time(true, [&] { pc_apply(pc, basis(mm), tmp.get(), false, st); });
                 ++ws.launches;
                 z = tmp.get();
             }
             kt.time(false, [&] { op_apply(op, z, w.get(), st); });
             ws.launches += 2;
-            // MGS, all m+2 passes and the next basis vector in one cooperative launch
-            double* vnext = (m + 1 <= cycle) ? basis(m + 1) : nullptr;
-            ws.mgs_all(m, w.get(), vnext, hd, hd + m + 2);
-            CPDDG_CUDA(cudaMemcpyAsync(hh.p, hd, sizeof(double) * (m + 3), cudaMemcpyDeviceToHost, st));
-            CPDDG_CUDA(cudaStreamSynchronize(st));
-            kt.collect();
-            std::vector<double> h(hh.p, hh.p + m + 2);
+            double* vnext = (mm + 1 <= cycle) ? basis(mm + 1) : nullptr;
+            ws.mgs_all(mm, w.get(), vnext, hd, hd + mm + 2);
+            CPDDG_CUDA(cudaMemcpyAsync(hslot[slot], hd, sizeof(double) * (mm + 3), cudaMemcpyDeviceToHost, st));
+            CPDDG_CUDA(cudaEventRecord(hev[slot], st));
+        };
+        int slot = 0;
+        bool queued = false;  // step m already enqueued (speculatively, by step m-1)
+        while (m < cycle && total < max_iter) {
+            if (!queued) enqueue(m, slot);
+            // pipelining: enqueue step m+1 before the host reads step m's
+            // column, so the device never waits for the host's Givens update.
+            // Only while the residual trend says step m will not converge (a
+            // wasted step costs a preconditioner apply); step m+1 depends on
+            // V_{m+1}, which step m writes on the device.
+            bool spec = !kt.on && m + 1 < cycle && total + 1 < max_iter;
+            if (spec) {
+                const std::size_t nr = residuals.size();
+                const double last = residuals[nr - 1];
+                const double rate = nr >= 2 && m >= 1 ? std::min(1.0, last / residuals[nr - 2]) : 1.0;
+                spec = last * rate > 4.0 * target;
+            }
+            if (spec) enqueue(m + 1, slot ^ 1);
+            CPDDG_CUDA(cudaEventSynchronize(hev[slot]));
+            if (!spec) kt.collect();
+            const double* hp = hslot[slot];
+            std::vector<double> h(hp, hp + m + 2);
             h[static_cast<std::size_t>(m) + 1] = std::sqrt(h[static_cast<std::size_t>(m) + 1]);
-            const double wnorm0 = std::sqrt(hh.p[m + 2]);
+            const double wnorm0 = std::sqrt(hp[m + 2]);
             const double subdiag = h[static_cast<std::size_t>(m) + 1];
             check_finite(subdiag, "gmres basis norm");
             for (int i = 0; i < m; ++i) {
@@ -475,6 +607,8 @@ static void gmres(cpddg_op* op, cpddg_pc* pc, const double* b, double* u, const 
             H.push_back(std::move(h));
             ++m;
             ++total;
+            slot ^= 1;
+            queued = spec;
             const double est = std::abs(g[static_cast<std::size_t>(m)]);
             check_finite(est, "gmres residual estimate");
             residuals.push_back(est);
@@ -494,12 +628,13 @@ static void gmres(cpddg_op* op, cpddg_pc* pc, const double* b, double* u, const 
                     throw DivergenceError("gmres encountered a singular projection");
                 y[static_cast<std::size_t>(i)] = s / H[static_cast<std::size_t>(i)][static_cast<std::size_t>(i)];
             }
+            double* yh = hh.p + 2 * (cap + 4);  // not a Hessenberg slot: a speculative step may still write those
             for (int k = 0; k < m; ++k) {
                 vptr_h[static_cast<std::size_t>(k)] = basis(k);
-                hh.p[k] = y[static_cast<std::size_t>(k)];
+                yh[k] = y[static_cast<std::size_t>(k)];
             }
             CPDDG_CUDA(cudaMemcpyAsync(vptr.get(), vptr_h.data(), sizeof(double*) * m, cudaMemcpyHostToDevice, st));
-            CPDDG_CUDA(cudaMemcpyAsync(yd.get(), hh.p, sizeof(double) * m, cudaMemcpyHostToDevice, st));
+            CPDDG_CUDA(cudaMemcpyAsync(yd.get(), yh, sizeof(double) * m, cudaMemcpyHostToDevice, st));
             k_combine<<<ws.grid, kRedThreads, 0, st>>>(n, m, vptr.get(), yd.get(), tmp.get());
             CPDDG_CUDA(cudaGetLastError());
             ++ws.launches;

@@ -18,7 +18,7 @@ for _ in range(3): f()
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
-for _ in range(10): f()
+for _ in range(30): f()
 e1.record(); torch.cuda.synchronize()
 env = {k: v for k, v in os.environ.items() if k.startswith("CPDDG_")}
-print(f"mode {mode} {env}: {e0.elapsed_time(e1) / 10:.3f} ms", flush=True)
+print(f"mode {mode} {env}: {e0.elapsed_time(e1) / 30:.3f} ms", flush=True)
