@@ -211,6 +211,49 @@ def test_staged_extension_matches_gather_kernel(h, monkeypatch):
     assert staged.bytes()[1] != gather.bytes()[1]  # the staged tables were really built
 
 
+@pytest.mark.parametrize("name", ["sphere05_oras_gmres", "circle_ras_gmres"])
+def test_factor_layouts_agree(name, monkeypatch):
+    """The factor layouts give the same preconditioner: nonsymmetric
+    envelopes (default) vs the symmetric profile (CPDDG_ENVELOPE=sym), and
+    the reversed-U-row backward (default) vs the column backward
+    (CPDDG_BWD_LAYOUT=cols).  All four within 1e-13 of each other and of the
+    reference at the usual 1e-9."""
+    import torch
+
+    from paper_1909_08734_b200 import api
+    g, cfg, P, A, M, torch = _setup(name)
+    x = torch.from_numpy(g["x"]).cuda()
+    z0 = M.apply(x).cpu().numpy()
+    for env, val in (("CPDDG_ENVELOPE", "sym"), ("CPDDG_BWD_LAYOUT", "cols")):
+        monkeypatch.setenv(env, val)
+        Mv = api.SchwarzPreconditioner.from_problem(P)
+        z = Mv.apply(x).cpu().numpy()
+        assert np.linalg.norm(z - z0) <= 1e-13 * np.linalg.norm(z0), (env, val)
+        assert np.linalg.norm(z - g["Mx"]) <= 1e-9 * np.linalg.norm(g["Mx"])
+    st = M.stats()
+    assert st["profile_entries"] <= st["factor_entries"]
+
+
+def test_pipelined_gmres_matches_synchronous_loop():
+    """The pipelined Arnoldi loop (a step is enqueued before the host reads
+    the previous Hessenberg column) reproduces the synchronous loop
+    (profile=True disables pipelining) bit for bit, restarts included."""
+    import torch
+
+    from paper_1909_08734_b200 import api, inputs
+    P = api.Problem("sphere", h=0.1, p=3, c=1.0)
+    P.decompose(inputs.rcb_partition(P.active_cp, 8), 2, "oras", 4.0, 40.0)
+    A = api.DeviceHelmholtz.from_problem(P)
+    M = api.SchwarzPreconditioner.from_problem(P)
+    b = torch.from_numpy(inputs.rhs_sphere(P.active_cp)).cuda()
+    for restart in (50, 5):
+        a = api.gmres_solve(A, b, M, 1e-10, 500, restart)
+        s = api.gmres_solve(A, b, M, 1e-10, 500, restart, profile=True)
+        assert a.log.iterations == s.log.iterations and a.log.converged
+        assert np.array_equal(np.asarray(a.log.residuals), np.asarray(s.log.residuals))
+        assert torch.equal(a.u, s.u)
+
+
 def test_run_solve_pipeline_with_files(tmp_path):
     """run_solve (pipeline.hpp:183-241) fed through a partition file and an rhs
     file, writing the reference's output files."""
