@@ -570,6 +570,8 @@ static void gmres(cpddg_op* op, cpddg_pc* pc, const double* b, double* u, const 
         };
         int slot = 0;
         bool queued = false;  // step m already enqueued (speculatively, by step m-1)
+        const char* sync_env = std::getenv("CPDDG_GMRES_SYNC");  // tests: the synchronous loop
+        const bool pipelined = !(sync_env && std::string(sync_env) == "1");
         while (m < cycle && total < max_iter) {
             if (!queued) enqueue(m, slot);
             // pipelining: enqueue step m+1 before the host reads step m's
@@ -577,7 +579,7 @@ static void gmres(cpddg_op* op, cpddg_pc* pc, const double* b, double* u, const 
             // Only while the residual trend says step m will not converge (a
             // wasted step costs a preconditioner apply); step m+1 depends on
             // V_{m+1}, which step m writes on the device.
-            bool spec = !kt.on && m + 1 < cycle && total + 1 < max_iter;
+            bool spec = pipelined && m + 1 < cycle && total + 1 < max_iter;
             if (spec) {
                 const std::size_t nr = residuals.size();
                 const double last = residuals[nr - 1];
@@ -586,7 +588,8 @@ static void gmres(cpddg_op* op, cpddg_pc* pc, const double* b, double* u, const 
             }
             if (spec) enqueue(m + 1, slot ^ 1);
             CPDDG_CUDA(cudaEventSynchronize(hev[slot]));
-            if (!spec) kt.collect();
+            // kernel timings (profile_kernels) are collected after the next full
+            // stream synchronisation: a speculative step may still be in flight
             const double* hp = hslot[slot];
             std::vector<double> h(hp, hp + m + 2);
             h[static_cast<std::size_t>(m) + 1] = std::sqrt(h[static_cast<std::size_t>(m) + 1]);

@@ -662,22 +662,10 @@ __device__ __forceinline__ void lower_solve(int n, const int* __restrict__ f, co
                 }
             }
             const int rb = min(RB, n - r0);
-            if (rb == RB) {
-                // full block: unrolled, so the triangle's shared-memory loads
-                // issue ahead of the shuffle chain
-#pragma unroll
-                for (int c = 0; c < RB; ++c) {
-                    const double t = tri[cur][lane][RB + c];
-                    if (d && lane == c) s *= dl;
-                    const double xc = __shfl_sync(0xffffffffu, s, c);
-                    if (lane > c && live) s = fma(-t, xc, s);
-                }
-            } else {
-                for (int c = 0; c < rb; ++c) {
-                    if (d && lane == c) s *= dl;  // d: reciprocal pivots
-                    const double xc = __shfl_sync(0xffffffffu, s, c);
-                    if (lane > c && live) s = fma(-tri[cur][lane][RB + c], xc, s);
-                }
+            for (int c = 0; c < rb; ++c) {
+                if (d && lane == c) s *= dl;  // d: reciprocal pivots
+                const double xc = __shfl_sync(0xffffffffu, s, c);
+                if (lane > c && live) s = fma(-tri[cur][lane][RB + c], xc, s);
             }
             if (live) y[i] = s;
             if (tr && lane == 0) g_trace[k][1] = clock64();

@@ -1,4 +1,5 @@
-CPDDG_SOLVE_DEBUG=16 CPDDG_SOLVE_LIMIT=1 python scripts/trace_solve.py 1 | head -3
-CPDDG_SOLVE_DEBUG=16 CPDDG_SOLVE_LIMIT=1 python scripts/trace_solve.py 2 | head -3
-for m in 1 2 0; do python scripts/pc_time.py $m; done
-python scripts/spec_compare.py
+for r in 1 2; do
+for L in libcpddg.so libcpddg_prev.so; do
+  CPDDG_LIB=$PWD/paper_1909_08734_b200/lib/$L python scripts/pc_time.py 0 | sed "s/^/$L /"
+done; done
+python scripts/spec_compare.py 2>&1 | head -2

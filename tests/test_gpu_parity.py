@@ -234,10 +234,10 @@ def test_factor_layouts_agree(name, monkeypatch):
     assert st["profile_entries"] <= st["factor_entries"]
 
 
-def test_pipelined_gmres_matches_synchronous_loop():
+def test_pipelined_gmres_matches_synchronous_loop(monkeypatch):
     """The pipelined Arnoldi loop (a step is enqueued before the host reads
     the previous Hessenberg column) reproduces the synchronous loop
-    (profile=True disables pipelining) bit for bit, restarts included."""
+    (CPDDG_GMRES_SYNC=1) bit for bit, restarts and kernel profiling included."""
     import torch
 
     from paper_1909_08734_b200 import api, inputs
@@ -248,7 +248,11 @@ def test_pipelined_gmres_matches_synchronous_loop():
     b = torch.from_numpy(inputs.rhs_sphere(P.active_cp)).cuda()
     for restart in (50, 5):
         a = api.gmres_solve(A, b, M, 1e-10, 500, restart)
-        s = api.gmres_solve(A, b, M, 1e-10, 500, restart, profile=True)
+        ap = api.gmres_solve(A, b, M, 1e-10, 500, restart, profile=True)
+        monkeypatch.setenv("CPDDG_GMRES_SYNC", "1")
+        s = api.gmres_solve(A, b, M, 1e-10, 500, restart)
+        monkeypatch.delenv("CPDDG_GMRES_SYNC")
+        assert torch.equal(a.u, ap.u) and ap.log.kernel_times["pc_launches"] >= ap.log.iterations
         assert a.log.iterations == s.log.iterations and a.log.converged
         assert np.array_equal(np.asarray(a.log.residuals), np.asarray(s.log.residuals))
         assert torch.equal(a.u, s.u)
