@@ -309,7 +309,7 @@ struct Timer {
 struct KernelTimer {
     bool on = false;
     cudaStream_t st = nullptr;
-    std::vector<cudaEvent_t> pool;
+    std::vector<cudaEvent_t>& pool;  // owned by the operator's KrylovCache: reused across solves
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pc_pending, op_pending;
     double pc_s = 0, op_s = 0;
     std::int64_t pc_n = 0, op_n = 0;
@@ -353,9 +353,7 @@ struct KernelTimer {
         op_pending.clear();
         used = 0;
     }
-    ~KernelTimer() {
-        for (auto e : pool) cudaEventDestroy(e);
-    }
+    explicit KernelTimer(std::vector<cudaEvent_t>& p) : pool(p) {}
 };
 
 constexpr int kSmallMgs = 16384;  // single-CTA orthogonalisation below this size
@@ -517,7 +515,7 @@ static void gmres(cpddg_op* op, cpddg_pc* pc, const double* b, double* u, const 
     DevBuf<double>& yd = ws.kc.yd;
     std::vector<const double*> vptr_h(static_cast<std::size_t>(cap));
 
-    KernelTimer kt;
+    KernelTimer kt(op->kc.events);
     kt.on = prm.profile_kernels != 0;
     kt.st = st;
     Timer timer(st);
@@ -675,7 +673,7 @@ static void stationary(cpddg_op* op, cpddg_pc* pc, const double* b, double* u, c
         double* p;
     } hh{ws.kc.host};
     DevBuf<double>& r = ws.kc.r;
-    KernelTimer kt;
+    KernelTimer kt(op->kc.events);
     kt.on = prm.profile_kernels != 0;
     kt.st = st;
     Timer timer(st);

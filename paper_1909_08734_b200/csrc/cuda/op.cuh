@@ -17,8 +17,10 @@ struct KrylovCache {
     double* host = nullptr;  // pinned scratch
     int host_cap = 0;
     cpddg::ReduceWork red;
+    std::vector<cudaEvent_t> events;  // per-launch timing events (profile_kernels), created once
     ~KrylovCache() {
         if (host) cudaFreeHost(host);
+        for (auto e : events) cudaEventDestroy(e);
     }
 };
 
