@@ -82,6 +82,13 @@ struct cpddg_pc {
     int bwd_prefetch = 1;  // backward L2 prefetch distance in blocks (0 = off)
     bool urows = true;     // backward layout: reversed U rows (true) or U columns (false)
     int shape = 1;         // solve block shape: 0 big (1 CTA/SM), 1 mid (2/SM), 2 small (4/SM)
+    // small systems: dense local inverses (k_solve_dense), row-major in factor order
+    bool dense = false, dense_probe = false;
+    int dense_tiles = 0;
+    std::int64_t dense_entries = 0;
+    cpddg::DevBuf<double> Ainv;
+    cpddg::DevBuf<std::int64_t> dense_base;
+    cpddg::DevBuf<int> dense_tile_sub, dense_tile_row0;
 };
 
 namespace cpddg {

@@ -961,6 +961,91 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) k_solve(const in
     }
 }
 
+// ------------------------------------------------------ small systems: dense inverses
+//
+// For a handful of small subdomains (BASELINE config 1: 8 systems of ~400
+// unknowns) the envelope solve is one CTA per subdomain walking a chain of
+// n dependent substitution steps (~60 us), with most of the GPU idle.  The
+// local inverses A_j^-1 (n_j^2 entries, formed once at setup from the
+// factors, column by column) turn the apply into a batched dense
+// matrix-vector product spread over many CTAs: each CTA gathers R_j r into
+// shared memory and produces kDenseRows rows of A_j^-1 (R_j r), then the
+// restricted scatter.  Rows are in factor order like everything else.
+
+constexpr int kDenseRows = 16;     // rows of one subdomain per CTA (one warp per 2 rows)
+constexpr int kDenseThreads = 256;
+
+__global__ void __launch_bounds__(kDenseThreads) k_solve_dense(const int* __restrict__ tile_sub,
+                                                               const int* __restrict__ tile_row0,
+                                                               const int* __restrict__ n_rows,
+                                                               const std::int64_t* __restrict__ vbase,
+                                                               const std::int64_t* __restrict__ dbase,
+                                                               const double* __restrict__ Ainv,
+                                                               const int* __restrict__ gidx_all,
+                                                               const int* __restrict__ sidx_all,
+                                                               const double* __restrict__ r, double* z,
+                                                               int accumulate, int mode3) {
+    extern __shared__ double b[];
+    const int j = tile_sub[blockIdx.x], row0 = tile_row0[blockIdx.x];
+    const int n = n_rows[j];
+    const std::int64_t vb = vbase[j];
+    for (int p = threadIdx.x; p < n; p += blockDim.x) {
+        if (mode3) {
+            b[p] = r[vb + p];
+        } else {
+            const int g = __ldg(gidx_all + vb + p);
+            b[p] = g >= 0 ? __ldg(r + g) : 0.0;
+        }
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const double* M = Ainv + dbase[j];
+    for (int rr = warp; rr < kDenseRows; rr += kDenseThreads / 32) {
+        const int i = row0 + rr;
+        if (i >= n) break;
+        const double* row = M + static_cast<std::int64_t>(i) * n;
+        double s0 = 0.0, s1 = 0.0;
+        int c = lane;
+        for (; c + 32 < n; c += 64) {
+            s0 = fma(__ldcs(row + c), b[c], s0);
+            s1 = fma(__ldcs(row + c + 32), b[c + 32], s1);
+        }
+        if (c < n) s0 = fma(__ldcs(row + c), b[c], s0);
+        const double v = warp_sum(s0 + s1);
+        if (lane == 0) {
+            if (mode3) {
+                z[vb + i] = v;
+            } else {
+                const int sg = __ldg(sidx_all + vb + i);
+                if (sg >= 0) z[sg] = accumulate ? z[sg] + v : v;
+            }
+        }
+    }
+}
+
+/** e_k probe right-hand sides (factor order, per-row arrays): r[vb + k] = 1. */
+__global__ void k_unit_rhs(int n_sub, const int* __restrict__ n_rows, const std::int64_t* __restrict__ vbase,
+                           int k, double* __restrict__ r) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < n_sub && k < n_rows[j]) r[vbase[j] + k] = 1.0;
+}
+__global__ void k_unit_clear(int n_sub, const int* __restrict__ n_rows, const std::int64_t* __restrict__ vbase,
+                             int k, double* __restrict__ r) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < n_sub && k < n_rows[j]) r[vbase[j] + k] = 0.0;
+}
+/** Column k of every A_j^-1 (z, factor order) into the row-major inverses. */
+__global__ void __launch_bounds__(256) k_store_column(int k, const int* __restrict__ n_rows,
+                                                      const std::int64_t* __restrict__ vbase,
+                                                      const std::int64_t* __restrict__ dbase,
+                                                      const double* __restrict__ z, double* __restrict__ Ainv) {
+    const int j = blockIdx.x;
+    const int n = n_rows[j];
+    if (k >= n) return;
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+        Ainv[dbase[j] + static_cast<std::int64_t>(i) * n + k] = z[vbase[j] + i];
+}
+
 template <class T>
 void append(std::vector<T>& dst, const std::vector<T>& src) {
     dst.insert(dst.end(), src.begin(), src.end());
@@ -998,6 +1083,14 @@ void pc_apply_mode(const cpddg_pc* pc, const double* r, double* z, bool accumula
     }();
     const int grid = (limit > 0 && mode != 3) ? std::min(limit, pc->n_sub) : pc->n_sub;
     const int dbg = mode == 3 ? 0 : dbg_flags;
+    if (pc->dense && (mode == 0 || (mode == 3 && pc->dense_probe))) {
+        k_solve_dense<<<pc->dense_tiles, kDenseThreads, sizeof(double) * pc->max_rows, st>>>(
+            pc->dense_tile_sub.get(), pc->dense_tile_row0.get(), pc->n_rows.get(), pc->vbase.get(),
+            pc->dense_base.get(), pc->Ainv.get(), pc->gidx.get(), pc->sidx.get(), r, z, accumulate ? 1 : 0,
+            mode == 3 ? 1 : 0);
+        CPDDG_CUDA(cudaGetLastError());
+        return;
+    }
     if (!pc->urows)
         launch_solve<false, ShapeMid>(pc, grid, r, z, accumulate, mode, dbg, st);
     else if (pc->shape == 0)
@@ -1239,10 +1332,72 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
                 throw DivergenceError("inaccurate factorization of subdomain " + std::to_string(j) +
                                       " (probe residual " + std::to_string(res[static_cast<std::size_t>(j)]) + ")");
     }
+    // small systems: dense inverses (k_solve_dense) when the envelope solve
+    // would be a latency-bound chain on a mostly idle GPU
+    {
+        std::int64_t dense_entries = 0;
+        for (int nj : n_rows) dense_entries += static_cast<std::int64_t>(nj) * nj;
+        const char* e = std::getenv("CPDDG_DENSE");
+        const bool auto_dense = pc->max_rows <= 1024 && n_sub <= sm_count() && 8 * dense_entries <= (256LL << 20);
+        pc->dense = e ? std::string(e) == "1" && 8 * dense_entries <= (4LL << 30) : auto_dense;
+        if (pc->dense) {
+            std::vector<std::int64_t> dbase(static_cast<std::size_t>(n_sub));
+            std::vector<int> tsub, trow;
+            std::int64_t acc = 0;
+            for (int j = 0; j < n_sub; ++j) {
+                dbase[static_cast<std::size_t>(j)] = acc;
+                acc += static_cast<std::int64_t>(n_rows[static_cast<std::size_t>(j)]) * n_rows[static_cast<std::size_t>(j)];
+                for (int r0 = 0; r0 < n_rows[static_cast<std::size_t>(j)]; r0 += kDenseRows) {
+                    tsub.push_back(j);
+                    trow.push_back(r0);
+                }
+            }
+            pc->dense_base.upload(dbase);
+            pc->dense_tile_sub.upload(tsub);
+            pc->dense_tile_row0.upload(trow);
+            pc->dense_tiles = static_cast<int>(tsub.size());
+            pc->Ainv.alloc(static_cast<std::size_t>(std::max<std::int64_t>(acc, 1)));
+            if (static_cast<int>(sizeof(double)) * pc->max_rows > 48 * 1024)
+                CPDDG_CUDA(cudaFuncSetAttribute(k_solve_dense, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                static_cast<int>(sizeof(double)) * pc->max_rows));
+            // column k of A_j^-1 = the envelope solve of e_k, for all subdomains at once
+            DevBuf<double> er(static_cast<std::size_t>(vb)), ez(static_cast<std::size_t>(vb));
+            er.zero();
+            const int ub = (n_sub + 127) / 128;
+            for (int k = 0; k < pc->max_rows; ++k) {
+                k_unit_rhs<<<ub, 128>>>(n_sub, pc->n_rows.get(), pc->vbase.get(), k, er.get());
+                pc_apply_mode(pc.get(), er.get(), ez.get(), false, 3, nullptr);  // envelope path (dense_probe off)
+                k_store_column<<<n_sub, 256>>>(k, pc->n_rows.get(), pc->vbase.get(), pc->dense_base.get(), ez.get(),
+                                               pc->Ainv.get());
+                k_unit_clear<<<ub, 128>>>(n_sub, pc->n_rows.get(), pc->vbase.get(), k, er.get());
+            }
+            CPDDG_CUDA(cudaGetLastError());
+            CPDDG_CUDA(cudaDeviceSynchronize());
+            pc->dense_entries = acc;
+            // the inverses reproduce the envelope solve on the probe right-hand sides
+            if (!probe_all.empty()) {
+                DevBuf<double> pb, z1(static_cast<std::size_t>(vb)), z2(static_cast<std::size_t>(vb));
+                pb.upload(probe_all);
+                pc_apply_mode(pc.get(), pb.get(), z1.get(), false, 3, nullptr);
+                pc->dense_probe = true;
+                pc_apply_mode(pc.get(), pb.get(), z2.get(), false, 3, nullptr);
+                pc->dense_probe = false;
+                std::vector<double> a(static_cast<std::size_t>(vb)), c(static_cast<std::size_t>(vb));
+                CPDDG_CUDA(cudaMemcpy(a.data(), z1.get(), a.size() * sizeof(double), cudaMemcpyDeviceToHost));
+                CPDDG_CUDA(cudaMemcpy(c.data(), z2.get(), c.size() * sizeof(double), cudaMemcpyDeviceToHost));
+                double dmax = 0.0, amax = 0.0;
+                for (std::size_t q = 0; q < a.size(); ++q) {
+                    dmax = std::max(dmax, std::abs(a[q] - c[q]));
+                    amax = std::max(amax, std::abs(a[q]));
+                }
+                if (!(dmax <= 1e-10 * amax)) pc->dense = false;  // keep the envelope solve
+            }
+        }
+    }
     // bytes one apply streams: L, U, diag, first, roff per row, gather/scatter maps, r gathers, z writes
     // streamed per apply: L and reversed-U values, diagonal, and the per-row
     // tables (first + offset) of both passes
-    pc->factor_bytes = 8 * (ebs + pc->u_entries + vb) + 2 * 12 * vb;
+    pc->factor_bytes = pc->dense ? 8 * pc->dense_entries : 8 * (ebs + pc->u_entries + vb) + 2 * 12 * vb;
     std::int64_t gathers = 0, scatters = 0;
     for (int g : gidx) gathers += g >= 0 ? 1 : 0;
     for (int s : sidx) scatters += s >= 0 ? 1 : 0;
