@@ -355,12 +355,13 @@ def main():
             "setup_s": {"problem": t_problem, "decompose": t_decomp, "factor_and_upload": t_locals,
                         "device_factor": pcs["factor_seconds"], "host_analyse": pcs["analyse_seconds"]},
             "pc": {k: pcs[k] for k in ("factor_entries", "profile_entries", "factor_bytes", "n_rows_total",
-                                       "max_rows", "n_reduced", "max_probe_residual")},
+                                       "max_rows", "n_reduced", "max_probe_residual", "apply_mode")},
             "pc_stored_over_profile": pcs["factor_entries"] / pcs["profile_entries"],
             "kernel_ms": {"pc_apply_avg": 1e3 * avg_pc, "op_apply_avg": 1e3 * op_s / max(op_n, 1)},
             "op_roofline_GBs": op_alg / (op_s / max(op_n, 1)) / 1e9 if op_n else None,
         },
-        "roofline": {"bound": "hbm", "kernel": "k_solve (preconditioner apply)", "achieved": achieved,
+        "roofline": {"bound": "hbm", "kernel": "k_solve_dense (preconditioner apply, dense small-system mode)"
+                     if pcs["apply_mode"] == 1 else "k_solve (preconditioner apply)", "achieved": achieved,
                      "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "traffic": ncu_traffic(),
                      "algorithmic_bytes_per_launch": pcs["algorithmic_bytes"], "peak_source": peak_src},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n},

@@ -162,13 +162,14 @@ typedef struct {
     int n_reduced;              /* subdomains whose Dirichlet closure block was eliminated */
     int64_t n_rows_total;       /* sum of factored system sizes */
     int64_t factor_entries;     /* stored L + U + diag entries */
-    int64_t profile_entries;    /* minimal symmetric-profile entries (2 sum_i (i - f_i) + n) */
-    int64_t factor_bytes;       /* bytes the triangular solves stream per apply */
+    int64_t profile_entries;    /* envelope entries: sum_i (i - fL_i) + sum_c (c - fU_c) + n (nonsymmetric envelopes) */
+    int64_t factor_bytes;       /* bytes the apply streams (factors, or the dense inverses in apply_mode 1) */
     int64_t algorithmic_bytes;  /* B_pc of SURVEY.md 8(d) */
     int max_rows;
     double factor_seconds;      /* device factorisation time */
     double analyse_seconds;     /* host ordering + symbolic time */
     double max_probe_residual;  /* when check_residual */
+    int apply_mode;             /* 0: envelope triangular solves (k_solve); 1: dense local inverses (small systems) */
 } cpddg_pc_stats;
 
 int cpddg_pc_create(int n_global, int n_sub, const cpddg_local_desc* locals,
