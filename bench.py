@@ -362,7 +362,8 @@ def main():
         },
         "roofline": {"bound": "hbm", "kernel": "k_solve_dense (preconditioner apply, dense small-system mode)"
                      if pcs["apply_mode"] == 1 else "k_solve (preconditioner apply)", "achieved": achieved,
-                     "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "traffic": ncu_traffic(),
+                     "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                     "traffic": ncu_traffic() if WORKLOAD is CONFIGS["headline"] else None,
                      "algorithmic_bytes_per_launch": pcs["algorithmic_bytes"], "peak_source": peak_src},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n},
         "gpu_launches": launches,
