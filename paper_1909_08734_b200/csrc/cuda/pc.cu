@@ -45,6 +45,21 @@ namespace cpddg {
 
 namespace {
 
+/** Streaming loads of factor data: ld.global.nc with L1::no_allocate (the
+ *  data is used once; keeps L1 for the index tables).  Measured on B200
+ *  (scripts/micro/ld_variants.cu): one SM streams 162 GB/s this way but only
+ *  58 GB/s with ld.global.cs (__ldcs), which capped the doubly-loaded SMs. */
+__device__ __forceinline__ double ld_stream(const double* p) {
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double2 ld_stream(const double2* p) {
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+
 constexpr int NB = 32;    // factor panel width
 constexpr int TILE = 64;  // trailing-update tile
 
@@ -593,8 +608,8 @@ __device__ __forceinline__ void lower_solve(int n, const int* __restrict__ f, co
                 const double* Li = V + (__ldg(ro + i) - fi);
                 // stash loads first: they share the round trip of the partial loads
                 const int col0 = lim + lane, col1 = lim + lane + 32;
-                const double t0 = (lane < 2 * RB && col0 >= fi && col0 < i) ? __ldcs(Li + col0) : 0.0;
-                const double t1 = (lane + 32 < 2 * RB && col1 >= fi && col1 < i) ? __ldcs(Li + col1) : 0.0;
+                const double t0 = (lane < 2 * RB && col0 >= fi && col0 < i) ? ld_stream(Li + col0) : 0.0;
+                const double t1 = (lane + 32 < 2 * RB && col1 >= fi && col1 < i) ? ld_stream(Li + col1) : 0.0;
                 double s1 = 0.0, s2 = 0.0, s3 = 0.0;
                 const double2* Li2 = reinterpret_cast<const double2*>(Li + fi);  // fi even, row 16B-aligned
                 const double2* y2 = reinterpret_cast<const double2*>(y);
@@ -603,7 +618,7 @@ __device__ __forceinline__ void lower_solve(int n, const int* __restrict__ f, co
 #pragma unroll
                     for (int u = 0; u < 8; ++u) {
                         const int c = base + 2 * lane + 64 * u;
-                        a[u] = c < lim ? __ldcs(Li2 + ((c - fi) >> 1)) : make_double2(0.0, 0.0);
+                        a[u] = c < lim ? ld_stream(Li2 + ((c - fi) >> 1)) : make_double2(0.0, 0.0);
                     }
 #pragma unroll
                     for (int u = 0; u < 8; u += 2) {
@@ -771,7 +786,7 @@ __device__ __forceinline__ void upper_solve_cols(int n, const int* __restrict__ 
                 if (col < n && i < col) {
                     const int slot = (cl < RB ? K : K + 1) & 3, cc = cl < RB ? cl : cl - RB;
                     const int fc = cf[slot][cc];
-                    if (i >= fc) v[q] = __ldcs(V + cro[slot][cc] + (i - fc));
+                    if (i >= fc) v[q] = ld_stream(V + cro[slot][cc] + (i - fc));
                 }
             }
         }
@@ -852,7 +867,7 @@ __device__ __forceinline__ void upper_solve_cols(int n, const int* __restrict__ 
                         for (int u = 0; u < 10; ++u) {
                             const int c = cb + u;
                             a[u] = (ok && c < cb1 && jr >= cf[nxt][c])
-                                       ? __ldcs(reinterpret_cast<const double2*>(V + cro[nxt][c] + (jr - cf[nxt][c])))
+                                       ? ld_stream(reinterpret_cast<const double2*>(V + cro[nxt][c] + (jr - cf[nxt][c])))
                                        : make_double2(0.0, 0.0);
                         }
 #pragma unroll
@@ -1007,10 +1022,10 @@ __global__ void __launch_bounds__(kDenseThreads) k_solve_dense(const int* __rest
         double s0 = 0.0, s1 = 0.0;
         int c = lane;
         for (; c + 32 < n; c += 64) {
-            s0 = fma(__ldcs(row + c), b[c], s0);
-            s1 = fma(__ldcs(row + c + 32), b[c + 32], s1);
+            s0 = fma(ld_stream(row + c), b[c], s0);
+            s1 = fma(ld_stream(row + c + 32), b[c + 32], s1);
         }
-        if (c < n) s0 = fma(__ldcs(row + c), b[c], s0);
+        if (c < n) s0 = fma(ld_stream(row + c), b[c], s0);
         const double v = warp_sum(s0 + s1);
         if (lane == 0) {
             if (mode3) {
