@@ -35,6 +35,7 @@
 #include <algorithm>
 #include <chrono>
 #include <climits>
+#include <cstdio>
 #include <cstdlib>
 #include <string>
 #include <type_traits>
@@ -79,20 +80,29 @@ struct HostSub {
  *  Components in order of their lowest-degree node; each starts at a
  *  pseudo-peripheral node (repeated BFS, min-degree node of the last level);
  *  neighbours enqueued by (degree, index).  Returns perm[new] = old. */
-std::vector<int> rcm(const std::vector<std::vector<int>>& adj) {
-    const int n = static_cast<int>(adj.size());
+/** Symmetric pattern in CSR form: neighbours of v are adj[xadj[v] .. xadj[v+1]), sorted. */
+struct Graph {
+    std::vector<int> xadj, adj;
+    int size() const { return static_cast<int>(xadj.size()) - 1; }
+    const int* begin(int v) const { return adj.data() + xadj[static_cast<std::size_t>(v)]; }
+    const int* end(int v) const { return adj.data() + xadj[static_cast<std::size_t>(v) + 1]; }
+    int degree(int v) const { return xadj[static_cast<std::size_t>(v) + 1] - xadj[static_cast<std::size_t>(v)]; }
+};
+
+std::vector<int> rcm(const Graph& g) {
+    const int n = g.size();
     std::vector<int> order;
     order.reserve(static_cast<std::size_t>(n));
     std::vector<char> done(static_cast<std::size_t>(n), 0);
     std::vector<int> level(static_cast<std::size_t>(n), -1);
-    auto deg = [&](int v) { return static_cast<int>(adj[static_cast<std::size_t>(v)].size()); };
+    auto deg = [&](int v) { return g.degree(v); };
     auto far_node = [&](int s, int& ecc) {
         std::vector<int> q{s};
         level[static_cast<std::size_t>(s)] = 0;
         for (std::size_t h = 0; h < q.size(); ++h) {
             const int v = q[h];
-            for (int w : adj[static_cast<std::size_t>(v)])
-                if (!done[static_cast<std::size_t>(w)] && level[static_cast<std::size_t>(w)] < 0) {
+            for (const int* pw = g.begin(v); pw != g.end(v); ++pw)
+                if (const int w = *pw; !done[static_cast<std::size_t>(w)] && level[static_cast<std::size_t>(w)] < 0) {
                     level[static_cast<std::size_t>(w)] = level[static_cast<std::size_t>(v)] + 1;
                     q.push_back(w);
                 }
@@ -127,8 +137,8 @@ std::vector<int> rcm(const std::vector<std::vector<int>>& adj) {
         done[static_cast<std::size_t>(s)] = 1;
         for (std::size_t h = start; h < order.size(); ++h) {
             nb.clear();
-            for (int w : adj[static_cast<std::size_t>(order[h])])
-                if (!done[static_cast<std::size_t>(w)]) nb.push_back(w);
+            for (const int* pw = g.begin(order[h]); pw != g.end(order[h]); ++pw)
+                if (!done[static_cast<std::size_t>(*pw)]) nb.push_back(*pw);
             std::sort(nb.begin(), nb.end(), [&](int a, int b) { return deg(a) != deg(b) ? deg(a) < deg(b) : a < b; });
             for (int w : nb) {
                 done[static_cast<std::size_t>(w)] = 1;
@@ -156,19 +166,38 @@ HostSub analyse(const cpddg_local_desc& d, int n_global) {
     S.reduced = reducible && d.n_bc > 0;
     const int n = reducible ? d.n_overlap : nl;
     S.n = n;
-    std::vector<std::vector<int>> adj(static_cast<std::size_t>(n));
-    for (int r = 0; r < n; ++r)
-        for (std::int64_t k = rp[r]; k < rp[r + 1]; ++k) {
-            const int c = d.col[k];
-            if (c >= n || c == r) continue;
-            adj[static_cast<std::size_t>(r)].push_back(c);
-            adj[static_cast<std::size_t>(c)].push_back(r);
+    // pattern(A + A^T) without the diagonal, CSR: count, fill, sort + unique per row
+    Graph gr;
+    {
+        std::vector<int> cnt(static_cast<std::size_t>(n) + 1, 0);
+        for (int r = 0; r < n; ++r)
+            for (std::int64_t k = rp[r]; k < rp[r + 1]; ++k) {
+                const int c = d.col[k];
+                if (c >= n || c == r) continue;
+                ++cnt[static_cast<std::size_t>(r) + 1];
+                ++cnt[static_cast<std::size_t>(c) + 1];
+            }
+        for (int v = 0; v < n; ++v) cnt[static_cast<std::size_t>(v) + 1] += cnt[static_cast<std::size_t>(v)];
+        std::vector<int> raw(static_cast<std::size_t>(cnt[static_cast<std::size_t>(n)])), fill(cnt.begin(), cnt.end() - 1);
+        for (int r = 0; r < n; ++r)
+            for (std::int64_t k = rp[r]; k < rp[r + 1]; ++k) {
+                const int c = d.col[k];
+                if (c >= n || c == r) continue;
+                raw[static_cast<std::size_t>(fill[static_cast<std::size_t>(r)]++)] = c;
+                raw[static_cast<std::size_t>(fill[static_cast<std::size_t>(c)]++)] = r;
+            }
+        gr.xadj.assign(static_cast<std::size_t>(n) + 1, 0);
+        gr.adj.reserve(raw.size());
+        for (int v = 0; v < n; ++v) {
+            int* b = raw.data() + cnt[static_cast<std::size_t>(v)];
+            int* e = raw.data() + cnt[static_cast<std::size_t>(v) + 1];
+            std::sort(b, e);
+            e = std::unique(b, e);
+            gr.adj.insert(gr.adj.end(), b, e);
+            gr.xadj[static_cast<std::size_t>(v) + 1] = static_cast<int>(gr.adj.size());
         }
-    for (auto& a : adj) {
-        std::sort(a.begin(), a.end());
-        a.erase(std::unique(a.begin(), a.end()), a.end());
     }
-    const std::vector<int> perm = rcm(adj);
+    const std::vector<int> perm = rcm(gr);
     std::vector<int> inv(static_cast<std::size_t>(n));
     for (int k = 0; k < n; ++k) inv[static_cast<std::size_t>(perm[static_cast<std::size_t>(k)])] = k;
     // envelopes of the actual (nonsymmetric) pattern in factor order: L row i
@@ -261,24 +290,47 @@ HostSub analyse(const cpddg_local_desc& d, int n_global) {
     return S;
 }
 
-/** Scatter A_j (the factored system, Dirichlet closure eliminated) into
- *  envelope storage: L rows, U columns, diagonal (factor order). */
-void scatter_values(const cpddg_local_desc& d, const HostSub& S, double* L, double* U, double* diag) {
+/** The entries of A_j as (destination, value) pairs: destination = slot in
+ *  the concatenated L (tag 0), U (tag 1) or diagonal (tag 2) storage, tag in
+ *  the top two bits.  Built on the host per subdomain (16 bytes per entry)
+ *  and scattered on the device into the zeroed envelopes (k_scatter_pairs):
+ *  the envelopes themselves (~40 MB per headline subdomain, mostly fill)
+ *  never cross the host link. */
+constexpr int kTagShift = 62;
+std::int64_t scatter_pairs(const cpddg_local_desc& d, const HostSub& S, std::int64_t eb, std::int64_t ebu,
+                           std::int64_t v0, std::int64_t* dst, double* val) {
     const int n = S.n;
     const std::int64_t* rp = d.row_ptr;
+    std::int64_t m = 0;
     for (int r = 0; r < n; ++r)
         for (std::int64_t k = rp[r]; k < rp[r + 1]; ++k) {
             const int c = d.col[k];
             if (c >= n) continue;  // eliminated Dirichlet closure column (z_b = 0)
             const int pi = S.inv[static_cast<std::size_t>(r)], pj = S.inv[static_cast<std::size_t>(c)];
-            const double v = d.val[k];
+            std::int64_t to;
             if (pi == pj)
-                diag[pi] += v;
+                to = (2LL << kTagShift) | (v0 + pi);
             else if (pj < pi)
-                L[S.roff[static_cast<std::size_t>(pi)] + (pj - S.first[static_cast<std::size_t>(pi)])] += v;
+                to = eb + S.roff[static_cast<std::size_t>(pi)] + (pj - S.first[static_cast<std::size_t>(pi)]);
             else
-                U[S.roffU[static_cast<std::size_t>(pj)] + (pi - S.firstU[static_cast<std::size_t>(pj)])] += v;
+                to = (1LL << kTagShift) | (ebu + S.roffU[static_cast<std::size_t>(pj)] + (pi - S.firstU[static_cast<std::size_t>(pj)]));
+            dst[m] = to;
+            val[m] = d.val[k];
+            ++m;
         }
+    return m;
+}
+
+__global__ void k_scatter_pairs(std::int64_t m, const std::int64_t* __restrict__ dst, const double* __restrict__ val,
+                                double* L, double* U, double* diag) {
+    for (std::int64_t e = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; e < m;
+         e += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const std::int64_t t = dst[e];
+        const int tag = static_cast<int>(static_cast<unsigned long long>(t) >> kTagShift);
+        const std::int64_t i = t & ((1LL << kTagShift) - 1);
+        double* base = tag == 0 ? L : tag == 1 ? U : diag;
+        atomicAdd(base + i, val[e]);  // duplicate (r, c) entries of the CSR are summed
+    }
 }
 
 struct SubPtrs {
@@ -1159,20 +1211,50 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
     pc->L.alloc(static_cast<std::size_t>(std::max<std::int64_t>(ebs, 1)));
     pc->U.alloc(static_cast<std::size_t>(std::max<std::int64_t>(ebsU, 1)));
     pc->diag.alloc(static_cast<std::size_t>(vb));
-    parallel_for(n_sub, opt ? opt->workers : 0, [&](int j, int) {
-        const HostSub& S = subs[static_cast<std::size_t>(j)];
-        std::vector<double> Lb(static_cast<std::size_t>(S.ne), 0.0), Ub(static_cast<std::size_t>(S.neU), 0.0),
-            Db(static_cast<std::size_t>(S.n), 0.0);
-        scatter_values(locals[j], S, Lb.data(), Ub.data(), Db.data());
-        const std::size_t eb = static_cast<std::size_t>(ebase[static_cast<std::size_t>(j)]);
-        const std::size_t ebu = static_cast<std::size_t>(ebaseU[static_cast<std::size_t>(j)]);
-        const std::size_t v0 = static_cast<std::size_t>(vbase[static_cast<std::size_t>(j)]);
-        if (S.ne)
-            CPDDG_CUDA(cudaMemcpy(pc->L.get() + eb, Lb.data(), Lb.size() * sizeof(double), cudaMemcpyHostToDevice));
-        if (S.neU)
-            CPDDG_CUDA(cudaMemcpy(pc->U.get() + ebu, Ub.data(), Ub.size() * sizeof(double), cudaMemcpyHostToDevice));
-        CPDDG_CUDA(cudaMemcpy(pc->diag.get() + v0, Db.data(), Db.size() * sizeof(double), cudaMemcpyHostToDevice));
-    });
+    const auto t_an = std::chrono::steady_clock::now();
+    {
+        // A_j's entries as (destination, value) pairs, scattered on the device
+        std::vector<std::int64_t> pbase(static_cast<std::size_t>(n_sub) + 1, 0);
+        for (int j = 0; j < n_sub; ++j)
+            pbase[static_cast<std::size_t>(j) + 1] =
+                pbase[static_cast<std::size_t>(j)] + locals[j].row_ptr[subs[static_cast<std::size_t>(j)].n];
+        const std::int64_t cap = std::max<std::int64_t>(pbase.back(), 1);
+        DevBuf<std::int64_t> pdst(static_cast<std::size_t>(cap));
+        DevBuf<double> pval(static_cast<std::size_t>(cap));
+        std::vector<std::int64_t> used(static_cast<std::size_t>(n_sub), 0);
+        CPDDG_CUDA(cudaMemset(pc->L.get(), 0, sizeof(double) * static_cast<std::size_t>(std::max<std::int64_t>(ebs, 1))));
+        CPDDG_CUDA(cudaMemset(pc->U.get(), 0, sizeof(double) * static_cast<std::size_t>(std::max<std::int64_t>(ebsU, 1))));
+        CPDDG_CUDA(cudaMemset(pc->diag.get(), 0, sizeof(double) * static_cast<std::size_t>(vb)));
+        parallel_for(n_sub, opt ? opt->workers : 0, [&](int j, int) {
+            const HostSub& S = subs[static_cast<std::size_t>(j)];
+            const std::int64_t room = pbase[static_cast<std::size_t>(j) + 1] - pbase[static_cast<std::size_t>(j)];
+            std::vector<std::int64_t> dst(static_cast<std::size_t>(room));
+            std::vector<double> val(static_cast<std::size_t>(room));
+            const std::int64_t m = scatter_pairs(locals[j], S, ebase[static_cast<std::size_t>(j)],
+                                                 ebaseU[static_cast<std::size_t>(j)], vbase[static_cast<std::size_t>(j)],
+                                                 dst.data(), val.data());
+            used[static_cast<std::size_t>(j)] = m;
+            const std::size_t o = static_cast<std::size_t>(pbase[static_cast<std::size_t>(j)]);
+            if (m) {
+                CPDDG_CUDA(cudaMemcpy(pdst.get() + o, dst.data(), sizeof(std::int64_t) * m, cudaMemcpyHostToDevice));
+                CPDDG_CUDA(cudaMemcpy(pval.get() + o, val.data(), sizeof(double) * m, cudaMemcpyHostToDevice));
+            }
+        });
+        // unused tails of each subdomain's range: point them at a harmless zero add
+        for (int j = 0; j < n_sub; ++j) {
+            const std::int64_t o = pbase[static_cast<std::size_t>(j)] + used[static_cast<std::size_t>(j)];
+            const std::int64_t rest = pbase[static_cast<std::size_t>(j) + 1] - o;
+            if (rest > 0) {
+                CPDDG_CUDA(cudaMemset(pdst.get() + o, 0, sizeof(std::int64_t) * static_cast<std::size_t>(rest)));
+                CPDDG_CUDA(cudaMemset(pval.get() + o, 0, sizeof(double) * static_cast<std::size_t>(rest)));
+            }
+        }
+        const int blocks = 4 * sm_count();
+        k_scatter_pairs<<<blocks, 256>>>(pbase.back(), pdst.get(), pval.get(), pc->L.get(), pc->U.get(),
+                                         pc->diag.get());
+        CPDDG_CUDA(cudaGetLastError());
+        CPDDG_CUDA(cudaDeviceSynchronize());
+    }
     first.reserve(static_cast<std::size_t>(vb));
     for (auto& S : subs) {
         append(first, S.first);
@@ -1231,6 +1313,9 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
     pc->sidx.upload(sidx);
 
     const auto t1 = std::chrono::steady_clock::now();
+    if (std::getenv("CPDDG_VERBOSE"))
+        std::fprintf(stderr, "[cpddg] pc analyse %.3f s, scatter+upload %.3f s\n",
+                     std::chrono::duration<double>(t_an - t0).count(), std::chrono::duration<double>(t1 - t_an).count());
     pc->analyse_seconds = std::chrono::duration<double>(t1 - t0).count();
 
     // device factorisation
