@@ -23,6 +23,7 @@
 #include "op.cuh"
 
 #include <cmath>
+#include <numeric>
 
 namespace cpddg {
 
@@ -198,6 +199,7 @@ __global__ void __launch_bounds__(256) k_extend_p3(int nb, const double* __restr
  *  is k_extend_p3's ((a0 + a1) + (a2 + a3)), so v is bit-identical. */
 __global__ void __launch_bounds__(kExtTile, CPDDG_EXT_MINB) k_extend_staged(int nb, const double* __restrict__ t,
                                                            const std::uint16_t* __restrict__ lines16,
+                                                           const int* __restrict__ perm,
                                                            const int* __restrict__ tile_k0,
                                                            const int* __restrict__ stage_base,
                                                            const int* __restrict__ stage_idx,
@@ -246,7 +248,7 @@ __global__ void __launch_bounds__(kExtTile, CPDDG_EXT_MINB) k_extend_staged(int 
         }
         part[a] = __dmul_rn(w0[a], sa);
     }
-    v[k] = (part[0] + part[1]) + (part[2] + part[3]);
+    v[__ldg(perm + k)] = (part[0] + part[1]) + (part[2] + part[3]);  // k is the tile slot
 }
 
 /** y = cg x - ih2 sum v[nbr]; if b != nullptr: y <- b - y and partial ||y||^2. */
@@ -303,8 +305,14 @@ __global__ void __launch_bounds__(kRedThreads) k_helm(int na, double cg, double 
  *  sorted unique active ordinals its runs cover and every run's 16-bit start
  *  inside that list.  Left empty (gather kernel) if even a 32-node tile
  *  overflows the cap. */
-static void build_stage(cpddg_op* op, const std::vector<int>& lines, int nb) {
+static void build_stage(cpddg_op* op, const std::vector<int>& lines, const std::vector<double>& t, int nb) {
     constexpr int R = 16, Q = 4;
+    // within a tile, threads take the nodes in order of their first stencil
+    // run (x, y, z of the stencil base): the lanes of a warp then read the
+    // same few stage rows, so a stencil read is ~1-2 shared-memory wavefronts
+    // instead of one per column group in the warp
+    std::vector<int> perm(static_cast<std::size_t>(nb));
+    std::vector<double> tp(static_cast<std::size_t>(3) * nb);
     const int groups = (nb + kExtTile - 1) / kExtTile;
     struct Tile {
         int k0, k1;
@@ -342,12 +350,20 @@ static void build_stage(cpddg_op* op, const std::vector<int>& lines, int nb) {
                 todo.push_back({k0, mid});
                 continue;
             }
-            for (int l = 0; l < R; ++l)
-                for (int k = k0; k < k1; ++k) {
+            std::vector<int> ord(static_cast<std::size_t>(k1 - k0));
+            std::iota(ord.begin(), ord.end(), k0);
+            std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return lines[a] < lines[b]; });
+            for (int q = 0; q < k1 - k0; ++q) {
+                const int k = ord[static_cast<std::size_t>(q)], slot = k0 + q;
+                perm[static_cast<std::size_t>(slot)] = k;
+                for (int a = 0; a < 3; ++a)
+                    tp[static_cast<std::size_t>(a) * nb + slot] = t[static_cast<std::size_t>(a) * nb + k];
+                for (int l = 0; l < R; ++l) {
                     const int o = lines[static_cast<std::size_t>(l) * nb + k];
-                    l16[static_cast<std::size_t>(l) * nb + k] =
+                    l16[static_cast<std::size_t>(l) * nb + slot] =
                         static_cast<std::uint16_t>(std::lower_bound(u.begin(), u.end(), o) - u.begin());
                 }
+            }
             out.push_back({k0, k1, std::move(u)});
         }
     });
@@ -362,6 +378,8 @@ static void build_stage(cpddg_op* op, const std::vector<int>& lines, int nb) {
         }
     k0s.push_back(nb);
     op->lines16.upload(l16);
+    op->ext_perm.upload(perm);
+    op->ext_t.upload(tp);
     op->tile_k0.upload(k0s);
     op->stage_base.upload(base);
     op->stage_idx.upload(idx);
@@ -418,7 +436,7 @@ static void build_tables(cpddg_op* op, const Ix<D>* ix, const Vec<D>* cp, const 
         }
     }
     if constexpr (D == 3) {
-        if (p == 3 && !std::getenv("CPDDG_EXT_GATHER")) build_stage(op, lines, nb);
+        if (p == 3 && !std::getenv("CPDDG_EXT_GATHER")) build_stage(op, lines, t, nb);
     }
     op->t.upload(t);
     op->lines.upload(lines);
@@ -439,8 +457,8 @@ static void launch_apply(const cpddg_op* op, const double* x, const double* b, d
     const int nb = op->na + op->ng;
     const int thr = 256;
     if (op->ext_tiles) {
-        k_extend_staged<<<op->ext_tiles, kExtTile, op->ext_smem, st>>>(nb, op->t.get(), op->lines16.get(),
-                                                                       op->tile_k0.get(),
+        k_extend_staged<<<op->ext_tiles, kExtTile, op->ext_smem, st>>>(nb, op->ext_t.get(), op->lines16.get(),
+                                                                       op->ext_perm.get(), op->tile_k0.get(),
                                                                        op->stage_base.get(), op->stage_idx.get(), x,
                                                                        op->v.get());
     } else if (op->p == 3) {

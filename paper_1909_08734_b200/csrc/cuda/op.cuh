@@ -36,7 +36,9 @@ struct cpddg_op {
     // memory and addresses them with 16-bit tile-local run starts.
     int ext_tiles = 0, ext_smem = 0;                // 0 tiles: gather kernel
     cpddg::DevBuf<std::uint16_t> lines16;          // [16][N_B] run start in the tile's stage
-    cpddg::DevBuf<int> tile_k0;                     // [tiles+1] first band node of each tile
+    cpddg::DevBuf<int> tile_k0;                     // [tiles+1] first slot of each tile
+    cpddg::DevBuf<int> ext_perm;                    // [N_B] band node computed by each tile slot
+    cpddg::DevBuf<double> ext_t;                    // [d][N_B] stencil offsets in slot order
     cpddg::DevBuf<int> stage_base;                  // [tiles+1] first entry of each tile's stage list
     cpddg::DevBuf<int> stage_idx;                   // stage list: active ordinal of each staged x
     cpddg::DevBuf<double> rn2;  // scalar slot for ||b - A x||^2
