@@ -24,6 +24,12 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#if defined(__GNUC__)
+#define CPDDG_API __attribute__((visibility("default")))
+#else
+#define CPDDG_API
+#endif
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -38,8 +44,8 @@ enum {
 };
 
 /** Copy the calling thread's last error message into buf; returns its code. */
-int cpddg_last_error(char* buf, size_t len);
-const char* cpddg_version(void);
+CPDDG_API int cpddg_last_error(char* buf, size_t len);
+CPDDG_API const char* cpddg_version(void);
 
 /* ======================================================================
  * Host setup.  Mirrors build_problem (proj/include/cpdd/pipeline.hpp:155-168)
@@ -67,16 +73,16 @@ typedef struct {
 
 /** build_band_tube + build_extension + assemble_helmholtz
  *  (band.hpp:150-182, operators.hpp:30-51, 96-112). */
-int cpddg_setup_create(const cpddg_problem_desc* desc, cpddg_setup** out);
-int cpddg_setup_destroy(cpddg_setup* s);
+CPDDG_API int cpddg_setup_create(const cpddg_problem_desc* desc, cpddg_setup** out);
+CPDDG_API int cpddg_setup_destroy(cpddg_setup* s);
 /** n_active, n_ghost, nnz(E), nnz(A). */
-int cpddg_setup_sizes(const cpddg_setup* s, int* n_active, int* n_ghost, int64_t* nnz_E,
+CPDDG_API int cpddg_setup_sizes(const cpddg_setup* s, int* n_active, int* n_ghost, int64_t* nnz_E,
                       int64_t* nnz_A);
 /** Band nodes in band-code order (BandGrid::active then ::ghost,
  *  band.hpp:36-60): lattice index (N_B x dim), cp, normal (N_B x dim), dist. */
-int cpddg_setup_band(const cpddg_setup* s, int32_t* ix, double* cp, double* normal, double* dist);
+CPDDG_API int cpddg_setup_band(const cpddg_setup* s, int32_t* ix, double* cp, double* normal, double* dist);
 /** CSR of E (which = 0) or A (which = 1) (SparseOperator, sparse.hpp:19-103). */
-int cpddg_setup_csr(const cpddg_setup* s, int which, int64_t* row_ptr, int32_t* col, double* val);
+CPDDG_API int cpddg_setup_csr(const cpddg_setup* s, int which, int64_t* row_ptr, int32_t* col, double* val);
 
 enum { CPDDG_RAS = 0, CPDDG_ORAS = 1 };
 
@@ -87,22 +93,22 @@ enum { CPDDG_RAS = 0, CPDDG_ORAS = 1 };
  *  (ConfigError otherwise, as load_partition).  alpha_cross < 0 means alpha
  *  (SolverConfig::effective_alpha_cross, solve.hpp:38).  part_out (may be
  *  NULL) receives the aligned labels, moves the alignment move count. */
-int cpddg_setup_decompose(cpddg_setup* s, const int32_t* part, int n_part, int n_overlap, int method,
+CPDDG_API int cpddg_setup_decompose(cpddg_setup* s, const int32_t* part, int n_part, int n_overlap, int method,
                           double alpha, double alpha_cross, int32_t* part_out, int* moves);
-int cpddg_setup_n_subdomains(const cpddg_setup* s);
+CPDDG_API int cpddg_setup_n_subdomains(const cpddg_setup* s);
 /** counts[8] = |disjoint|, |overlap|, |final_layer|, |ghosts|, |bc|,
  *  fallback_count, n_lambda, #cross_flagged (Subdomain, subdomain.hpp:47-56). */
-int cpddg_setup_subdomain_counts(const cpddg_setup* s, int j, int32_t* counts);
+CPDDG_API int cpddg_setup_subdomain_counts(const cpddg_setup* s, int j, int32_t* counts);
 /** bc_int: |bc| x (dim+4) = ix..., global_active, is_ghost_type,
  *  cross_flagged, fallback; bc_real: |bc| x (4 dim + 1) = x, cp, cp_local,
  *  conormal, dq (BoundaryNode, subdomain.hpp:30-44). */
-int cpddg_setup_subdomain_sets(const cpddg_setup* s, int j, int32_t* disjoint, int32_t* overlap,
+CPDDG_API int cpddg_setup_subdomain_sets(const cpddg_setup* s, int j, int32_t* disjoint, int32_t* overlap,
                                int32_t* final_layer, int32_t* ghosts, int32_t* bc_int,
                                double* bc_real);
 /** sizes[4] = n_overlap, n_bc, nnz, |scatter| (LocalOperator,
  *  transmission.hpp:47-70). */
-int cpddg_setup_local_sizes(const cpddg_setup* s, int j, int64_t* sizes);
-int cpddg_setup_local(const cpddg_setup* s, int j, int64_t* row_ptr, int32_t* col, double* val,
+CPDDG_API int cpddg_setup_local_sizes(const cpddg_setup* s, int j, int64_t* sizes);
+CPDDG_API int cpddg_setup_local(const cpddg_setup* s, int j, int64_t* row_ptr, int32_t* col, double* val,
                       int32_t* scatter_local, int32_t* scatter_global);
 
 /* ======================================================================
@@ -120,18 +126,18 @@ typedef struct {
     const double* cp;  /* (n_active + n_ghost) x dim closest points */
 } cpddg_band_desc;
 
-int cpddg_op_create(const cpddg_band_desc* band, cpddg_op** out);
-int cpddg_op_create_from_setup(const cpddg_setup* s, cpddg_op** out);
+CPDDG_API int cpddg_op_create(const cpddg_band_desc* band, cpddg_op** out);
+CPDDG_API int cpddg_op_create_from_setup(const cpddg_setup* s, cpddg_op** out);
 /** y_dev = A x_dev (sizes n_active). */
-int cpddg_op_apply(cpddg_op* op, const double* x_dev, double* y_dev, void* stream);
+CPDDG_API int cpddg_op_apply(cpddg_op* op, const double* x_dev, double* y_dev, void* stream);
 /** r_dev = b_dev - A x_dev, and ||r||_2 into *rnorm (host, synchronises). */
-int cpddg_op_residual(cpddg_op* op, const double* b_dev, const double* x_dev, double* r_dev,
+CPDDG_API int cpddg_op_residual(cpddg_op* op, const double* b_dev, const double* x_dev, double* r_dev,
                       double* rnorm, void* stream);
-int cpddg_op_size(const cpddg_op* op);
+CPDDG_API int cpddg_op_size(const cpddg_op* op);
 /** Bytes one apply must move at minimum (SURVEY.md 8(d) B_op) and the bytes
  *  the kernels stream (index tables included). */
-int cpddg_op_bytes(const cpddg_op* op, int64_t* algorithmic, int64_t* streamed);
-int cpddg_op_destroy(cpddg_op* op);
+CPDDG_API int cpddg_op_bytes(const cpddg_op* op, int64_t* algorithmic, int64_t* streamed);
+CPDDG_API int cpddg_op_destroy(cpddg_op* op);
 
 /* ======================================================================
  * Device Schwarz preconditioner.  Replaces the factored LocalOperator
@@ -172,13 +178,13 @@ typedef struct {
     int apply_mode;             /* 0: envelope triangular solves (k_solve); 1: dense local inverses (small systems) */
 } cpddg_pc_stats;
 
-int cpddg_pc_create(int n_global, int n_sub, const cpddg_local_desc* locals,
+CPDDG_API int cpddg_pc_create(int n_global, int n_sub, const cpddg_local_desc* locals,
                     const cpddg_pc_options* opt, cpddg_pc** out);
-int cpddg_pc_create_from_setup(const cpddg_setup* s, const cpddg_pc_options* opt, cpddg_pc** out);
+CPDDG_API int cpddg_pc_create_from_setup(const cpddg_setup* s, const cpddg_pc_options* opt, cpddg_pc** out);
 /** z_dev = M r_dev (sizes n_global). */
-int cpddg_pc_apply(cpddg_pc* pc, const double* r_dev, double* z_dev, void* stream);
-int cpddg_pc_stats_get(const cpddg_pc* pc, cpddg_pc_stats* st);
-int cpddg_pc_destroy(cpddg_pc* pc);
+CPDDG_API int cpddg_pc_apply(cpddg_pc* pc, const double* r_dev, double* z_dev, void* stream);
+CPDDG_API int cpddg_pc_stats_get(const cpddg_pc* pc, cpddg_pc_stats* st);
+CPDDG_API int cpddg_pc_destroy(cpddg_pc* pc);
 
 /* ======================================================================
  * Solvers.  Replace stationary_solve and gmres_solve (solve.hpp:95-214);
@@ -210,10 +216,20 @@ typedef struct {
     int64_t op_launches;
 } cpddg_log;
 
-int cpddg_gmres(cpddg_op* op, cpddg_pc* pc, const double* b_dev, double* u_dev,
+CPDDG_API int cpddg_gmres(cpddg_op* op, cpddg_pc* pc, const double* b_dev, double* u_dev,
                 const cpddg_solve_params* prm, cpddg_log* log, void* stream);
-int cpddg_stationary(cpddg_op* op, cpddg_pc* pc, const double* b_dev, double* u_dev,
+CPDDG_API int cpddg_stationary(cpddg_op* op, cpddg_pc* pc, const double* b_dev, double* u_dev,
                      const cpddg_solve_params* prm, cpddg_log* log, void* stream);
+
+/* ----------------------------------------------------------------------
+ * Development / profiling entry points (not part of the reference boundary).
+ * -------------------------------------------------------------------- */
+/** One preconditioner pass: mode 0 full apply, 1 forward substitution only,
+ *  2 backward only, 3 factor probe (r, z per-row arrays in factor order). */
+CPDDG_API int cpddg_pc_apply_mode(cpddg_pc* pc, const double* r_dev, double* z_dev, int mode, void* stream);
+/** Per-block timing trace of CTA 0 from the last solve run with
+ *  CPDDG_SOLVE_DEBUG & 16 (1024 x 20 clock64 values). */
+CPDDG_API int cpddg_dev_trace(long long* out);
 
 #ifdef __cplusplus
 }

@@ -98,6 +98,9 @@ _SIGS = {
                               C.POINTER(cpddg_log), _vp]),
     "cpddg_stationary": (C.c_int, [_vp, _vp, _vp, _vp, C.POINTER(cpddg_solve_params),
                                    C.POINTER(cpddg_log), _vp]),
+    # development / profiling entry points (last section of include/cpddg.h)
+    "cpddg_pc_apply_mode": (C.c_int, [_vp, _vp, _vp, C.c_int, _vp]),
+    "cpddg_dev_trace": (C.c_int, [_vp]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)

@@ -1568,8 +1568,8 @@ int cpddg_pc_stats_get(const cpddg_pc* pc, cpddg_pc_stats* st) {
     });
 }
 
-/** Development hook: time one pass of the preconditioner (mode 1 forward,
- *  2 backward, 0 both).  Not part of include/cpddg.h. */
+/** Development hooks (include/cpddg.h, last section): the per-block trace and
+ *  one pass of the preconditioner (mode 1 forward, 2 backward, 0 both, 3 probe). */
 int cpddg_dev_trace(long long* out) {  // development: copy g_trace
     return guarded([&] { CPDDG_CUDA(cudaMemcpyFromSymbol(out, g_trace, sizeof(long long) * 1024 * 20)); });
 }
