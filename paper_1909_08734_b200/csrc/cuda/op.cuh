@@ -84,6 +84,12 @@ struct cpddg_pc {
     int bwd_prefetch = 1;  // backward L2 prefetch distance in blocks (0 = off)
     bool urows = true;     // backward layout: reversed U rows (true) or U columns (false)
     int shape = 1;         // solve block shape: 0 big (1 CTA/SM), 1 mid (2/SM), 2 small (4/SM)
+    // record solve (default with urows): per block [W | T^-1] records, rows
+    // compacted to their far parts (k_block_records, k_compact_rows)
+    bool blockinv = false;
+    std::int64_t rec_entries = 0, far_entries = 0;
+    cpddg::DevBuf<std::int64_t> rbase; // [n_sub] first record entry of each subdomain
+    cpddg::DevBuf<double> recL, recU;
     // small systems: dense local inverses (k_solve_dense), row-major in factor order
     bool dense = false, dense_probe = false;
     int dense_tiles = 0;

@@ -600,6 +600,7 @@ struct SolveShape {
 using ShapeBig = SolveShape<31, 1, 1>;    // n_sub <= #SMs: 992 threads, one CTA per SM
 using ShapeMid = SolveShape<16, 2, 2>;    // n_sub <= 2 #SMs: 512 threads, two per SM
 using ShapeSmall = SolveShape<8, 2, 4>;   // more subdomains: 256 threads, up to four per SM
+using ShapeRec = SolveShape<15, 1, 2>;    // record solve, n_sub > #SMs: one row per panel warp, 2 per SM
 constexpr int RB = ShapeMid::RB;  // the column-layout backward (upper_solve_cols) uses ShapeMid
 constexpr int TS = ShapeMid::TS;
 constexpr int kSolveThreads = ShapeMid::kThreads;
@@ -627,6 +628,17 @@ __device__ __noinline__ void prefetch_rows(const double* V, const int* f, const 
     const std::int64_t lo = ro[b];
     const int l = e - 1;
     const std::int64_t hi = ro[l] + (l + (l & 1)) - f[l];
+    if (hi > lo) prefetch_l2(V + lo, (hi - lo) * 8);
+}
+
+/** L2 prefetch of the far parts of rows [b, e) in the record layout: row i
+ *  occupies [ro_i, ro_i + lim_i - f_i), lim_i = max(f_i, (i / rb - 1) rb). */
+__device__ __noinline__ void prefetch_rows_far(const double* V, const int* f, const std::int64_t* ro, int b, int e,
+                                               int rb) {
+    if (b >= e) return;
+    const std::int64_t lo = ro[b];
+    const int l = e - 1;
+    const std::int64_t hi = ro[l] + max(0, (l / rb - 1) * rb - f[l]);
     if (hi > lo) prefetch_l2(V + lo, (hi - lo) * 8);
 }
 
@@ -744,6 +756,195 @@ __device__ __forceinline__ void lower_solve(int n, const int* __restrict__ f, co
     }
 }
 
+/** Record lower solve y <- T^-1 y (T unit lower, or lower with its pivots
+ *  folded into the records) on the far parts of T's rows: row i keeps
+ *  columns [f_i, (i / RB - 1) RB) at V + ro_i, the rest of the row is in the
+ *  block records [W | T_kk^-1] (k_block_records).  Step k: warp 0 forms
+ *  x_k = T_kk^-1 (y_k - part_k) - W_k x_{k-1} (no dependent chain); panel
+ *  warp w owns rows RPW (w-1) .. of every block and computes block k+1's
+ *  far-part dots.  The far part of a row does not depend on x, so the first
+ *  512 columns of each warp's first row of block k+2 are loaded at the end
+ *  of step k and held in registers across the barrier: a step waits on one
+ *  load round trip (the warp's other rows), not two.  Row tables (f, ro) go
+ *  through a shared ring three blocks ahead, records by cp.async a step
+ *  ahead; one barrier per block. */
+template <class SH>
+__device__ __forceinline__ void lower_solve_rec(int n, const int* __restrict__ f, const std::int64_t* __restrict__ ro,
+                                                const double* __restrict__ V, const double* __restrict__ rec,
+                                                double* y, double (*part)[SH::RB + 2], double (*tri)[SH::RB][SH::TS],
+                                                int (*tf)[SH::RB], long long (*tro)[SH::RB], int dbg) {
+    constexpr int RB = SH::RB, RPW = SH::kRows;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, ptid = threadIdx.x - 32;
+    const int nblk = (n + RB - 1) / RB;
+    const int rr0 = RPW * (warp - 1);  // this panel warp's first row in a block
+    const double2* y2 = reinterpret_cast<const double2*>(y);
+    // table loads are issued at a step's start and stored at its end (a store
+    // right after the load would stall the loading warp for a round trip)
+    auto table_load = [&](int B, int& fv, long long& rv) {
+        fv = 0;
+        rv = 0;
+        if (B < nblk && ptid >= 0 && ptid < RB && B * RB + ptid < n) {
+            fv = __ldg(f + B * RB + ptid);
+            rv = __ldg(ro + B * RB + ptid);
+        }
+    };
+    auto table_store = [&](int B, int fv, long long rv) {
+        if (B < nblk && ptid >= 0 && ptid < RB) {
+            tf[B & 3][ptid] = fv;
+            tro[B & 3][ptid] = rv;
+        }
+    };
+    auto load_table = [&](int B) {
+        int fv;
+        long long rv;
+        table_load(B, fv, rv);
+        table_store(B, fv, rv);
+    };
+    auto load_rec = [&](int B, int buf) {
+        const double* src = rec + static_cast<std::int64_t>(B) * RB * 2 * RB;
+        for (int e = ptid; e < RB * 2 * RB; e += blockDim.x - 32) {
+            const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(&tri[buf][e / (2 * RB)][e % (2 * RB)]));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src + e) : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    double2 pre[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) pre[u] = make_double2(0.0, 0.0);
+    // first 512 columns of row rr0 of block B (far part [f, (B - 1) RB))
+    auto issue_pre = [&](int B) {
+        const int i = B * RB + rr0, lim = (B - 1) * RB;
+        const bool ok = B < nblk && i < n;
+        const int fi = ok ? tf[B & 3][rr0] : 0;
+        const double2* L2 = reinterpret_cast<const double2*>(V + (ok ? tro[B & 3][rr0] : 0));
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int c = fi + 2 * lane + 64 * u;
+            pre[u] = (ok && c < lim) ? ld_stream(L2 + lane + 32 * u) : make_double2(0.0, 0.0);
+        }
+    };
+    // dot of y with the columns [c, lim) of a row held as a[] (c = fi + 2 lane + 64 u + base)
+    auto dot8 = [&](const double2* a, int cb, int lim, double& s0, double& s1, double& s2, double& s3) {
+#pragma unroll
+        for (int u = 0; u < 8; u += 2) {
+            const int c = cb + 2 * lane + 64 * u;
+            if (c < lim) {
+                const double2 yy = y2[c >> 1];
+                s0 = fma(a[u].x, yy.x, s0);
+                s1 = fma(a[u].y, yy.y, s1);
+            }
+            if (c + 64 < lim) {
+                const double2 yy = y2[(c + 64) >> 1];
+                s2 = fma(a[u + 1].x, yy.x, s2);
+                s3 = fma(a[u + 1].y, yy.y, s3);
+            }
+        }
+    };
+    // the rest of a row from column cb on, loaded in this step
+    auto stream_row = [&](const double2* L2, int fi, int cb, int lim, double& s0, double& s1, double& s2,
+                          double& s3) {
+        for (int base = cb; base < lim; base += 512) {
+            double2 a[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int c = base + 2 * lane + 64 * u;
+                a[u] = c < lim ? ld_stream(L2 + ((c - fi) >> 1)) : make_double2(0.0, 0.0);
+            }
+            dot8(a, base, lim, s0, s1, s2, s3);
+        }
+    };
+    auto panel = [&](int B, int buf, bool tr) {
+        const bool tw = tr && lane == 0 && warp == 1;
+        const int b0 = B * RB, lim = b0 - RB;
+        if (!(dbg & 2)) load_rec(B, buf);  // dbg & 2: no records (timing experiments)
+        double sr[RPW];
+        {
+            const int fi = tf[B & 3][rr0];
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+            dot8(pre, fi, lim, s0, s1, s2, s3);
+            if (fi + 512 < lim)
+                stream_row(reinterpret_cast<const double2*>(V + tro[B & 3][rr0]), fi, fi + 512, lim, s0, s1, s2, s3);
+            sr[0] = (s0 + s1) + (s2 + s3);
+        }
+        if (tw) g_trace[B - 1][2] = clock64();
+#pragma unroll
+        for (int q = 1; q < RPW; ++q) {
+            const int fi = tf[B & 3][rr0 + q];
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+            stream_row(reinterpret_cast<const double2*>(V + tro[B & 3][rr0 + q]), fi, fi, lim, s0, s1, s2, s3);
+            sr[q] = (s0 + s1) + (s2 + s3);
+        }
+        if (tw) g_trace[B - 1][3] = clock64();
+        issue_pre(B + 1);  // in flight across the barrier
+        if (tw) g_trace[B - 1][4] = clock64();
+#pragma unroll
+        for (int q = 0; q < RPW; ++q) {
+            const double s = warp_sum(sr[q]);
+            if (lane == 0) part[buf][rr0 + q] = s;
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        if (tw) g_trace[B - 1][5] = clock64();
+        if (tr && lane == 0) g_trace[B - 1][6 + warp] = clock64();
+    };
+    // L2 bulk prefetch of block B's far rows (tables from the shared ring) and record
+    auto prefetch_block = [&](int B) {
+        if (B < nblk) {
+            const int l = min(RB, n - B * RB) - 1;
+            const long long lo = tro[B & 3][0];
+            const long long hi = tro[B & 3][l] + max(0, (B - 1) * RB - tf[B & 3][l]);
+            if (hi > lo) prefetch_l2(V + lo, (hi - lo) * 8);
+            prefetch_l2(rec + static_cast<std::int64_t>(B) * RB * 2 * RB, 8LL * RB * 2 * RB);
+        }
+    };
+    load_table(0);
+    load_table(1);
+    load_table(2);
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int q = 0; q < 2; ++q) prefetch_block(q);
+    if (warp > 0) panel(0, 0, false);  // block 0: empty far parts, record 0, pre for block 1
+    __syncthreads();
+    for (int k = 0; k < nblk; ++k) {
+        const int cur = k & 1;
+        const int r0 = k * RB;
+        const bool tr = (dbg & 16) && blockIdx.x == (dbg >> 16) && k < 1024;
+        if (tr && threadIdx.x == 0) g_trace[k][0] = clock64();
+        // L2 bulk prefetch two blocks ahead (tables of block k + 2 are in the
+        // ring since step k - 1); dbg & 4: off
+        if (!(dbg & 4) && threadIdx.x == 0) prefetch_block(k + 2);
+        if (warp == 0 && !(dbg & 1)) {  // dbg & 1: warp 0 idle (timing experiments)
+            const int i = r0 + lane;
+            const bool live = lane < RB && i < n;
+            const double t = live ? y[i] - part[cur][lane] : 0.0;
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+            const double* trow = tri[cur][lane < RB ? lane : 0];
+#pragma unroll
+            for (int c = 0; c < RB; c += 2) {
+                const double t0 = __shfl_sync(0xffffffffu, t, c);
+                const double t1 = __shfl_sync(0xffffffffu, t, c + 1);
+                a2 = fma(trow[RB + c], t0, a2);
+                a3 = fma(trow[RB + c + 1], t1, a3);
+            }
+            if (r0 >= RB) {
+#pragma unroll
+                for (int c = 0; c < RB; c += 2) {
+                    a0 = fma(trow[c], y[r0 - RB + c], a0);
+                    a1 = fma(trow[c + 1], y[r0 - RB + c + 1], a1);
+                }
+            }
+            if (live) y[i] = (a2 + a3) - (a0 + a1);
+            if (tr && lane == 0) g_trace[k][1] = clock64();
+        } else if (warp > 0) {
+            int fv;
+            long long rv;
+            table_load(k + 3, fv, rv);
+            if (k + 1 < nblk) panel(k + 1, cur ^ 1, tr);
+            table_store(k + 3, fv, rv);
+        }
+        __syncthreads();
+    }
+}
+
 /** Re-lay U (column profile storage from the factorisation) as reversed
  *  rows for a row-oriented backward pass: reversed row i' = n-1-i holds
  *  U(i, j), j in (i, rlast_i], at reversed column j' = n-1-j over
@@ -784,6 +985,154 @@ __global__ void __launch_bounds__(256) k_reverse_u(const int* __restrict__ order
             }
             out[jp] = v;
         }
+    }
+}
+
+/** Block records of the blocked lower solve (T unit lower, or lower with
+ *  reciprocal pivots d), for blocks of RB rows.  Block k (rows r0 = k RB ..)
+ *  satisfies T_kk x_k = s_k - T_k,k-1 x_{k-1}, s_k = y_k - (row dots over
+ *  the columns before block k-1), so with the block's triangle inverted
+ *
+ *      x_k = T_kk^-1 s_k - W_k x_{k-1},   W_k = T_kk^-1 T_k,k-1,
+ *
+ *  a dense RB x 2RB matrix-vector product instead of RB dependent
+ *  substitution steps.  Record k = [W_k | T_kk^-1] row-major (RB x 2RB,
+ *  zero-padded past the last row; W_0 = 0).  One warp per block: lane e
+ *  solves T_kk x = e_e (the reference substitution order, column by column)
+ *  into X[.][e]; then W = X P with P the block's previous-block columns. */
+template <int RB>
+__global__ void __launch_bounds__(64) k_block_records(const int* __restrict__ n_rows,
+                                                       const std::int64_t* __restrict__ vbase,
+                                                       const std::int64_t* __restrict__ ebase,
+                                                       const int* __restrict__ f_all,
+                                                       const std::int64_t* __restrict__ ro_all,
+                                                       const double* __restrict__ V_all,
+                                                       const double* __restrict__ d_all,
+                                                       const std::int64_t* __restrict__ rbase,
+                                                       double* __restrict__ rec_all) {
+    __shared__ double X[2][RB][33], P[2][RB][33];
+    const int j = blockIdx.x;
+    const int n = n_rows[j];
+    const std::int64_t vb = vbase[j];
+    const int* f = f_all + vb;
+    const std::int64_t* ro = ro_all + vb;
+    const double* V = V_all + ebase[j];
+    const double* d = d_all ? d_all + vb : nullptr;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nblk = (n + RB - 1) / RB;
+    for (int k = blockIdx.y * 2 + warp; k < nblk; k += 2 * gridDim.y) {
+        const int r0 = k * RB, rb = min(RB, n - r0);
+        double* rec = rec_all + rbase[j] + static_cast<std::int64_t>(k) * RB * 2 * RB;
+        for (int i = 0; i < RB; ++i) {
+            double s = 0.0;
+            if (i < rb) {
+                const int gi = r0 + i;
+                const double* Ti = V + ro[gi] - f[gi];
+                s = lane == i ? 1.0 : 0.0;
+                for (int c = max(0, f[gi] - r0); c < i; ++c) s = fma(-Ti[r0 + c], X[warp][c][lane], s);
+                if (d) s *= d[gi];
+                // previous-block columns of this row
+                const int pc = r0 - RB + lane;
+                P[warp][i][lane] = (k > 0 && lane < RB && pc >= f[gi]) ? Ti[pc] : 0.0;
+            } else {
+                P[warp][i][lane] = 0.0;
+            }
+            X[warp][i][lane] = s;
+            __syncwarp();
+        }
+        for (int i = 0; i < RB; ++i) {
+            if (lane < RB) {
+                double w = 0.0;
+                for (int m = 0; m <= i && m < rb; ++m) w = fma(X[warp][i][m], P[warp][m][lane], w);
+                rec[i * 2 * RB + lane] = w;
+                rec[i * 2 * RB + RB + lane] = X[warp][i][lane];
+            }
+        }
+        __syncwarp();
+    }
+}
+
+/** Block records of the column-oriented backward solve U x = y (blocks of
+ *  RB rows from the last): block K satisfies U_KK x_K = y_K - U_K,K+1 x_{K+1}
+ *  - (updates of blocks > K + 1), so record K = [W_K | U_KK^-1] with
+ *  W_K = U_KK^-1 U_K,K+1 (zero for the last block).  U column c holds rows
+ *  [f_c, c) at V + ro_c; d = reciprocal pivots.  One warp per block: lane e
+ *  solves U_KK x = e_e by backward substitution into X[.][e]. */
+template <int RB>
+__global__ void __launch_bounds__(64) k_block_records_upper(const int* __restrict__ n_rows,
+                                                            const std::int64_t* __restrict__ vbase,
+                                                            const std::int64_t* __restrict__ ebase,
+                                                            const int* __restrict__ f_all,
+                                                            const std::int64_t* __restrict__ ro_all,
+                                                            const double* __restrict__ V_all,
+                                                            const double* __restrict__ d_all,
+                                                            const std::int64_t* __restrict__ rbase,
+                                                            double* __restrict__ rec_all) {
+    __shared__ double X[2][RB][33], P[2][RB][33];
+    const int j = blockIdx.x;
+    const int n = n_rows[j];
+    const std::int64_t vb = vbase[j];
+    const int* f = f_all + vb;
+    const std::int64_t* ro = ro_all + vb;
+    const double* V = V_all + ebase[j];
+    const double* d = d_all + vb;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nblk = (n + RB - 1) / RB;
+    auto U = [&](int r, int c) { return r >= f[c] ? V[ro[c] + r - f[c]] : 0.0; };
+    for (int k = blockIdx.y * 2 + warp; k < nblk; k += 2 * gridDim.y) {
+        const int r0 = k * RB, rb = min(RB, n - r0);
+        double* rec = rec_all + rbase[j] + static_cast<std::int64_t>(k) * RB * 2 * RB;
+        for (int i = RB - 1; i >= 0; --i) {
+            double s = 0.0;
+            if (i < rb) {
+                const int gi = r0 + i;
+                s = lane == i ? 1.0 : 0.0;
+                for (int c = rb - 1; c > i; --c) s = fma(-U(gi, r0 + c), X[warp][c][lane], s);
+                s *= d[gi];
+                const int nc = r0 + RB + lane;  // next block's columns
+                P[warp][i][lane] = (lane < RB && nc < n) ? U(gi, nc) : 0.0;
+            } else {
+                P[warp][i][lane] = 0.0;
+            }
+            X[warp][i][lane] = s;
+            __syncwarp();
+        }
+        for (int i = 0; i < RB; ++i) {
+            if (lane < RB) {
+                double w = 0.0;
+                for (int m = i; m < rb; ++m) w = fma(X[warp][i][m], P[warp][m][lane], w);
+                rec[i * 2 * RB + lane] = w;
+                rec[i * 2 * RB + RB + lane] = X[warp][i][lane];
+            }
+        }
+        __syncwarp();
+    }
+}
+
+/** Far part of each row for the record solve: row i keeps columns
+ *  [f_i, lim_i), lim_i = max(f_i, (i / RB - 1) RB) -- everything left of the
+ *  previous block (the rest is in the block records).  lim_i and f_i are
+ *  even, so rows stay 16-byte aligned.  One warp per row. */
+template <int RB>
+__global__ void __launch_bounds__(256) k_compact_rows(const int* __restrict__ n_rows,
+                                                      const std::int64_t* __restrict__ vbase,
+                                                      const std::int64_t* __restrict__ ebase,
+                                                      const int* __restrict__ f_all,
+                                                      const std::int64_t* __restrict__ ro_all,
+                                                      const double* __restrict__ V_all,
+                                                      const std::int64_t* __restrict__ cbase,
+                                                      const std::int64_t* __restrict__ roc_all,
+                                                      double* __restrict__ Vc_all) {
+    const int j = blockIdx.x;
+    const int n = n_rows[j];
+    const std::int64_t vb = vbase[j];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = warp; i < n; i += 8) {
+        const int fi = f_all[vb + i];
+        const int lim = max(fi, (i / RB - 1) * RB);
+        const double* src = V_all + ebase[j] + ro_all[vb + i] - fi;
+        double* dst = Vc_all + cbase[j] + roc_all[vb + i] - fi;
+        for (int c = fi + lane; c < lim; c += 32) dst[c] = src[c];
     }
 }
 
@@ -945,11 +1294,151 @@ __device__ __forceinline__ void upper_solve_cols(int n, const int* __restrict__ 
     }
 }
 
+/** Record backward solve on U's column envelope (far parts only: column c
+ *  keeps rows [f_c, (c / RB - 1) RB), the rest is in the block records).
+ *  Step K: warp 0 forms x_K = U_KK^-1 y_K - W_K x_{K+1} from the record in
+ *  the stash; the panel warps apply block K+1's columns to every row above
+ *  block K -- lane = (row pair, group of 8 columns), 16-byte loads down the
+ *  columns, the four groups of a pair combined by a fixed butterfly (results
+ *  are bitwise reproducible) -- and bring in block K-1's record (cp.async)
+ *  and block K's column tables (shared ring of two).  Streams each stored
+ *  entry of U exactly once; one barrier per block. */
+template <class SH>
+__device__ __forceinline__ void upper_solve_rec(int n, const int* __restrict__ f, const std::int64_t* __restrict__ ro,
+                                                const double* __restrict__ V, const double* __restrict__ rec,
+                                                double* y, double (*tri)[SH::RB][SH::TS], int (*cf)[SH::RB],
+                                                long long (*cro)[SH::RB]) {
+    constexpr int RB = SH::RB;
+    constexpr int kPanelWarps = SH::kWarps - 1;
+    constexpr int NG = (RB + 7) / 8;  // groups of eight columns per block
+    constexpr int PPW = 32 / NG;      // row pairs per warp pass
+    static_assert(NG == 2 || NG == 4, "two or four groups of eight columns cover a block");
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ptid = threadIdx.x - 32;
+    const int nblk = (n + RB - 1) / RB;
+    auto load_rec = [&](int K, int buf) {
+        const double* src = rec + static_cast<std::int64_t>(K) * RB * 2 * RB;
+        for (int e = ptid; e < RB * 2 * RB; e += blockDim.x - 32) {
+            const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(&tri[buf][e / (2 * RB)][e % (2 * RB)]));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src + e) : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    auto load_table = [&](int K, int slot) {
+        if (K >= 0 && ptid < RB) {
+            const int c = K * RB + ptid;
+            cf[slot][ptid] = c < n ? __ldg(f + c) : INT_MAX;
+            cro[slot][ptid] = c < n ? __ldg(ro + c) : 0;
+        }
+    };
+    // columns of block K: contiguous far parts [ro_{K RB}, end of the last
+    // column), from the shared table of block K
+    auto prefetch_block = [&](int K, int slot) {
+        if (K >= 1) {
+            const int l = min(RB, n - K * RB) - 1;
+            const long long lo = cro[slot][0];
+            const long long hi = cro[slot][l] + max(0, (K - 1) * RB - cf[slot][l]);
+            if (hi > lo) prefetch_l2(V + lo, (hi - lo) * 8);
+        }
+    };
+    if (warp > 0) {
+        load_rec(nblk - 1, (nblk - 1) & 1);
+        load_table(nblk - 1, (nblk - 1) & 1);
+        asm volatile("cp.async.wait_all;" ::: "memory");
+    }
+    __syncthreads();
+    if (ptid == 0) prefetch_block(nblk - 1, (nblk - 1) & 1);
+    for (int K = nblk - 1; K >= 0; --K) {
+        const int cur = K & 1;
+        const int r0 = K * RB;
+        if (warp == 0) {
+            const int i = r0 + lane;
+            const bool live = lane < RB && i < n;
+            const double t = live ? y[i] : 0.0;
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+            const double* trow = tri[cur][lane < RB ? lane : 0];
+#pragma unroll
+            for (int c = 0; c < RB; c += 2) {
+                const double t0 = __shfl_sync(0xffffffffu, t, c);
+                const double t1 = __shfl_sync(0xffffffffu, t, c + 1);
+                a2 = fma(trow[RB + c], t0, a2);
+                a3 = fma(trow[RB + c + 1], t1, a3);
+            }
+            if (K + 1 < nblk) {
+                const int nb = min(RB, n - (r0 + RB));
+                for (int c = 0; c < nb; ++c) (c & 1 ? a1 : a0) = fma(trow[c], y[r0 + RB + c], c & 1 ? a1 : a0);
+            }
+            if (live) y[i] = (a2 + a3) - (a0 + a1);
+        } else {
+            if (K >= 1) load_rec(K - 1, cur ^ 1);
+            if (ptid == 0 && K >= 2)
+                prefetch_l2(rec + static_cast<std::int64_t>(K - 2) * RB * 2 * RB, 8LL * RB * 2 * RB);
+            // block K's column table, for step K - 1 (slot cur was last read at
+            // step K + 1); loaded now, stored after this step's loads
+            int tfv = INT_MAX;
+            long long trv = 0;
+            if (K >= 0 && ptid < RB && K * RB + ptid < n) {
+                tfv = __ldg(f + K * RB + ptid);
+                trv = __ldg(ro + K * RB + ptid);
+            }
+            if (K + 1 < nblk) {
+                const int slot = cur ^ 1;
+                const int c0 = r0 + RB;
+                const int g = lane % NG, pp = lane / NG;
+                int jmin = r0;
+                for (int c = 0; c < RB; ++c) jmin = min(jmin, cf[slot][c]);
+                double xc[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int c = g * 8 + u;
+                    xc[u] = c < RB && c0 + c < n ? y[c0 + c] : 0.0;
+                }
+                for (int base = (jmin & ~1) + 2 * PPW * (warp - 1); base < r0; base += 2 * PPW * kPanelWarps) {
+                    const int r = base + 2 * pp;
+                    double2 a[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int c = g * 8 + u;
+                        const int fc = c < RB ? cf[slot][c] : INT_MAX;
+                        a[u] = (r < r0 && r >= fc)
+                                   ? ld_stream(reinterpret_cast<const double2*>(V + cro[slot][c] + (r - fc)))
+                                   : make_double2(0.0, 0.0);
+                    }
+                    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        s0 = fma(a[u].x, xc[u], s0);
+                        s1 = fma(a[u].y, xc[u], s1);
+                    }
+#pragma unroll
+                    for (int m = 1; m < NG; m <<= 1) {
+                        s0 += __shfl_xor_sync(0xffffffffu, s0, m);
+                        s1 += __shfl_xor_sync(0xffffffffu, s1, m);
+                    }
+                    if (g == 0 && r < r0) {
+                        y[r] -= s0;
+                        y[r + 1] -= s1;
+                    }
+                }
+            }
+            if (ptid < RB) {
+                cf[cur][ptid] = tfv;
+                cro[cur][ptid] = trv;
+            }
+            asm volatile("cp.async.wait_all;" ::: "memory");
+        }
+        __syncthreads();
+        // block K's columns are applied at step K - 1: bulk-prefetch them now
+        if (ptid == 0 && K >= 1) prefetch_block(K, cur);
+    }
+}
+
 // MODE 0: full apply; 1: forward only; 2: backward only (profiling);
 // 3: factor probe -- r / z are per-row arrays in factor order (vbase
 //    indexing) instead of global vectors, no gather / scatter.
 // UROWS: backward on reversed U rows (k_reverse_u) instead of U columns.
-template <int MODE, bool UROWS, class SH>
+// INV: record solve (k_block_records) on the compacted far rows.
+template <int MODE, bool UROWS, class SH, bool INV>
 __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) k_solve(const int* __restrict__ order,
                                                             const int* __restrict__ n_rows,
                                                             const std::int64_t* __restrict__ vbase,
@@ -969,7 +1458,10 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) k_solve(const in
                                                             const std::int64_t* __restrict__ ubase,
                                                             const int* __restrict__ ufirst_all,
                                                             const std::int64_t* __restrict__ uroff_all,
-                                                            const double* __restrict__ drev_all, int dbg) {
+                                                            const double* __restrict__ drev_all, int dbg,
+                                                            const std::int64_t* __restrict__ rbase,
+                                                            const double* __restrict__ recL_all,
+                                                            const double* __restrict__ recU_all) {
     const int j = order[blockIdx.x];
     const int n = n_rows[j];
     const std::int64_t vb = vbase[j];
@@ -977,6 +1469,17 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) k_solve(const in
     __shared__ double part[2][SH::RB + 2];
     __shared__ double tri[2][SH::RB][SH::TS];
     const int tid = threadIdx.x;
+    // development (CPDDG_SOLVE_DEBUG & 32): per-CTA start / end (globaltimer ns), SM, subdomain
+    const bool ctr = (dbg & 32) && tid == 0 && blockIdx.x < 1024;
+    if (ctr) {
+        long long t0;
+        unsigned sm;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        g_trace[blockIdx.x][0] = t0;
+        g_trace[blockIdx.x][2] = sm;
+        g_trace[blockIdx.x][3] = j;
+    }
 
     for (int p = tid; p < n; p += blockDim.x) {
         if (MODE == 3) {
@@ -988,7 +1491,15 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) k_solve(const in
     }
     __syncthreads();
     // forward: L y = b (unit lower)
-    if (MODE != 2) lower_solve<SH>(n, first_all + vb, roff_all + vb, L_all + ebase[j], nullptr, y, part, tri, dbg);
+    __shared__ int tf[4][SH::RB];
+    __shared__ long long tro[4][SH::RB];
+    if (MODE != 2) {
+        if constexpr (INV)
+            lower_solve_rec<SH>(n, first_all + vb, roff_all + vb, L_all + ebase[j], recL_all + rbase[j], y, part, tri,
+                                tf, tro, dbg);
+        else
+            lower_solve<SH>(n, first_all + vb, roff_all + vb, L_all + ebase[j], nullptr, y, part, tri, dbg);
+    }
     if constexpr (UROWS) {
         // backward: U x = y as a forward solve on the reversed system
         for (int p = tid; p < n / 2; p += blockDim.x) {
@@ -998,7 +1509,13 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) k_solve(const in
         }
         __syncthreads();
         if (MODE != 1)
-            lower_solve<SH>(n, ufirst_all + vb, uroff_all + vb, U_all + ubase[j], drev_all + vb, y, part, tri, dbg);
+        {
+            if constexpr (INV)
+                lower_solve_rec<SH>(n, ufirst_all + vb, uroff_all + vb, U_all + ubase[j], recU_all + rbase[j], y, part,
+                                    tri, tf, tro, dbg);
+            else
+                lower_solve<SH>(n, ufirst_all + vb, uroff_all + vb, U_all + ubase[j], drev_all + vb, y, part, tri, dbg);
+        }
         for (int p = tid; p < n; p += blockDim.x) {
             if (MODE == 3) {
                 z[vb + p] = y[n - 1 - p];
@@ -1010,13 +1527,28 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) k_solve(const in
                 z[s] = accumulate ? z[s] + v : v;
             }
         }
+        if (ctr) {
+            long long t1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            g_trace[blockIdx.x][1] = t1;
+        }
     } else {
-        static_assert(std::is_same_v<SH, ShapeMid>, "the column-layout backward is built for ShapeMid");
-        // backward: U x = y, column-oriented on the factorisation's U layout
-        __shared__ int cf[4][RB];
-        __shared__ long long cro[4][RB];
-        if (MODE != 1)
-            upper_solve_cols(n, firstU_all + vb, roffU_all + vb, U_all + ebaseU[j], diag_all + vb, y, tri, cf, cro, pf);
+        if constexpr (INV) {
+            // backward: U x = y on the far parts of U's columns + block records
+            __shared__ int cf[2][SH::RB];
+            __shared__ long long cro[2][SH::RB];
+            if (MODE != 1)
+                upper_solve_rec<SH>(n, firstU_all + vb, roffU_all + vb, U_all + ebaseU[j], recU_all + rbase[j], y, tri,
+                                    cf, cro);
+        } else {
+            static_assert(INV || std::is_same_v<SH, ShapeMid>, "the column-layout backward is built for ShapeMid");
+            // backward: U x = y, column-oriented on the factorisation's U layout
+            __shared__ int cf[4][RB];
+            __shared__ long long cro[4][RB];
+            if (MODE != 1)
+                upper_solve_cols(n, firstU_all + vb, roffU_all + vb, U_all + ebaseU[j], diag_all + vb, y, tri, cf, cro,
+                                 pf);
+        }
         for (int p = tid; p < n; p += blockDim.x) {
             if (MODE == 3) {
                 z[vb + p] = y[p];
@@ -1024,6 +1556,11 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) k_solve(const in
             }
             const int s = __ldg(sidx_all + vb + p);
             if (s >= 0) z[s] = accumulate ? z[s] + y[p] : y[p];
+        }
+        if (ctr) {
+            long long t1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            g_trace[blockIdx.x][1] = t1;
         }
     }
 }
@@ -1120,22 +1657,24 @@ void append(std::vector<T>& dst, const std::vector<T>& src) {
 
 }  // namespace
 
-template <bool UROWS, class SH>
+template <bool UROWS, class SH, bool INV>
 static void launch_solve(const cpddg_pc* pc, int grid, const double* r, double* z, bool accumulate, int mode,
                          int dbg, cudaStream_t st) {
-    auto kern = mode == 1 ? k_solve<1, UROWS, SH> : mode == 2 ? k_solve<2, UROWS, SH>
-              : mode == 3 ? k_solve<3, UROWS, SH> : k_solve<0, UROWS, SH>;
+    auto kern = mode == 1 ? k_solve<1, UROWS, SH, INV> : mode == 2 ? k_solve<2, UROWS, SH, INV>
+              : mode == 3 ? k_solve<3, UROWS, SH, INV> : k_solve<0, UROWS, SH, INV>;
     kern<<<grid, SH::kThreads, pc->solve_smem, st>>>(
         pc->order.get(), pc->n_rows.get(), pc->vbase.get(), pc->ebase.get(), pc->first.get(), pc->roff.get(),
         pc->ebaseU.get(), pc->firstU.get(), pc->roffU.get(),
         pc->dinv.get(), pc->L.get(), pc->U.get(), pc->gidx.get(), pc->sidx.get(), r, z, accumulate ? 1 : 0,
-        pc->bwd_prefetch, pc->ubase.get(), pc->ufirst.get(), pc->uroff.get(), pc->drev.get(), dbg);
+        pc->bwd_prefetch, pc->ubase.get(), pc->ufirst.get(), pc->uroff.get(), pc->drev.get(), dbg,
+        pc->rbase.get(), pc->recL.get(), pc->recU.get());
     CPDDG_CUDA(cudaGetLastError());
 }
 
-template <bool UROWS, class SH>
+template <bool UROWS, class SH, bool INV>
 static void set_solve_smem(int bytes) {
-    for (auto kern : {k_solve<0, UROWS, SH>, k_solve<1, UROWS, SH>, k_solve<2, UROWS, SH>, k_solve<3, UROWS, SH>})
+    for (auto kern : {k_solve<0, UROWS, SH, INV>, k_solve<1, UROWS, SH, INV>, k_solve<2, UROWS, SH, INV>,
+                      k_solve<3, UROWS, SH, INV>})
         CPDDG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(bytes, 1)));
 }
 
@@ -1158,14 +1697,28 @@ void pc_apply_mode(const cpddg_pc* pc, const double* r, double* z, bool accumula
         CPDDG_CUDA(cudaGetLastError());
         return;
     }
-    if (!pc->urows)
-        launch_solve<false, ShapeMid>(pc, grid, r, z, accumulate, mode, dbg, st);
-    else if (pc->shape == 0)
-        launch_solve<true, ShapeBig>(pc, grid, r, z, accumulate, mode, dbg, st);
+    if (!pc->urows && pc->blockinv) {
+        if (pc->shape == 0)
+            launch_solve<false, ShapeBig, true>(pc, grid, r, z, accumulate, mode, dbg, st);
+        else if (pc->shape == 1)
+            launch_solve<false, ShapeMid, true>(pc, grid, r, z, accumulate, mode, dbg, st);
+        else
+            launch_solve<false, ShapeRec, true>(pc, grid, r, z, accumulate, mode, dbg, st);
+    } else if (!pc->urows)
+        launch_solve<false, ShapeMid, false>(pc, grid, r, z, accumulate, mode, dbg, st);
+    else if (pc->blockinv) {
+        if (pc->shape == 0)
+            launch_solve<true, ShapeBig, true>(pc, grid, r, z, accumulate, mode, dbg, st);
+        else if (pc->shape == 1)
+            launch_solve<true, ShapeMid, true>(pc, grid, r, z, accumulate, mode, dbg, st);
+        else
+            launch_solve<true, ShapeRec, true>(pc, grid, r, z, accumulate, mode, dbg, st);
+    } else if (pc->shape == 0)
+        launch_solve<true, ShapeBig, false>(pc, grid, r, z, accumulate, mode, dbg, st);
     else if (pc->shape == 1)
-        launch_solve<true, ShapeMid>(pc, grid, r, z, accumulate, mode, dbg, st);
+        launch_solve<true, ShapeMid, false>(pc, grid, r, z, accumulate, mode, dbg, st);
     else
-        launch_solve<true, ShapeSmall>(pc, grid, r, z, accumulate, mode, dbg, st);
+        launch_solve<true, ShapeSmall, false>(pc, grid, r, z, accumulate, mode, dbg, st);
 }
 
 void pc_apply(const cpddg_pc* pc, const double* r, double* z, bool accumulate, cudaStream_t st) {
@@ -1346,10 +1899,20 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
         if (st[static_cast<std::size_t>(j)]) throw DivergenceError("singular factorization of subdomain " + std::to_string(j));
 
     pc->u_entries = ebsU;
+    // record solve (default): U by columns; substitution-chain solve
+    // (CPDDG_BLOCKINV=0): reversed U rows.  CPDDG_BWD_LAYOUT=rows|cols overrides.
+    {
+        const char* e = std::getenv("CPDDG_BLOCKINV");
+        pc->blockinv = !(e && std::string(e) == "0");
+    }
+    pc->urows = !pc->blockinv;
     if (const char* e = std::getenv("CPDDG_BWD_LAYOUT")) pc->urows = std::string(e) != "cols";
+    std::vector<int> ufirst;
+    std::vector<std::int64_t> uroff, ubase;
     if (pc->urows) {
-        std::vector<int> ufirst(static_cast<std::size_t>(vb));
-        std::vector<std::int64_t> uroff(static_cast<std::size_t>(vb)), ubase(static_cast<std::size_t>(n_sub));
+        ufirst.assign(static_cast<std::size_t>(vb), 0);
+        uroff.assign(static_cast<std::size_t>(vb), 0);
+        ubase.assign(static_cast<std::size_t>(n_sub), 0);
         std::int64_t ub = 0;
         for (int j = 0; j < n_sub; ++j) {
             const int nj = n_rows[static_cast<std::size_t>(j)];
@@ -1383,18 +1946,125 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
     pc->solve_smem = static_cast<int>(sizeof(double)) * pc->max_rows;
     if (const char* e = std::getenv("CPDDG_BWD_PREFETCH")) pc->bwd_prefetch = std::atoi(e);
     if (pc->solve_smem > 200 * 1024) throw ConfigError("subdomain system too large for the shared-memory solve");
-    set_solve_smem<false, ShapeMid>(pc->solve_smem);
-    set_solve_smem<true, ShapeBig>(pc->solve_smem);
-    set_solve_smem<true, ShapeMid>(pc->solve_smem);
-    set_solve_smem<true, ShapeSmall>(pc->solve_smem);
+    set_solve_smem<false, ShapeMid, false>(pc->solve_smem);
+    set_solve_smem<true, ShapeBig, false>(pc->solve_smem);
+    set_solve_smem<true, ShapeMid, false>(pc->solve_smem);
+    set_solve_smem<true, ShapeSmall, false>(pc->solve_smem);
+    set_solve_smem<true, ShapeBig, true>(pc->solve_smem);
+    set_solve_smem<true, ShapeMid, true>(pc->solve_smem);
+    set_solve_smem<true, ShapeRec, true>(pc->solve_smem);
+    set_solve_smem<false, ShapeBig, true>(pc->solve_smem);
+    set_solve_smem<false, ShapeMid, true>(pc->solve_smem);
+    set_solve_smem<false, ShapeRec, true>(pc->solve_smem);
     // block shape: one CTA per subdomain, all resident in one wave
     {
         const int S = sm_count();
-        pc->shape = n_sub <= S ? 0 : 1;  // measured: two waves of ShapeMid beat one wave of ShapeSmall
+        // measured: two waves of ShapeMid beat one wave of ShapeSmall; the
+        // record solve uses ShapeRec (shape 3) when n_sub > #SMs
+        pc->shape = n_sub <= S ? 0 : pc->blockinv ? 3 : 1;
         if (const char* e = std::getenv("CPDDG_SOLVE_SHAPE")) {
             const std::string v(e);
-            pc->shape = v == "big" ? 0 : v == "mid" ? 1 : v == "small" ? 2 : pc->shape;
+            pc->shape = v == "big" ? 0 : v == "mid" ? 1 : v == "small" ? 2 : v == "rec" ? 3 : pc->shape;
         }
+    }
+    // record solve: block records from the full rows, then the rows compacted
+    // to their far parts (CPDDG_BLOCKINV=0 keeps the substitution-chain solve)
+    if (pc->blockinv) {
+        const int rb = pc->shape >= 2 ? ShapeRec::RB : ShapeMid::RB;
+        static_assert(ShapeBig::RB == ShapeMid::RB && ShapeSmall::RB == ShapeRec::RB,
+                      "records are built for RB = 30 or RB = 14");
+        std::vector<std::int64_t> rbase(static_cast<std::size_t>(n_sub));
+        std::int64_t rt = 0;
+        for (int j = 0; j < n_sub; ++j) {
+            rbase[static_cast<std::size_t>(j)] = rt;
+            rt += static_cast<std::int64_t>((n_rows[static_cast<std::size_t>(j)] + rb - 1) / rb) * rb * 2 * rb;
+        }
+        pc->rec_entries = 2 * rt;
+        pc->rbase.upload(rbase);
+        pc->recL.alloc(static_cast<std::size_t>(std::max<std::int64_t>(rt, 1)));
+        pc->recU.alloc(static_cast<std::size_t>(std::max<std::int64_t>(rt, 1)));
+        const dim3 rgrid(static_cast<unsigned>(n_sub), 16);
+        auto records = rb == 30 ? k_block_records<30> : k_block_records<ShapeSmall::RB>;
+        auto compact = rb == 30 ? k_compact_rows<30> : k_compact_rows<ShapeSmall::RB>;
+        records<<<rgrid, 64>>>(pc->n_rows.get(), pc->vbase.get(), pc->ebase.get(), pc->first.get(), pc->roff.get(),
+                               pc->L.get(), nullptr, pc->rbase.get(), pc->recL.get());
+        if (pc->urows)
+            records<<<rgrid, 64>>>(pc->n_rows.get(), pc->vbase.get(), pc->ubase.get(), pc->ufirst.get(),
+                                   pc->uroff.get(), pc->U.get(), pc->drev.get(), pc->rbase.get(), pc->recU.get());
+        else
+            (rb == 30 ? k_block_records_upper<30> : k_block_records_upper<ShapeSmall::RB>)<<<rgrid, 64>>>(
+                pc->n_rows.get(), pc->vbase.get(), pc->ebaseU.get(), pc->firstU.get(), pc->roffU.get(), pc->U.get(),
+                pc->dinv.get(), pc->rbase.get(), pc->recU.get());
+        CPDDG_CUDA(cudaGetLastError());
+        // far parts: row i keeps [f_i, max(f_i, (i / rb - 1) rb))
+        auto far_layout = [&](const std::vector<int>& f, std::vector<std::int64_t>& roc, std::vector<std::int64_t>& cb) {
+            roc.assign(static_cast<std::size_t>(vb), 0);
+            cb.assign(static_cast<std::size_t>(n_sub), 0);
+            std::int64_t tot = 0;
+            for (int j = 0; j < n_sub; ++j) {
+                cb[static_cast<std::size_t>(j)] = tot;
+                const std::int64_t v0 = vbase[static_cast<std::size_t>(j)];
+                std::int64_t off = 0;
+                for (int i = 0; i < n_rows[static_cast<std::size_t>(j)]; ++i) {
+                    const int fi = f[static_cast<std::size_t>(v0 + i)];
+                    roc[static_cast<std::size_t>(v0 + i)] = off;
+                    off += std::max(0, (i / rb - 1) * rb - fi);
+                }
+                tot += off;
+            }
+            return tot;
+        };
+        if (std::getenv("CPDDG_VERBOSE")) {
+            // layout study: U far entries by columns vs per-block rectangles
+            std::int64_t cols = 0, rect = 0, lrows = 0;
+            for (int j = 0; j < n_sub; ++j) {
+                const std::int64_t v0 = vbase[static_cast<std::size_t>(j)];
+                const int nj = n_rows[static_cast<std::size_t>(j)];
+                for (int K = 1; K * rb < nj; ++K) {
+                    int fmin = INT_MAX;
+                    for (int c = K * rb; c < std::min(nj, K * rb + rb); ++c) {
+                        const int fc = firstU[static_cast<std::size_t>(v0 + c)];
+                        fmin = std::min(fmin, fc);
+                        cols += std::max(0, (K - 1) * rb - fc);
+                        lrows += std::max(0, (K - 1) * rb - first[static_cast<std::size_t>(v0 + c)]);
+                    }
+                    rect += static_cast<std::int64_t>(rb) * std::max(0, (K - 1) * rb - fmin);
+                }
+            }
+            std::fprintf(stderr, "[cpddg] far entries: L rows %lld, U cols %lld, U block rectangles %lld\n",
+                         static_cast<long long>(lrows), static_cast<long long>(cols), static_cast<long long>(rect));
+        }
+        std::vector<std::int64_t> rocL, cbL, rocU, cbU;
+        const std::int64_t nL = far_layout(first, rocL, cbL), nU = far_layout(pc->urows ? ufirst : firstU, rocU, cbU);
+        DevBuf<std::int64_t> drocL, dcbL, drocU, dcbU;
+        drocL.upload(rocL);
+        dcbL.upload(cbL);
+        drocU.upload(rocU);
+        dcbU.upload(cbU);
+        DevBuf<double> Lc(static_cast<std::size_t>(std::max<std::int64_t>(nL, 1))),
+            Uc(static_cast<std::size_t>(std::max<std::int64_t>(nU, 1)));
+        compact<<<n_sub, 256>>>(pc->n_rows.get(), pc->vbase.get(), pc->ebase.get(), pc->first.get(), pc->roff.get(),
+                                pc->L.get(), dcbL.get(), drocL.get(), Lc.get());
+        if (pc->urows)
+            compact<<<n_sub, 256>>>(pc->n_rows.get(), pc->vbase.get(), pc->ubase.get(), pc->ufirst.get(),
+                                    pc->uroff.get(), pc->U.get(), dcbU.get(), drocU.get(), Uc.get());
+        else  // U columns: the same far-part rule, [f_c, (c / rb - 1) rb)
+            compact<<<n_sub, 256>>>(pc->n_rows.get(), pc->vbase.get(), pc->ebaseU.get(), pc->firstU.get(),
+                                    pc->roffU.get(), pc->U.get(), dcbU.get(), drocU.get(), Uc.get());
+        CPDDG_CUDA(cudaGetLastError());
+        CPDDG_CUDA(cudaDeviceSynchronize());
+        pc->L = std::move(Lc);
+        pc->U = std::move(Uc);
+        pc->roff = std::move(drocL);
+        pc->ebase = std::move(dcbL);
+        if (pc->urows) {
+            pc->uroff = std::move(drocU);
+            pc->ubase = std::move(dcbU);
+        } else {
+            pc->roffU = std::move(drocU);
+            pc->ebaseU = std::move(dcbU);
+        }
+        pc->far_entries = nL + nU;
     }
     // factor probe (cpddg_pc_options::check_residual): solve A_j z = A_j x_probe
     // on the device for every subdomain and check the residual on the host --
@@ -1497,7 +2167,10 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
     // bytes one apply streams: L, U, diag, first, roff per row, gather/scatter maps, r gathers, z writes
     // streamed per apply: L and reversed-U values, diagonal, and the per-row
     // tables (first + offset) of both passes
-    pc->factor_bytes = pc->dense ? 8 * pc->dense_entries : 8 * (ebs + pc->u_entries + vb) + 2 * 12 * vb;
+    if (pc->blockinv) pc->entries = pc->far_entries + pc->rec_entries;
+    pc->factor_bytes = pc->dense      ? 8 * pc->dense_entries
+                       : pc->blockinv ? 8 * (pc->far_entries + pc->rec_entries) + 2 * 12 * vb
+                                      : 8 * (ebs + pc->u_entries + vb) + 2 * 12 * vb;
     std::int64_t gathers = 0, scatters = 0;
     for (int g : gidx) gathers += g >= 0 ? 1 : 0;
     for (int s : sidx) scatters += s >= 0 ? 1 : 0;
