@@ -90,6 +90,13 @@ struct cpddg_pc {
     std::int64_t rec_entries = 0, far_entries = 0;
     cpddg::DevBuf<std::int64_t> rbase; // [n_sub] first record entry of each subdomain
     cpddg::DevBuf<double> recL, recU;
+    // persistent TMA-streamed solve (k_solve_tma): per-CTA subdomain lists,
+    // per-step items (32 B each) and row descriptors
+    bool tma = false;
+    int tma_grid = 0, tma_smem = 0;
+    cpddg::DevBuf<int> tma_cta_begin, tma_cta_subs, tma_desc;
+    cpddg::DevBuf<std::int64_t> tma_itbase;
+    cpddg::DevBuf<unsigned char> tma_items;
     // small systems: dense local inverses (k_solve_dense), row-major in factor order
     bool dense = false, dense_probe = false;
     int dense_tiles = 0;

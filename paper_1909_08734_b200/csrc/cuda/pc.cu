@@ -601,9 +601,18 @@ using ShapeBig = SolveShape<31, 1, 1>;    // n_sub <= #SMs: 992 threads, one CTA
 using ShapeMid = SolveShape<16, 2, 2>;    // n_sub <= 2 #SMs: 512 threads, two per SM
 using ShapeSmall = SolveShape<8, 2, 4>;   // more subdomains: 256 threads, up to four per SM
 using ShapeRec = SolveShape<15, 1, 2>;    // record solve, n_sub > #SMs: one row per panel warp, 2 per SM
+using ShapeRec8 = SolveShape<9, 1, 2>;    // record solve with the streamed path's RB = 8 (its fallback)
 constexpr int RB = ShapeMid::RB;  // the column-layout backward (upper_solve_cols) uses ShapeMid
 constexpr int TS = ShapeMid::TS;
 constexpr int kSolveThreads = ShapeMid::kThreads;
+
+/** Block record layout: RB rows of [W | T^-1 | 0], row stride 2 RB + 1 (the
+ *  stash's padded stride, so a record copies linearly into it); RB even
+ *  keeps records 16-byte aligned. */
+__host__ __device__ constexpr int rec_stride(int rb) { return 2 * rb + 1; }
+__host__ __device__ constexpr int rec_size(int rb) { return rb * (2 * rb + 1); }
+// distance between records: 128-byte aligned (whole lines for the bulk copies)
+__host__ __device__ constexpr int rec_pitch(int rb) { return (rec_size(rb) + 15) / 16 * 16; }
 
 // development timing trace (CPDDG_SOLVE_DEBUG & 16): per block of CTA 0,
 // [k][0] step start, [k][1] warp 0 done, [k][2 + w] panel warp w done
@@ -801,11 +810,10 @@ __device__ __forceinline__ void lower_solve_rec(int n, const int* __restrict__ f
         table_store(B, fv, rv);
     };
     auto load_rec = [&](int B, int buf) {
-        const double* src = rec + static_cast<std::int64_t>(B) * RB * 2 * RB;
-        for (int e = ptid; e < RB * 2 * RB; e += blockDim.x - 32) {
-            const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(&tri[buf][e / (2 * RB)][e % (2 * RB)]));
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src + e) : "memory");
-        }
+        const double* src = rec + static_cast<std::int64_t>(B) * rec_pitch(RB);
+        const unsigned base = static_cast<unsigned>(__cvta_generic_to_shared(&tri[buf][0][0]));
+        for (int e = 2 * ptid; e < rec_size(RB); e += 2 * (blockDim.x - 32))
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(base + 8 * e), "l"(src + e) : "memory");
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
     double2 pre[8];
@@ -893,7 +901,7 @@ __device__ __forceinline__ void lower_solve_rec(int n, const int* __restrict__ f
             const long long lo = tro[B & 3][0];
             const long long hi = tro[B & 3][l] + max(0, (B - 1) * RB - tf[B & 3][l]);
             if (hi > lo) prefetch_l2(V + lo, (hi - lo) * 8);
-            prefetch_l2(rec + static_cast<std::int64_t>(B) * RB * 2 * RB, 8LL * RB * 2 * RB);
+            prefetch_l2(rec + static_cast<std::int64_t>(B) * rec_pitch(RB), 8LL * rec_size(RB));
         }
     };
     load_table(0);
@@ -1022,7 +1030,7 @@ __global__ void __launch_bounds__(64) k_block_records(const int* __restrict__ n_
     const int nblk = (n + RB - 1) / RB;
     for (int k = blockIdx.y * 2 + warp; k < nblk; k += 2 * gridDim.y) {
         const int r0 = k * RB, rb = min(RB, n - r0);
-        double* rec = rec_all + rbase[j] + static_cast<std::int64_t>(k) * RB * 2 * RB;
+        double* rec = rec_all + rbase[j] + static_cast<std::int64_t>(k) * rec_pitch(RB);
         for (int i = 0; i < RB; ++i) {
             double s = 0.0;
             if (i < rb) {
@@ -1044,8 +1052,9 @@ __global__ void __launch_bounds__(64) k_block_records(const int* __restrict__ n_
             if (lane < RB) {
                 double w = 0.0;
                 for (int m = 0; m <= i && m < rb; ++m) w = fma(X[warp][i][m], P[warp][m][lane], w);
-                rec[i * 2 * RB + lane] = w;
-                rec[i * 2 * RB + RB + lane] = X[warp][i][lane];
+                rec[i * rec_stride(RB) + lane] = w;
+                rec[i * rec_stride(RB) + RB + lane] = X[warp][i][lane];
+                if (lane == 0) rec[i * rec_stride(RB) + 2 * RB] = 0.0;
             }
         }
         __syncwarp();
@@ -1081,7 +1090,7 @@ __global__ void __launch_bounds__(64) k_block_records_upper(const int* __restric
     auto U = [&](int r, int c) { return r >= f[c] ? V[ro[c] + r - f[c]] : 0.0; };
     for (int k = blockIdx.y * 2 + warp; k < nblk; k += 2 * gridDim.y) {
         const int r0 = k * RB, rb = min(RB, n - r0);
-        double* rec = rec_all + rbase[j] + static_cast<std::int64_t>(k) * RB * 2 * RB;
+        double* rec = rec_all + rbase[j] + static_cast<std::int64_t>(k) * rec_pitch(RB);
         for (int i = RB - 1; i >= 0; --i) {
             double s = 0.0;
             if (i < rb) {
@@ -1101,8 +1110,9 @@ __global__ void __launch_bounds__(64) k_block_records_upper(const int* __restric
             if (lane < RB) {
                 double w = 0.0;
                 for (int m = i; m < rb; ++m) w = fma(X[warp][i][m], P[warp][m][lane], w);
-                rec[i * 2 * RB + lane] = w;
-                rec[i * 2 * RB + RB + lane] = X[warp][i][lane];
+                rec[i * rec_stride(RB) + lane] = w;
+                rec[i * rec_stride(RB) + RB + lane] = X[warp][i][lane];
+                if (lane == 0) rec[i * rec_stride(RB) + 2 * RB] = 0.0;
             }
         }
         __syncwarp();
@@ -1312,16 +1322,15 @@ __device__ __forceinline__ void upper_solve_rec(int n, const int* __restrict__ f
     constexpr int kPanelWarps = SH::kWarps - 1;
     constexpr int NG = (RB + 7) / 8;  // groups of eight columns per block
     constexpr int PPW = 32 / NG;      // row pairs per warp pass
-    static_assert(NG == 2 || NG == 4, "two or four groups of eight columns cover a block");
+    static_assert(NG == 1 || NG == 2 || NG == 4, "one, two or four groups of eight columns cover a block");
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ptid = threadIdx.x - 32;
     const int nblk = (n + RB - 1) / RB;
     auto load_rec = [&](int K, int buf) {
-        const double* src = rec + static_cast<std::int64_t>(K) * RB * 2 * RB;
-        for (int e = ptid; e < RB * 2 * RB; e += blockDim.x - 32) {
-            const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(&tri[buf][e / (2 * RB)][e % (2 * RB)]));
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src + e) : "memory");
-        }
+        const double* src = rec + static_cast<std::int64_t>(K) * rec_pitch(RB);
+        const unsigned base = static_cast<unsigned>(__cvta_generic_to_shared(&tri[buf][0][0]));
+        for (int e = 2 * ptid; e < rec_size(RB); e += 2 * (blockDim.x - 32))
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(base + 8 * e), "l"(src + e) : "memory");
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
     auto load_table = [&](int K, int slot) {
@@ -1372,7 +1381,7 @@ __device__ __forceinline__ void upper_solve_rec(int n, const int* __restrict__ f
         } else {
             if (K >= 1) load_rec(K - 1, cur ^ 1);
             if (ptid == 0 && K >= 2)
-                prefetch_l2(rec + static_cast<std::int64_t>(K - 2) * RB * 2 * RB, 8LL * RB * 2 * RB);
+                prefetch_l2(rec + static_cast<std::int64_t>(K - 2) * rec_pitch(RB), 8LL * rec_size(RB));
             // block K's column table, for step K - 1 (slot cur was last read at
             // step K + 1); loaded now, stored after this step's loads
             int tfv = INT_MAX;
@@ -1467,7 +1476,7 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) k_solve(const in
     const std::int64_t vb = vbase[j];
     extern __shared__ double y[];
     __shared__ double part[2][SH::RB + 2];
-    __shared__ double tri[2][SH::RB][SH::TS];
+    __shared__ __align__(16) double tri[2][SH::RB][SH::TS];
     const int tid = threadIdx.x;
     // development (CPDDG_SOLVE_DEBUG & 32): per-CTA start / end (globaltimer ns), SM, subdomain
     const bool ctr = (dbg & 32) && tid == 0 && blockIdx.x < 1024;
@@ -1562,6 +1571,372 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) k_solve(const in
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
             g_trace[blockIdx.x][1] = t1;
         }
+    }
+}
+
+// ------------------------------------------------- persistent TMA-streamed solve
+//
+// The register-staged k_solve keeps one wave of factor loads in flight per
+// warp and waits, every block step, for the slowest of its warps' loads: a
+// latency-bound 4.6 TB/s.  k_solve_tma decouples the stream from the steps:
+// one CTA per SM walks its subdomains (byte-balanced at setup) and, per
+// subdomain, the forward then the backward record solve.  Every step is an
+// *item* -- the far rows (forward) or far columns (backward) its consumers
+// apply, its block record, its row descriptor -- that a producer warp copies
+// with cp.async.bulk into a 128 KB shared ring (item slots with an mbarrier
+// each), as far ahead as the ring allows and across pass and subdomain
+// boundaries.  Warp 0 solves the step's block from the record, 14 consumer
+// warps apply the staged item from shared memory; one named barrier per
+// step (the producer is not part of it).
+namespace tmas {
+constexpr int RB = 8;                   // block rows (records built for it; ShapeRec8 is the fallback)
+constexpr int NB = 6;                   // item slots
+constexpr int RING = 128 * 1024;        // staging ring, bytes (power of two)
+constexpr int kMask = RING / 8 - 1;     // ring index mask, doubles
+constexpr int kConsumers = RB;          // consumer warps 2 .. RB + 1 (one per block row)
+constexpr int kThreads = 32 * (2 + kConsumers);
+constexpr int kStep = kThreads - 32;    // warp 0 + consumers: named barrier 1
+constexpr int TS = rec_stride(RB);
+constexpr int kRec = rec_size(RB);      // doubles per record
+constexpr int kDesc = 16;               // ints per descriptor (64 B): f and offset per row
+static_assert(2 * RB <= kDesc, "descriptor holds RB f values and RB offsets");
+struct Item {
+    const double* data;  // far rows / columns of the step's data block (contiguous)
+    long long bytes;     // 0 when the step applies nothing
+    const double* rec;   // the solved block's record
+    const int* desc;     // [0, RB): f of the data block's rows / columns (INT_MAX past n);
+                         // [RB, 2 RB): their offsets in the item (doubles)
+};
+static_assert(sizeof(Item) == 32, "items are 32 bytes");
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+    unsigned done = 0;
+    while (!done) {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+    }
+}
+__device__ __forceinline__ void bulk_copy(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void step_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kStep) : "memory"); }
+}  // namespace tmas
+
+template <int MODE>
+__global__ void __launch_bounds__(tmas::kThreads, 1) k_solve_tma(const int* __restrict__ cta_begin,
+                                                                 const int* __restrict__ cta_subs,
+                                                                 const int* __restrict__ n_rows,
+                                                                 const std::int64_t* __restrict__ vbase,
+                                                                 const std::int64_t* __restrict__ itbase,
+                                                                 const tmas::Item* __restrict__ items,
+                                                                 const int* __restrict__ gidx_all,
+                                                                 const int* __restrict__ sidx_all,
+                                                                 const double* __restrict__ r, double* z,
+                                                                 int accumulate, int dbg) {
+    constexpr int RB = tmas::RB, NB = tmas::NB, RING = tmas::RING, kMask = tmas::kMask;
+    constexpr int kConsumers = tmas::kConsumers, kStep = tmas::kStep, TS = tmas::TS, kRec = tmas::kRec,
+                  kDesc = tmas::kDesc;
+    using tmas::Item;
+    using tmas::smem_u32;
+    using tmas::mbar_wait;
+    using tmas::bulk_copy;
+    using tmas::step_bar;
+    extern __shared__ __align__(128) unsigned char smem[];
+    double* ring = reinterpret_cast<double*>(smem);
+    double* recs = reinterpret_cast<double*>(smem + RING);       // [NB][RB][TS]
+    int* descs = reinterpret_cast<int*>(recs + NB * kRec);        // [NB][kDesc]
+    double* y = reinterpret_cast<double*>(descs + NB * kDesc);    // [max_rows]
+    __shared__ __align__(8) unsigned long long mbar[NB];
+    __shared__ long long prod_start[NB];
+    __shared__ int item_pos[NB];
+    __shared__ volatile int done;  // steps completed (written by thread 0 after the step barrier)
+    __shared__ double red[2][tmas::kConsumers][tmas::RB];  // forward partial dots per consumer warp
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int s0 = cta_begin[blockIdx.x], s1 = cta_begin[blockIdx.x + 1];
+    constexpr bool kFwd = MODE != 2, kBwd = MODE != 1;
+    if (tid == 0) {
+        for (int q = 0; q < NB; ++q) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar[q])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        done = 0;
+    }
+    __syncthreads();
+
+    if (warp == 1) {
+        // ---------------- producer (one thread): items of every step, in step order;
+        // the next item's 32-byte descriptor is loaded one item ahead
+        if (lane != 0) return;
+        unsigned long long head = 0;
+        int t = 0;
+        auto item_at = [&](int si, int pass, int q) -> const Item* {
+            const int j = cta_subs[si];
+            const int nblk = (n_rows[j] + RB - 1) / RB;
+            return items + itbase[j] + static_cast<std::int64_t>(pass) * nblk + q;
+        };
+        // step order: subdomains, then (enabled) passes, then blocks
+        int si = s0, pass = kFwd ? 0 : 1, q = 0;
+        int nblk = si < s1 ? (n_rows[cta_subs[si]] + RB - 1) / RB : 0;
+        auto advance = [&]() {
+            if (++q < nblk) return;
+            q = 0;
+            if (pass == 0 && kBwd) {
+                pass = 1;
+                return;
+            }
+            pass = kFwd ? 0 : 1;
+            if (++si < s1) nblk = (n_rows[cta_subs[si]] + RB - 1) / RB;
+        };
+        Item cur{};
+        if (si < s1) cur = *item_at(si, pass, q);
+        while (si < s1) {
+            advance();
+            Item nxt{};
+            if (si < s1) nxt = *item_at(si, pass, q);  // in flight while this item is issued
+            const long long bytes = cur.bytes;
+            const bool ptr = (dbg & 16) && blockIdx.x == (dbg >> 16) && t < 1024;
+            if (ptr) g_trace[t][6] = clock64();
+            const int slot = t % NB;
+            // spins back off: a tight loop of shared loads slows the consumers' traffic
+            while (done < t - NB + 1) __nanosleep(64);  // slot's previous item consumed
+            if (ptr) g_trace[t][7] = clock64();
+            for (;;) {                                  // ring space
+                const int d = done;
+                const unsigned long long freed = d >= t ? head : prod_start[d % NB];
+                if (head + ((bytes + 127) & ~127LL) - freed <= static_cast<unsigned long long>(RING)) break;
+                __nanosleep(64);
+            }
+            if (ptr) g_trace[t][8] = clock64();
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            prod_start[slot] = static_cast<long long>(head);
+            const unsigned off = static_cast<unsigned>(head & (RING - 1));
+            item_pos[slot] = static_cast<int>(off / 8);
+            const unsigned bar = smem_u32(&mbar[slot]);
+            const bool small = !(dbg & 2);  // dbg & 2: data only (timing experiment)
+            const unsigned tx = static_cast<unsigned>(bytes) + (small ? 8u * kRec + 4u * kDesc : 0u);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(tx) : "memory");
+            if (bytes > 0) {
+                const unsigned first = static_cast<unsigned>(min(bytes, static_cast<long long>(RING - off)));
+                bulk_copy(smem_u32(smem + off), cur.data, first, bar);
+                if (first < bytes)
+                    bulk_copy(smem_u32(smem), reinterpret_cast<const char*>(cur.data) + first,
+                              static_cast<unsigned>(bytes) - first, bar);
+            }
+            if (small) {
+                bulk_copy(smem_u32(recs + slot * kRec), cur.rec, 8u * kRec, bar);
+                bulk_copy(smem_u32(descs + slot * kDesc), cur.desc, 4u * kDesc, bar);
+            }
+            head += static_cast<unsigned long long>((bytes + 127) & ~127LL);
+            if (ptr) {
+                g_trace[t][5] = clock64();
+                g_trace[t][9] = bytes;
+            }
+            cur = nxt;
+            ++t;
+        }
+        return;
+    }
+
+    // ---------------- warp 0 (block solves) + consumer warps
+    const int stid = warp == 0 ? lane : tid - 32;  // 0 .. kStep-1
+    const int cw = warp - 2;                       // consumer warp 0 .. 13
+    const int ct = tid - 64;                       // consumer thread 0 .. 447
+    int t = 0;
+    const double2* ring2 = reinterpret_cast<const double2*>(ring);
+    for (int si = s0; si < s1; ++si) {
+        const int j = cta_subs[si];
+        const int n = n_rows[j];
+        const std::int64_t vb = vbase[j];
+        const int nblk = (n + RB - 1) / RB;
+        for (int p = stid; p < n; p += kStep) {
+            if (MODE == 3) {
+                y[p] = r[vb + p];
+            } else {
+                const int g = __ldg(gidx_all + vb + p);
+                y[p] = g >= 0 ? __ldg(r + g) : 0.0;
+            }
+        }
+        step_bar();
+        if constexpr (kFwd) {
+            for (int k = 0; k < nblk; ++k, ++t) {
+                const int slot = t % NB;
+                const bool tr = (dbg & 16) && blockIdx.x == (dbg >> 16) && t < 1024;
+                if (tr && stid == 0) g_trace[t][0] = clock64();
+                mbar_wait(smem_u32(&mbar[slot]), static_cast<unsigned>((t / NB) & 1));
+                if (tr && stid == 0) g_trace[t][1] = clock64();
+                const double* R = recs + slot * kRec;
+                const int r0 = k * RB;
+                if (dbg & 1) {
+                    // timing experiment: stream only (no solve work)
+                } else if (warp == 0) {
+                    if (tr && lane == 0) g_trace[t][10] = clock64();
+                    const int i = r0 + lane;
+                    const bool live = lane < RB && i < n;
+                    double pk = 0.0;
+                    if (k > 0 && lane < RB) {
+#pragma unroll
+                        for (int w = 0; w < kConsumers; ++w) pk += red[k & 1][w][lane];
+                    }
+                    const double tv = live ? y[i] - pk : 0.0;
+                    const double* trow = R + (lane < RB ? lane : 0) * TS;
+                    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+                    for (int c = 0; c < RB; c += 2) {
+                        a2 = fma(trow[RB + c], __shfl_sync(0xffffffffu, tv, c), a2);
+                        a3 = fma(trow[RB + c + 1], __shfl_sync(0xffffffffu, tv, c + 1), a3);
+                    }
+                    if (tr && lane == 0) g_trace[t][11] = clock64();
+                    if (r0 >= RB) {
+#pragma unroll
+                        for (int c = 0; c < RB; c += 2) {
+                            a0 = fma(trow[c], y[r0 - RB + c], a0);
+                            a1 = fma(trow[c + 1], y[r0 - RB + c + 1], a1);
+                        }
+                    }
+                    if (live) y[i] = (a2 + a3) - (a0 + a1);
+                } else if (k + 1 < nblk) {
+                    // partial dots of block k+1's rows over columns [f_r, k RB) of the
+                    // staged far rows: thread per column pair, y read once for all
+                    // RB rows, per-warp sums by a multi-value butterfly into red[]
+                    // (summed by warp 0 next step in warp order: deterministic)
+                    const int* D = descs + slot * kDesc;
+                    const int lim = r0;
+                    int fr[RB], orr[RB];
+                    int fmin = lim;
+#pragma unroll
+                    for (int q = 0; q < RB; ++q) {
+                        fr[q] = D[q];
+                        orr[q] = item_pos[slot] + D[RB + q] - fr[q];
+                        fmin = min(fmin, fr[q]);
+                    }
+                    double acc[RB];
+#pragma unroll
+                    for (int q = 0; q < RB; ++q) acc[q] = 0.0;
+                    const double2* y2 = reinterpret_cast<const double2*>(y);
+                    for (int c = (fmin & ~1) + 2 * ct; c < lim; c += 2 * 32 * kConsumers) {
+                        const double2 yy = y2[c >> 1];
+#pragma unroll
+                        for (int q = 0; q < RB; ++q) {
+                            if (c >= fr[q]) {
+                                const double2 v = ring2[((orr[q] + c) & kMask) >> 1];
+                                acc[q] = fma(v.x, yy.x, acc[q]);
+                                acc[q] = fma(v.y, yy.y, acc[q]);
+                            }
+                        }
+                    }
+                    static_assert(RB == 8, "the butterfly below reduces eight rows");
+                    // 8 values over 32 lanes: xor 16 / 8 / 4 halve the set, xor 2 / 1 finish
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const bool hi = lane & 16;
+                        const double send = hi ? acc[q] : acc[q + 4];
+                        const double keep = hi ? acc[q + 4] : acc[q];
+                        acc[q] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+                    }
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        const bool hi = lane & 8;
+                        const double send = hi ? acc[q] : acc[q + 2];
+                        const double keep = hi ? acc[q + 2] : acc[q];
+                        acc[q] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+                    }
+                    {
+                        const bool hi = lane & 4;
+                        const double send = hi ? acc[0] : acc[1];
+                        const double keep = hi ? acc[1] : acc[0];
+                        acc[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+                    }
+                    acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 2);
+                    acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 1);
+                    if ((lane & 3) == 0) {
+                        const int row = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+                        red[(k + 1) & 1][cw][row] = acc[0];
+                    }
+                }
+                if (tr && lane == 0 && warp == 0) g_trace[t][2] = clock64();
+                if (tr && lane == 0 && warp == 2) g_trace[t][3] = clock64();
+                step_bar();
+                if (tr && stid == 0) g_trace[t][4] = clock64();
+                if (stid == 0) done = t + 1;
+            }
+        }
+        if constexpr (kBwd) {
+            for (int K = nblk - 1; K >= 0; --K, ++t) {
+                const int slot = t % NB;
+                const bool tr = (dbg & 16) && blockIdx.x == (dbg >> 16) && t < 1024;
+                if (tr && stid == 0) g_trace[t][0] = clock64();
+                mbar_wait(smem_u32(&mbar[slot]), static_cast<unsigned>((t / NB) & 1));
+                if (tr && stid == 0) g_trace[t][1] = clock64();
+                const double* R = recs + slot * kRec;
+                const int r0 = K * RB;
+                if (dbg & 1) {
+                    // timing experiment: stream only (no solve work)
+                } else if (warp == 0) {
+                    const int i = r0 + lane;
+                    const bool live = lane < RB && i < n;
+                    const double tv = live ? y[i] : 0.0;
+                    const double* trow = R + (lane < RB ? lane : 0) * TS;
+                    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+                    for (int c = 0; c < RB; c += 2) {
+                        a2 = fma(trow[RB + c], __shfl_sync(0xffffffffu, tv, c), a2);
+                        a3 = fma(trow[RB + c + 1], __shfl_sync(0xffffffffu, tv, c + 1), a3);
+                    }
+                    if (K + 1 < nblk) {
+                        const int nb = min(RB, n - (r0 + RB));
+                        for (int c = 0; c < nb; ++c) {
+                            if (c & 1)
+                                a1 = fma(trow[c], y[r0 + RB + c], a1);
+                            else
+                                a0 = fma(trow[c], y[r0 + RB + c], a0);
+                        }
+                    }
+                    if (live) y[i] = (a2 + a3) - (a0 + a1);
+                } else if (K + 1 < nblk) {
+                    // block K+1's far columns onto rows [jmin, K RB): thread per row pair
+                    const int* D = descs + slot * kDesc;
+                    const int c0 = r0 + RB;
+                    int fc[RB], oc[RB];
+                    double xc[RB];
+                    int jmin = r0;
+#pragma unroll
+                    for (int c = 0; c < RB; ++c) {
+                        fc[c] = D[c];
+                        oc[c] = D[RB + c] - fc[c];
+                        if (fc[c] < r0) jmin = min(jmin, fc[c]);
+                        xc[c] = c0 + c < n ? y[c0 + c] : 0.0;
+                    }
+                    const int base = item_pos[slot];
+                    for (int row = (jmin & ~1) + 2 * ct; row < r0; row += 2 * 32 * kConsumers) {
+                        double q0 = 0.0, q1 = 0.0;
+#pragma unroll
+                        for (int c = 0; c < RB; ++c) {
+                            if (row >= fc[c]) {
+                                const double2 v = ring2[((base + oc[c] + row) & kMask) >> 1];
+                                q0 = fma(v.x, xc[c], q0);
+                                q1 = fma(v.y, xc[c], q1);
+                            }
+                        }
+                        y[row] -= q0;
+                        y[row + 1] -= q1;
+                    }
+                }
+                if (tr && lane == 0 && warp == 0) g_trace[t][2] = clock64();
+                if (tr && lane == 0 && warp == 2) g_trace[t][3] = clock64();
+                step_bar();
+                if (tr && stid == 0) g_trace[t][4] = clock64();
+                if (stid == 0) done = t + 1;
+            }
+        }
+        for (int p = stid; p < n; p += kStep) {
+            if (MODE == 3) {
+                z[vb + p] = y[p];
+            } else {
+                const int sx = __ldg(sidx_all + vb + p);
+                if (sx >= 0) z[sx] = accumulate ? z[sx] + y[p] : y[p];
+            }
+        }
+        step_bar();
     }
 }
 
@@ -1697,11 +2072,22 @@ void pc_apply_mode(const cpddg_pc* pc, const double* r, double* z, bool accumula
         CPDDG_CUDA(cudaGetLastError());
         return;
     }
+    if (pc->tma) {
+        auto kern = mode == 1 ? k_solve_tma<1> : mode == 2 ? k_solve_tma<2> : mode == 3 ? k_solve_tma<3> : k_solve_tma<0>;
+        kern<<<pc->tma_grid, tmas::kThreads, pc->tma_smem, st>>>(
+            pc->tma_cta_begin.get(), pc->tma_cta_subs.get(), pc->n_rows.get(), pc->vbase.get(), pc->tma_itbase.get(),
+            reinterpret_cast<const tmas::Item*>(pc->tma_items.get()), pc->gidx.get(), pc->sidx.get(), r, z,
+            accumulate ? 1 : 0, dbg);
+        CPDDG_CUDA(cudaGetLastError());
+        return;
+    }
     if (!pc->urows && pc->blockinv) {
         if (pc->shape == 0)
             launch_solve<false, ShapeBig, true>(pc, grid, r, z, accumulate, mode, dbg, st);
         else if (pc->shape == 1)
             launch_solve<false, ShapeMid, true>(pc, grid, r, z, accumulate, mode, dbg, st);
+        else if (pc->shape == 4)
+            launch_solve<false, ShapeRec8, true>(pc, grid, r, z, accumulate, mode, dbg, st);
         else
             launch_solve<false, ShapeRec, true>(pc, grid, r, z, accumulate, mode, dbg, st);
     } else if (!pc->urows)
@@ -1723,6 +2109,105 @@ void pc_apply_mode(const cpddg_pc* pc, const double* r, double* z, bool accumula
 
 void pc_apply(const cpddg_pc* pc, const double* r, double* z, bool accumulate, cudaStream_t st) {
     pc_apply_mode(pc, r, z, accumulate, 0, st);
+}
+
+/** Items, descriptors and the per-CTA subdomain lists of k_solve_tma (see
+ *  there).  Subdomains go to CTAs (one per SM) longest-processing-time first
+ *  by streamed bytes; the path is left off if an item would not fit the ring. */
+static void setup_tma(cpddg_pc* pc, const std::vector<int>& n_rows, const std::vector<std::int64_t>& vbase,
+                      const std::vector<int>& fL, const std::vector<int>& fU, const std::vector<std::int64_t>& rocL,
+                      const std::vector<std::int64_t>& cbL, const std::vector<std::int64_t>& rocU,
+                      const std::vector<std::int64_t>& cbU, const std::vector<std::int64_t>& rbase) {
+    using tmas::RB;
+    const int n_sub = pc->n_sub;
+    std::vector<std::int64_t> itbase(static_cast<std::size_t>(n_sub)), cost(static_cast<std::size_t>(n_sub), 0);
+    std::int64_t n_items = 0;
+    for (int j = 0; j < n_sub; ++j) {
+        itbase[static_cast<std::size_t>(j)] = n_items;
+        n_items += 2 * ((n_rows[static_cast<std::size_t>(j)] + RB - 1) / RB);
+    }
+    std::vector<tmas::Item> items(static_cast<std::size_t>(n_items));
+    std::vector<int> desc(static_cast<std::size_t>(n_items) * tmas::kDesc, INT_MAX);
+    DevBuf<int> ddesc(desc.size());
+    const double* Lc = pc->L.get();
+    const double* Uc = pc->U.get();
+    long long max_bytes = 0;
+    for (int j = 0; j < n_sub; ++j) {
+        const int n = n_rows[static_cast<std::size_t>(j)];
+        const int nblk = (n + RB - 1) / RB;
+        const std::int64_t v0 = vbase[static_cast<std::size_t>(j)];
+        for (int pass = 0; pass < 2; ++pass) {
+            const std::vector<int>& f = pass ? fU : fL;
+            const std::vector<std::int64_t>& roc = pass ? rocU : rocL;
+            const double* V = (pass ? Uc : Lc) + (pass ? cbU : cbL)[static_cast<std::size_t>(j)];
+            const double* rec = (pass ? pc->recU.get() : pc->recL.get()) + rbase[static_cast<std::size_t>(j)];
+            for (int q = 0; q < nblk; ++q) {
+                const int k = pass ? nblk - 1 - q : q;  // the block solved at this step
+                const int B = k + 1;                    // the block whose far part the step applies
+                const std::int64_t it = itbase[static_cast<std::size_t>(j)] + static_cast<std::int64_t>(pass) * nblk + q;
+                tmas::Item& I = items[static_cast<std::size_t>(it)];
+                I.rec = rec + static_cast<std::int64_t>(k) * rec_pitch(RB);
+                I.desc = ddesc.get() + it * tmas::kDesc;
+                I.data = V;
+                I.bytes = 0;
+                for (int c = 0; c < RB; ++c) desc[static_cast<std::size_t>(it * tmas::kDesc + RB + c)] = 0;
+                if (B < nblk) {
+                    const int lim = (B - 1) * RB;
+                    long long len = 0;
+                    for (int c = 0; c < RB && B * RB + c < n; ++c) {
+                        const int fc = f[static_cast<std::size_t>(v0 + B * RB + c)];
+                        desc[static_cast<std::size_t>(it * tmas::kDesc + c)] = fc;
+                        desc[static_cast<std::size_t>(it * tmas::kDesc + RB + c)] = static_cast<int>(len);
+                        len += std::max(0, lim - fc);
+                    }
+                    I.data = V + roc[static_cast<std::size_t>(v0 + B * RB)];
+                    I.bytes = 8 * len;
+                    max_bytes = std::max(max_bytes, I.bytes);
+                }
+                cost[static_cast<std::size_t>(j)] += I.bytes + 8 * tmas::kRec;
+            }
+        }
+    }
+    if (std::getenv("CPDDG_VERBOSE")) {
+        std::vector<long long> sz;
+        for (const auto& I : items) sz.push_back(I.bytes);
+        std::sort(sz.begin(), sz.end());
+        auto over = [&](long long b) { return static_cast<long long>(sz.end() - std::upper_bound(sz.begin(), sz.end(), b)); };
+        std::fprintf(stderr, "[cpddg] tma items %zu: p50 %lld p99 %lld max %lld bytes; over 64K %lld, over 96K %lld, over 128K %lld\n",
+                     sz.size(), sz[sz.size() / 2], sz[sz.size() * 99 / 100], sz.back(), over(65536), over(98304),
+                     over(131072));
+    }
+    if (max_bytes > tmas::RING) return;  // an item exceeds the ring: keep the register-staged solve
+    // longest processing time first onto min(#SMs, n_sub) CTAs
+    const int grid = std::min(sm_count(), n_sub);
+    std::vector<int> by_cost(static_cast<std::size_t>(n_sub));
+    std::iota(by_cost.begin(), by_cost.end(), 0);
+    std::stable_sort(by_cost.begin(), by_cost.end(),
+                     [&](int a, int b) { return cost[static_cast<std::size_t>(a)] > cost[static_cast<std::size_t>(b)]; });
+    std::vector<std::int64_t> load(static_cast<std::size_t>(grid), 0);
+    std::vector<std::vector<int>> lists(static_cast<std::size_t>(grid));
+    for (int j : by_cost) {
+        const auto m = std::min_element(load.begin(), load.end()) - load.begin();
+        lists[static_cast<std::size_t>(m)].push_back(j);
+        load[static_cast<std::size_t>(m)] += cost[static_cast<std::size_t>(j)];
+    }
+    std::vector<int> begin{0}, subs;
+    for (const auto& L : lists) {
+        subs.insert(subs.end(), L.begin(), L.end());
+        begin.push_back(static_cast<int>(subs.size()));
+    }
+    CPDDG_CUDA(cudaMemcpy(ddesc.get(), desc.data(), desc.size() * sizeof(int), cudaMemcpyHostToDevice));
+    pc->tma_desc = std::move(ddesc);
+    pc->tma_items.alloc(items.size() * sizeof(tmas::Item));
+    CPDDG_CUDA(cudaMemcpy(pc->tma_items.get(), items.data(), items.size() * sizeof(tmas::Item), cudaMemcpyHostToDevice));
+    pc->tma_itbase.upload(itbase);
+    pc->tma_cta_begin.upload(begin);
+    pc->tma_cta_subs.upload(subs);
+    pc->tma_grid = grid;
+    pc->tma_smem = tmas::RING + 8 * tmas::NB * tmas::kRec + 4 * tmas::NB * tmas::kDesc + 8 * pc->max_rows;
+    for (auto kern : {k_solve_tma<0>, k_solve_tma<1>, k_solve_tma<2>, k_solve_tma<3>})
+        CPDDG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pc->tma_smem));
+    pc->tma = true;
 }
 
 static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* locals, const cpddg_pc_options* opt) {
@@ -1956,6 +2441,7 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
     set_solve_smem<false, ShapeBig, true>(pc->solve_smem);
     set_solve_smem<false, ShapeMid, true>(pc->solve_smem);
     set_solve_smem<false, ShapeRec, true>(pc->solve_smem);
+    set_solve_smem<false, ShapeRec8, true>(pc->solve_smem);
     // block shape: one CTA per subdomain, all resident in one wave
     {
         const int S = sm_count();
@@ -1969,30 +2455,40 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
     }
     // record solve: block records from the full rows, then the rows compacted
     // to their far parts (CPDDG_BLOCKINV=0 keeps the substitution-chain solve)
+    // persistent TMA-streamed solve (k_solve_tma): U by columns, records for tmas::RB
+    bool want_tma = false;
+    {
+        const char* te = std::getenv("CPDDG_TMA");
+        const int tma_smem = tmas::RING + 8 * tmas::NB * tmas::kRec + 4 * tmas::NB * tmas::kDesc + 8 * pc->max_rows;
+        want_tma = pc->blockinv && !pc->urows && pc->shape == 3 && !(te && std::string(te) == "0") &&
+                   tma_smem <= 227 * 1024;
+        if (want_tma) pc->shape = 4;  // the streamed path's RB; ShapeRec8 if an item would not fit the ring
+    }
     if (pc->blockinv) {
-        const int rb = pc->shape >= 2 ? ShapeRec::RB : ShapeMid::RB;
+        const int rb = pc->shape == 4 ? tmas::RB : pc->shape >= 2 ? ShapeRec::RB : ShapeMid::RB;
         static_assert(ShapeBig::RB == ShapeMid::RB && ShapeSmall::RB == ShapeRec::RB,
                       "records are built for RB = 30 or RB = 14");
         std::vector<std::int64_t> rbase(static_cast<std::size_t>(n_sub));
         std::int64_t rt = 0;
         for (int j = 0; j < n_sub; ++j) {
             rbase[static_cast<std::size_t>(j)] = rt;
-            rt += static_cast<std::int64_t>((n_rows[static_cast<std::size_t>(j)] + rb - 1) / rb) * rb * 2 * rb;
+            rt += static_cast<std::int64_t>((n_rows[static_cast<std::size_t>(j)] + rb - 1) / rb) * rec_pitch(rb);
         }
         pc->rec_entries = 2 * rt;
         pc->rbase.upload(rbase);
         pc->recL.alloc(static_cast<std::size_t>(std::max<std::int64_t>(rt, 1)));
         pc->recU.alloc(static_cast<std::size_t>(std::max<std::int64_t>(rt, 1)));
         const dim3 rgrid(static_cast<unsigned>(n_sub), 16);
-        auto records = rb == 30 ? k_block_records<30> : k_block_records<ShapeSmall::RB>;
-        auto compact = rb == 30 ? k_compact_rows<30> : k_compact_rows<ShapeSmall::RB>;
+        auto records = rb == 30 ? k_block_records<30> : rb == 14 ? k_block_records<14> : k_block_records<tmas::RB>;
+        auto compact = rb == 30 ? k_compact_rows<30> : rb == 14 ? k_compact_rows<14> : k_compact_rows<tmas::RB>;
         records<<<rgrid, 64>>>(pc->n_rows.get(), pc->vbase.get(), pc->ebase.get(), pc->first.get(), pc->roff.get(),
                                pc->L.get(), nullptr, pc->rbase.get(), pc->recL.get());
         if (pc->urows)
             records<<<rgrid, 64>>>(pc->n_rows.get(), pc->vbase.get(), pc->ubase.get(), pc->ufirst.get(),
                                    pc->uroff.get(), pc->U.get(), pc->drev.get(), pc->rbase.get(), pc->recU.get());
         else
-            (rb == 30 ? k_block_records_upper<30> : k_block_records_upper<ShapeSmall::RB>)<<<rgrid, 64>>>(
+            (rb == 30 ? k_block_records_upper<30> : rb == 14 ? k_block_records_upper<14>
+                                                  : k_block_records_upper<tmas::RB>)<<<rgrid, 64>>>(
                 pc->n_rows.get(), pc->vbase.get(), pc->ebaseU.get(), pc->firstU.get(), pc->roffU.get(), pc->U.get(),
                 pc->dinv.get(), pc->rbase.get(), pc->recU.get());
         CPDDG_CUDA(cudaGetLastError());
@@ -2006,11 +2502,12 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
                 const std::int64_t v0 = vbase[static_cast<std::size_t>(j)];
                 std::int64_t off = 0;
                 for (int i = 0; i < n_rows[static_cast<std::size_t>(j)]; ++i) {
+                    if (i % rb == 0) off = (off + 15) / 16 * 16;  // blocks start on 128-byte lines
                     const int fi = f[static_cast<std::size_t>(v0 + i)];
                     roc[static_cast<std::size_t>(v0 + i)] = off;
                     off += std::max(0, (i / rb - 1) * rb - fi);
                 }
-                tot += off;
+                tot += (off + 15) / 16 * 16;
             }
             return tot;
         };
@@ -2065,6 +2562,7 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
             pc->ebaseU = std::move(dcbU);
         }
         pc->far_entries = nL + nU;
+        if (want_tma) setup_tma(pc.get(), n_rows, vbase, first, firstU, rocL, cbL, rocU, cbU, rbase);
     }
     // factor probe (cpddg_pc_options::check_residual): solve A_j z = A_j x_probe
     // on the device for every subdomain and check the residual on the host --
