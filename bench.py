@@ -364,8 +364,9 @@ def main():
             "kernel_ms": {"pc_apply_avg": 1e3 * avg_pc, "op_apply_avg": 1e3 * op_s / max(op_n, 1)},
             "op_roofline_GBs": op_alg / (op_s / max(op_n, 1)) / 1e9 if op_n else None,
         },
-        "roofline": {"bound": "hbm", "kernel": "k_solve_dense (preconditioner apply, dense small-system mode)"
-                     if pcs["apply_mode"] == 1 else "k_solve (preconditioner apply)", "achieved": achieved,
+        "roofline": {"bound": "hbm", "kernel": {1: "k_solve_dense (preconditioner apply, dense small-system mode)",
+                                                 2: "k_solve_tma (preconditioner apply, TMA-streamed record solve)"}
+                     .get(pcs["apply_mode"], "k_solve (preconditioner apply, record solve)"), "achieved": achieved,
                      "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": ncu_traffic() if WORKLOAD is CONFIGS["headline"] else None,
                      "algorithmic_bytes_per_launch": pcs["algorithmic_bytes"], "peak_source": peak_src},

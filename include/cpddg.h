@@ -175,7 +175,8 @@ typedef struct {
     double factor_seconds;      /* device factorisation time */
     double analyse_seconds;     /* host ordering + symbolic time */
     double max_probe_residual;  /* when check_residual */
-    int apply_mode;             /* 0: envelope triangular solves (k_solve); 1: dense local inverses (small systems) */
+    int apply_mode;             /* 0: register-staged record / envelope solves (k_solve); 1: dense local inverses
+                                   (small systems); 2: persistent TMA-streamed record solve (k_solve_tma) */
 } cpddg_pc_stats;
 
 CPDDG_API int cpddg_pc_create(int n_global, int n_sub, const cpddg_local_desc* locals,

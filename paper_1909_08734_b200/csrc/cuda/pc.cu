@@ -2735,7 +2735,7 @@ int cpddg_pc_stats_get(const cpddg_pc* pc, cpddg_pc_stats* st) {
         st->factor_seconds = pc->factor_seconds;
         st->analyse_seconds = pc->analyse_seconds;
         st->max_probe_residual = pc->max_probe_residual;
-        st->apply_mode = pc->dense ? 1 : 0;
+        st->apply_mode = pc->dense ? 1 : pc->tma ? 2 : 0;
     });
 }
 

@@ -300,3 +300,39 @@ def test_run_solve_pipeline_with_files(tmp_path):
     assert lines[0] == "iter,residual_2norm" and len(lines) == out["log"].iterations + 2
     assert (tmp_path / "solution.csv").read_text().startswith("x,y,z,u\n")
     assert (tmp_path / "timings.csv").read_text().splitlines()[-1].startswith("preconditioned_solve,")
+
+
+def test_streamed_record_and_chain_solves_agree(monkeypatch):
+    """The three preconditioner solve paths give the same A_j^-1 (to 1e-12)
+    and the same GMRES iteration count, and match the oracle restatement
+    (SuperLU per subdomain) at the usual 1e-9: the persistent TMA-streamed
+    record solve (k_solve_tma, default when there are more subdomains than
+    SMs), the register-staged record solve (CPDDG_TMA=0) and the
+    substitution-chain solve on reversed U rows (CPDDG_BLOCKINV=0).  Sphere
+    h = 0.05 cut into 256 RCB parts, so the streamed path is the one taken."""
+    import torch
+
+    import cpdd_oracle as O
+    from paper_1909_08734_b200 import api, inputs
+    P = api.Problem("sphere", h=0.05, p=3, c=1.0)
+    P.decompose(inputs.rcb_partition(P.active_cp, 256), 2, "oras", 4.0, 40.0)
+    A = api.DeviceHelmholtz.from_problem(P)
+    M = api.SchwarzPreconditioner.from_problem(P)
+    assert M.stats()["apply_mode"] == 2
+    monkeypatch.setenv("CPDDG_TMA", "0")
+    Mr = api.SchwarzPreconditioner.from_problem(P)
+    monkeypatch.setenv("CPDDG_BLOCKINV", "0")
+    Mc = api.SchwarzPreconditioner.from_problem(P)
+    assert Mr.stats()["apply_mode"] == 0 and Mc.stats()["apply_mode"] == 0
+    x = inputs.uniform_vector(P.n_active, 11)
+    xd = torch.from_numpy(x).cuda()
+    z, zr, zc = (m.apply(xd).cpu().numpy() for m in (M, Mr, Mc))
+    nz = np.linalg.norm(zc)
+    assert np.linalg.norm(z - zc) <= 1e-12 * nz and np.linalg.norm(zr - zc) <= 1e-12 * nz
+    assert np.array_equal(z, M.apply(xd).cpu().numpy())  # bitwise reproducible
+    locs = [P.local(j) for j in range(P.n_sub)]
+    z_ref = O.schwarz_apply(locs, x)
+    assert np.linalg.norm(z - z_ref) <= 1e-9 * np.linalg.norm(z_ref)
+    b = torch.from_numpy(inputs.rhs_sphere(P.active_cp)).cuda()
+    its = [api.gmres_solve(A, b, m, 1e-10, 1000, 50).log.iterations for m in (M, Mr, Mc)]
+    assert its[0] == its[1] == its[2]
