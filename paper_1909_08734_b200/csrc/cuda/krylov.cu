@@ -151,16 +151,19 @@ __global__ void __launch_bounds__(kRedThreads) k_mgs_reg(int n, int m, const dou
     const int nb = gridDim.x;
     const int stride = gridDim.x * blockDim.x;
     const int i0 = blockIdx.x * blockDim.x + threadIdx.x;
-    double wr[EPT], vr[EPT];
+    // vc: this pass's basis vector slice, loaded during the previous pass
+    // (before its grid barrier: the loads do not depend on h)
+    double wr[EPT], vr[EPT], vc[EPT];
 #pragma unroll
     for (int k = 0; k < EPT; ++k) {
         const int i = i0 + k * stride;
         wr[k] = i < n ? w[i] : 0.0;
         vr[k] = 0.0;
+        vc[k] = (i < n && m >= 0) ? __ldcg(V[0] + i) : 0.0;
     }
     double hprev = 0.0;
     for (int pass = 0; pass <= m + 1; ++pass) {
-        const double* vn = pass <= m ? V[pass] : nullptr;
+        const bool has_v = pass <= m;
         double a1 = 0.0, a2 = 0.0;
 #pragma unroll
         for (int k = 0; k < EPT; ++k) {
@@ -171,10 +174,18 @@ __global__ void __launch_bounds__(kRedThreads) k_mgs_reg(int n, int m, const dou
                     wi -= hprev * vr[k];
                     wr[k] = wi;
                 }
-                const double vi = vn ? __ldcg(vn + i) : wi;
+                const double vi = has_v ? vc[k] : wi;
                 vr[k] = vi;
                 a1 = fma(vi, wi, a1);
                 if (pass == 0) a2 = fma(wi, wi, a2);
+            }
+        }
+        if (pass + 1 <= m) {
+            const double* vn = V[pass + 1];
+#pragma unroll
+            for (int k = 0; k < EPT; ++k) {
+                const int i = i0 + k * stride;
+                vc[k] = i < n ? __ldcg(vn + i) : 0.0;
             }
         }
         const double b1 = block_sum<kRedThreads>(a1, sh);

@@ -1738,6 +1738,13 @@ __global__ void __launch_bounds__(tmas::kThreads, 1) k_solve_tma(const int* __re
     }
 
     // ---------------- warp 0 (block solves) + consumer warps
+    const bool ctr = (dbg & 32) && tid == 0 && blockIdx.x < 1024;
+    if (ctr) {
+        long long t0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        g_trace[blockIdx.x][0] = t0;
+        g_trace[blockIdx.x][2] = s1 - s0;
+    }
     const int stid = warp == 0 ? lane : tid - 32;  // 0 .. kStep-1
     const int cw = warp - 2;                       // consumer warp 0 .. 13
     const int ct = tid - 64;                       // consumer thread 0 .. 447
@@ -1937,6 +1944,11 @@ __global__ void __launch_bounds__(tmas::kThreads, 1) k_solve_tma(const int* __re
             }
         }
         step_bar();
+    }
+    if (ctr) {
+        long long t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        g_trace[blockIdx.x][1] = t1;
     }
 }
 
@@ -2164,7 +2176,8 @@ static void setup_tma(cpddg_pc* pc, const std::vector<int>& n_rows, const std::v
                     I.bytes = 8 * len;
                     max_bytes = std::max(max_bytes, I.bytes);
                 }
-                cost[static_cast<std::size_t>(j)] += I.bytes + 8 * tmas::kRec;
+                // measured step cost (scripts/trace_tma_steps.py): ~1,060 cycles + ~27 cycles per KB
+                cost[static_cast<std::size_t>(j)] += 1060 * 1024 + 27 * I.bytes;
             }
         }
     }
