@@ -1810,12 +1810,18 @@ __global__ void __launch_bounds__(tmas::kThreads, 1) k_solve_tma(const int* __re
                     const int lim = r0;
                     int fr[RB], orr[RB];
                     int fmin = lim;
+                    const int ipos = item_pos[slot];
+                    static_assert(RB % 4 == 0, "descriptor read as int4");
 #pragma unroll
-                    for (int q = 0; q < RB; ++q) {
-                        fr[q] = D[q];
-                        orr[q] = item_pos[slot] + D[RB + q] - fr[q];
-                        fmin = min(fmin, fr[q]);
+                    for (int q = 0; q < RB; q += 4) {  // 16-byte descriptor reads
+                        const int4 f4 = *reinterpret_cast<const int4*>(D + q);
+                        const int4 o4 = *reinterpret_cast<const int4*>(D + RB + q);
+                        fr[q] = f4.x, fr[q + 1] = f4.y, fr[q + 2] = f4.z, fr[q + 3] = f4.w;
+                        orr[q] = ipos + o4.x - f4.x, orr[q + 1] = ipos + o4.y - f4.y;
+                        orr[q + 2] = ipos + o4.z - f4.z, orr[q + 3] = ipos + o4.w - f4.w;
                     }
+#pragma unroll
+                    for (int q = 0; q < RB; ++q) fmin = min(fmin, fr[q]);
                     double acc[RB];
 #pragma unroll
                     for (int q = 0; q < RB; ++q) acc[q] = 0.0;
@@ -1907,11 +1913,23 @@ __global__ void __launch_bounds__(tmas::kThreads, 1) k_solve_tma(const int* __re
                     double xc[RB];
                     int jmin = r0;
 #pragma unroll
-                    for (int c = 0; c < RB; ++c) {
-                        fc[c] = D[c];
-                        oc[c] = D[RB + c] - fc[c];
-                        if (fc[c] < r0) jmin = min(jmin, fc[c]);
-                        xc[c] = c0 + c < n ? y[c0 + c] : 0.0;
+                    for (int c = 0; c < RB; c += 4) {  // 16-byte descriptor reads
+                        const int4 f4 = *reinterpret_cast<const int4*>(D + c);
+                        const int4 o4 = *reinterpret_cast<const int4*>(D + RB + c);
+                        fc[c] = f4.x, fc[c + 1] = f4.y, fc[c + 2] = f4.z, fc[c + 3] = f4.w;
+                        oc[c] = o4.x - f4.x, oc[c + 1] = o4.y - f4.y, oc[c + 2] = o4.z - f4.z, oc[c + 3] = o4.w - f4.w;
+                    }
+#pragma unroll
+                    for (int c = 0; c < RB; ++c) jmin = fc[c] < r0 ? min(jmin, fc[c]) : jmin;
+                    if (c0 + RB <= n) {  // x of block K+1 (16-byte aligned: c0 is a multiple of RB)
+#pragma unroll
+                        for (int c = 0; c < RB; c += 2) {
+                            const double2 x2 = *reinterpret_cast<const double2*>(y + c0 + c);
+                            xc[c] = x2.x, xc[c + 1] = x2.y;
+                        }
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < RB; ++c) xc[c] = c0 + c < n ? y[c0 + c] : 0.0;
                     }
                     const int base = item_pos[slot];
                     for (int row = (jmin & ~1) + 2 * ct; row < r0; row += 2 * 32 * kConsumers) {
