@@ -2208,7 +2208,11 @@ static void setup_tma(cpddg_pc* pc, const std::vector<int>& n_rows, const std::v
                      sz.size(), sz[sz.size() / 2], sz[sz.size() * 99 / 100], sz.back(), over(65536), over(98304),
                      over(131072));
     }
-    if (max_bytes > tmas::RING) return;  // an item exceeds the ring: keep the register-staged solve
+    // an item exceeds the ring: keep the register-staged solve (ShapeRec8 over the same
+    // records); CPDDG_TMA_RING_LIMIT (bytes) lowers the limit to exercise that fallback
+    long long limit = tmas::RING;
+    if (const char* e = std::getenv("CPDDG_TMA_RING_LIMIT")) limit = std::min(limit, std::atoll(e));
+    if (max_bytes > limit) return;
     // longest processing time first onto min(#SMs, n_sub) CTAs
     const int grid = std::min(sm_count(), n_sub);
     std::vector<int> by_cost(static_cast<std::size_t>(n_sub));

@@ -308,7 +308,8 @@ def test_streamed_record_and_chain_solves_agree(monkeypatch):
     (SuperLU per subdomain) at the usual 1e-9: the persistent TMA-streamed
     record solve (k_solve_tma, default when there are more subdomains than
     SMs), the register-staged record solve (CPDDG_TMA=0) and the
-    substitution-chain solve on reversed U rows (CPDDG_BLOCKINV=0).  Sphere
+    substitution-chain solve on reversed U rows (CPDDG_BLOCKINV=0); also the
+    streamed path's fallback when an item would not fit its ring.  Sphere
     h = 0.05 cut into 256 RCB parts, so the streamed path is the one taken."""
     import torch
 
@@ -319,6 +320,9 @@ def test_streamed_record_and_chain_solves_agree(monkeypatch):
     A = api.DeviceHelmholtz.from_problem(P)
     M = api.SchwarzPreconditioner.from_problem(P)
     assert M.stats()["apply_mode"] == 2
+    monkeypatch.setenv("CPDDG_TMA_RING_LIMIT", "1024")  # every item "too large": ShapeRec8 fallback
+    Mf = api.SchwarzPreconditioner.from_problem(P)
+    monkeypatch.delenv("CPDDG_TMA_RING_LIMIT")
     monkeypatch.setenv("CPDDG_TMA", "0")
     Mr = api.SchwarzPreconditioner.from_problem(P)
     monkeypatch.setenv("CPDDG_BLOCKINV", "0")
@@ -330,6 +334,9 @@ def test_streamed_record_and_chain_solves_agree(monkeypatch):
     nz = np.linalg.norm(zc)
     assert np.linalg.norm(z - zc) <= 1e-12 * nz and np.linalg.norm(zr - zc) <= 1e-12 * nz
     assert np.array_equal(z, M.apply(xd).cpu().numpy())  # bitwise reproducible
+    assert Mf.stats()["apply_mode"] == 0
+    zf = Mf.apply(xd).cpu().numpy()
+    assert np.linalg.norm(zf - zc) <= 1e-12 * nz
     locs = [P.local(j) for j in range(P.n_sub)]
     z_ref = O.schwarz_apply(locs, x)
     assert np.linalg.norm(z - z_ref) <= 1e-9 * np.linalg.norm(z_ref)
