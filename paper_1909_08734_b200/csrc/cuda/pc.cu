@@ -360,7 +360,7 @@ __device__ __forceinline__ SubPtrs sub_ptrs(int j, const int* n_rows, const std:
 constexpr int kFactorThreads = 256;
 constexpr int kTS = TILE + 1;  // padded tile row stride (doubles) -- tiles are [NB][TILE+1]
 
-__global__ void __launch_bounds__(kFactorThreads) k_factor(const int* __restrict__ order,
+__global__ void __launch_bounds__(kFactorThreads, 2) k_factor(const int* __restrict__ order,
                                                            const int* __restrict__ n_rows,
                                                            const std::int64_t* __restrict__ vbase,
                                                            const std::int64_t* __restrict__ ebase,
@@ -2394,6 +2394,8 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
     // device factorisation
     const int fsm = static_cast<int>(sizeof(double)) * (NB * (NB + 1) + 4 * NB * kTS);
     CPDDG_CUDA(cudaFuncSetAttribute(k_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm));
+    // two CTAs per SM (256 subdomains in one wave on 148 SMs): full shared-memory carveout
+    CPDDG_CUDA(cudaFuncSetAttribute(k_factor, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     DevBuf<int> status(static_cast<std::size_t>(n_sub));
     status.zero();
     pc->dinv.alloc(static_cast<std::size_t>(vb));

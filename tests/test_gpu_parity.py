@@ -16,7 +16,7 @@ from conftest import GOLDEN
 
 pytestmark = pytest.mark.gpu
 
-CASES = sorted(f[:-4] for f in os.listdir(GOLDEN) if f.endswith(".npz"))
+CASES = sorted(f[:-4] for f in os.listdir(GOLDEN) if f.endswith(".npz") and not f.startswith("fullsize_"))
 
 
 def _setup(name):
