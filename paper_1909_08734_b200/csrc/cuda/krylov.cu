@@ -420,7 +420,11 @@ struct Workspace {
         if (coop_grid == 0) {
             int per_sm = 0;
             CPDDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mgs_all, kRedThreads, 0));
-            coop_grid = std::max(1, std::min(per_sm, 4)) * sm_count();
+            static const int bps = [] {  // development knob: cooperative blocks per SM
+                const char* e = std::getenv("CPDDG_MGS_BPS");
+                return e ? std::max(1, std::atoi(e)) : 2;  // measured: 2 beats 4 (cheaper grid barriers)
+            }();
+            coop_grid = std::max(1, std::min(per_sm, bps)) * sm_count();
         }
         const std::size_t need = static_cast<std::size_t>(2 * coop_grid) * (m + 2);
         if (mgs_partials.size() < need) mgs_partials.alloc(std::max(need, static_cast<std::size_t>(2 * coop_grid) * 64));
