@@ -1,6 +1,10 @@
 // C ABI: host setup (include/cpddg.h, "Host setup" section).
 #include "setup.hpp"
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include <algorithm>
 #include <cstring>
 
@@ -51,9 +55,17 @@ void create_impl(const cpddg_problem_desc& d, cpddg_setup* s) {
             default: throw ConfigError("surface is not available in 3D");
         }
     }
+    const auto t0 = std::chrono::steady_clock::now();
     I->band = build_band_tube<D>(S, d.h, d.p, d.tube_radius, d.workers);
+    const auto t1 = std::chrono::steady_clock::now();
     I->E = build_extension<D>(I->band, d.workers);
+    const auto t2 = std::chrono::steady_clock::now();
     I->A = assemble_helmholtz<D>(I->band, I->E, d.c, d.workers);
+    const auto t3 = std::chrono::steady_clock::now();
+    if (std::getenv("CPDDG_VERBOSE"))
+        std::fprintf(stderr, "[cpddg] setup: band %.3f s, E %.3f s, A %.3f s\n",
+                     std::chrono::duration<double>(t1 - t0).count(), std::chrono::duration<double>(t2 - t1).count(),
+                     std::chrono::duration<double>(t3 - t2).count());
 }
 
 template <int D>
