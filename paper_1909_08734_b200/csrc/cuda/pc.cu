@@ -2251,6 +2251,15 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
     std::vector<HostSub> subs(static_cast<std::size_t>(n_sub));
     parallel_for(n_sub, opt ? opt->workers : 0,
                  [&](int j, int) { subs[static_cast<std::size_t>(j)] = analyse(locals[j], n_global); });
+    if (std::getenv("CPDDG_VERBOSE")) {
+        std::int64_t eL = 0, eU = 0;
+        for (const auto& S : subs) {
+            eL += S.ne;
+            eU += S.neU;
+        }
+        std::fprintf(stderr, "[cpddg] envelopes: L rows %lld, U columns %lld entries\n", static_cast<long long>(eL),
+                     static_cast<long long>(eU));
+    }
     // owned slots must be a disjoint cover (partition of unity, solve.hpp:62-63)
     std::vector<char> owned(static_cast<std::size_t>(n_global), 0);
     for (const auto& S : subs)
@@ -2285,15 +2294,7 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
     pc->U.alloc(static_cast<std::size_t>(std::max<std::int64_t>(ebsU, 1)));
     pc->diag.alloc(static_cast<std::size_t>(vb));
     const auto t_an = std::chrono::steady_clock::now();
-    if (std::getenv("CPDDG_VERBOSE")) {
-        std::int64_t eL = 0, eU = 0;
-        for (const auto& S : subs) {
-            eL += S.ne;
-            eU += S.neU;
-        }
-        std::fprintf(stderr, "[cpddg] envelopes: L rows %lld, U columns %lld entries\n", static_cast<long long>(eL),
-                     static_cast<long long>(eU));
-    }
+
     {
         // A_j's entries as (destination, value) pairs, scattered on the device
         std::vector<std::int64_t> pbase(static_cast<std::size_t>(n_sub) + 1, 0);
