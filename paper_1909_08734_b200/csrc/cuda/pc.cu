@@ -2494,7 +2494,7 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
         const int S = sm_count();
         // measured: two waves of ShapeMid beat one wave of ShapeSmall; the
         // record solve uses ShapeRec (shape 3) when n_sub > #SMs
-        pc->shape = n_sub <= S ? 0 : pc->blockinv ? 3 : 1;
+        pc->shape = pc->blockinv ? 3 : n_sub <= S ? 0 : 1;  // record solve: streamed (measured faster at 64 and 256 subdomains)
         if (const char* e = std::getenv("CPDDG_SOLVE_SHAPE")) {
             const std::string v(e);
             pc->shape = v == "big" ? 0 : v == "mid" ? 1 : v == "small" ? 2 : v == "rec" ? 3 : pc->shape;

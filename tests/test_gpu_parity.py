@@ -244,7 +244,7 @@ def test_dense_small_system_mode_matches_envelope_solve(monkeypatch):
     g, cfg, P, A, M, torch = _setup("circle_oras_gmres")
     monkeypatch.setenv("CPDDG_DENSE", "0")
     Me = api.SchwarzPreconditioner.from_problem(P)
-    assert M.stats()["apply_mode"] == 1 and Me.stats()["apply_mode"] == 0
+    assert M.stats()["apply_mode"] == 1 and Me.stats()["apply_mode"] in (0, 2)  # envelope: register or streamed
     x = torch.from_numpy(g["x"]).cuda()
     zd, ze = M.apply(x).cpu().numpy(), Me.apply(x).cpu().numpy()
     assert np.linalg.norm(zd - ze) <= 1e-12 * np.linalg.norm(ze)
