@@ -68,3 +68,25 @@ def test_solve_matches_reference_full_size(headline, method, alpha, ax, key):
     u = res.u.cpu().numpy()
     err = np.abs(u - inputs.exact_sphere(P.active_cp)).max()
     assert abs(err - r["err_inf_vs_exact"]) <= 1e-3 * r["err_inf_vs_exact"]
+
+
+def test_standard_oras_stagnates_like_the_reference(headline):
+    """BASELINE config 3 with the standard Robin condition (alpha_cross =
+    alpha = 4): the reference's GMRES(50) stagnates -- 2000 iterations, not
+    converged, relative residual 0.99975 (fullsize_reference.json) -- the
+    cross-point pathology that the modified condition removes.  The device
+    solve reproduces the stagnation and its level."""
+    import torch
+
+    from paper_1909_08734_b200 import api, inputs
+    P, part, ref = headline
+    r = ref["oras_a4_ax4"]
+    P.decompose(part, 3, "oras", 4.0, 4.0)
+    A = api.DeviceHelmholtz.from_problem(P)
+    M = api.SchwarzPreconditioner.from_problem(P)
+    b = inputs.rhs_sphere(P.active_cp)
+    res = api.gmres_solve(A, torch.from_numpy(b).cuda(), M, 1e-10, 2000, 50)
+    assert not res.log.converged and not r["converged"]
+    assert res.log.iterations == r["iterations"] == 2000
+    rel = res.log.final_true_residual / np.linalg.norm(b)
+    assert abs(rel - r["final_rel_residual"]) <= 1e-3
