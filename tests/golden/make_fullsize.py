@@ -7,7 +7,7 @@ build_subdomains would add hours at 512 subdomains).  Writes iteration counts,
 residuals and a strided sample of the solution into fullsize_reference.json /
 fullsize_<name>.npz.  CPU only; minutes per configuration.
 
-    python tests/golden/make_fullsize.py torus|trimesh
+    python tests/golden/make_fullsize.py torus|trimesh|torus_ras_stationary
 """
 import json
 import os
@@ -28,6 +28,9 @@ STRIDE = 997
 CONFIGS = {
     "torus": dict(surface="torus", major_radius=1.0, minor_radius=0.4, h=0.01, n_subdomains=512, n_overlap=2),
     "trimesh": dict(surface="obj", h=0.01, n_subdomains=512, n_overlap=2, subdivisions=6, mesh_seed=5),
+    # BASELINE config 4's other run: RAS as a stationary solver
+    "torus_ras_stationary": dict(surface="torus", major_radius=1.0, minor_radius=0.4, h=0.01, n_subdomains=512,
+                                 n_overlap=2, method="ras", mode="stationary"),
 }
 
 
@@ -42,11 +45,15 @@ def main(name):
                     minor_radius=w.get("minor_radius", 1 / 3))
     cp = P.active_cp
     part = inputs.rcb_partition(cp, w["n_subdomains"])
-    _, moves = P.decompose(part, w["n_overlap"], "oras", 4.0, 40.0)
+    method, mode = w.get("method", "oras"), w.get("mode", "gmres")
+    _, moves = (P.decompose(part, w["n_overlap"], "ras") if method == "ras"
+                else P.decompose(part, w["n_overlap"], "oras", 4.0, 40.0))
     b = inputs.rhs_trig(cp, seed=2024)
-    cfg = dict(surface=w["surface"], h=w["h"], p=3, c=1.0, method="oras", mode="gmres", gmres_restart=50,
-               n_overlap=w["n_overlap"], n_subdomains=w["n_subdomains"], alpha=4.0, alpha_cross=40.0,
-               rel_tol=1e-10, max_iter=2000)
+    cfg = dict(surface=w["surface"], h=w["h"], p=3, c=1.0, method=method, mode=mode, gmres_restart=50,
+               n_overlap=w["n_overlap"], n_subdomains=w["n_subdomains"], rel_tol=1e-10,
+               max_iter=2000 if mode == "gmres" else 5000)
+    if method == "oras":
+        cfg.update(alpha=4.0, alpha_cross=40.0)
     if w["surface"] == "torus":
         cfg.update(major_radius=w["major_radius"], minor_radius=w["minor_radius"])
     if obj:
@@ -59,12 +66,13 @@ def main(name):
     out = R.solve(b)
     t2 = time.time()
     u = out["u"]
-    key = f"{name}_h{w['h']}_rcb{w['n_subdomains']}_no{w['n_overlap']}_oras_a4_ax40"
+    key = f"{name.split('_')[0]}_h{w['h']}_rcb{w['n_subdomains']}_no{w['n_overlap']}_" + (
+        "oras_a4_ax40" if method == "oras" else f"{method}_{mode}")
     rec = dict(n_active=P.n_active, n_ghost=P.n_ghost, align_moves=moves, iterations=out["iterations"],
                converged=out["converged"],
                final_rel_residual=out["final_true_residual"] / float(np.linalg.norm(b)),
                u_norm2=float(np.linalg.norm(u)), u_norm_inf=float(np.abs(u).max()), sample_stride=STRIDE,
-               _how=f"tests/golden/make_fullsize.py {name}: oracle/_ref gmres_solve, {os.cpu_count()} threads, "
+               _how=f"tests/golden/make_fullsize.py {name}: oracle/_ref {mode} solve, {os.cpu_count()} threads, "
                     f"local factorisations {t1 - t0:.0f} s, solve {t2 - t1:.0f} s")
     path = os.path.join(HERE, "fullsize_reference.json")
     d = json.load(open(path))
