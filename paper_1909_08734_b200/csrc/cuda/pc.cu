@@ -40,6 +40,7 @@
 #include <string>
 #include <type_traits>
 #include <cmath>
+#include <mutex>
 #include <numeric>
 
 namespace cpddg {
@@ -2076,11 +2077,30 @@ static void launch_solve(const cpddg_pc* pc, int grid, const double* r, double* 
     CPDDG_CUDA(cudaGetLastError());
 }
 
+/** cudaFuncAttributeMaxDynamicSharedMemorySize is per kernel, not per
+ *  preconditioner: raise it to the largest request seen so far, so that a
+ *  preconditioner built earlier with larger subdomains still launches after
+ *  a smaller one was built. */
+static void raise_smem_limit(const void* kern, int bytes) {
+    static std::mutex m;
+    static std::vector<std::pair<const void*, int>> seen;
+    std::lock_guard<std::mutex> lk(m);
+    for (auto& [k, b] : seen)
+        if (k == kern) {
+            if (bytes <= b) return;
+            b = bytes;
+            CPDDG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+            return;
+        }
+    seen.emplace_back(kern, bytes);
+    CPDDG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+}
+
 template <bool UROWS, class SH, bool INV>
 static void set_solve_smem(int bytes) {
     for (auto kern : {k_solve<0, UROWS, SH, INV>, k_solve<1, UROWS, SH, INV>, k_solve<2, UROWS, SH, INV>,
                       k_solve<3, UROWS, SH, INV>})
-        CPDDG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(bytes, 1)));
+        raise_smem_limit(reinterpret_cast<const void*>(kern), std::max(bytes, 1));
 }
 
 void pc_apply_mode(const cpddg_pc* pc, const double* r, double* z, bool accumulate, int mode, cudaStream_t st) {
@@ -2241,7 +2261,7 @@ static void setup_tma(cpddg_pc* pc, const std::vector<int>& n_rows, const std::v
     pc->tma_grid = grid;
     pc->tma_smem = tmas::RING + 8 * tmas::NB * tmas::kRec + 4 * tmas::NB * tmas::kDesc + 8 * pc->max_rows;
     for (auto kern : {k_solve_tma<0>, k_solve_tma<1>, k_solve_tma<2>, k_solve_tma<3>})
-        CPDDG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pc->tma_smem));
+        raise_smem_limit(reinterpret_cast<const void*>(kern), pc->tma_smem);
     pc->tma = true;
 }
 
@@ -2673,8 +2693,8 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
             pc->dense_tiles = static_cast<int>(tsub.size());
             pc->Ainv.alloc(static_cast<std::size_t>(std::max<std::int64_t>(acc, 1)));
             if (static_cast<int>(sizeof(double)) * pc->max_rows > 48 * 1024)
-                CPDDG_CUDA(cudaFuncSetAttribute(k_solve_dense, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                static_cast<int>(sizeof(double)) * pc->max_rows));
+                raise_smem_limit(reinterpret_cast<const void*>(k_solve_dense),
+                                 static_cast<int>(sizeof(double)) * pc->max_rows);
             // column k of A_j^-1 = the envelope solve of e_k, for all subdomains at once
             DevBuf<double> er(static_cast<std::size_t>(vb)), ez(static_cast<std::size_t>(vb));
             er.zero();

@@ -343,3 +343,12 @@ def test_streamed_record_and_chain_solves_agree(monkeypatch):
     b = torch.from_numpy(inputs.rhs_sphere(P.active_cp)).cuda()
     its = [api.gmres_solve(A, b, m, 1e-10, 1000, 50).log.iterations for m in (M, Mr, Mc)]
     assert its[0] == its[1] == its[2]
+    # kernel shared-memory limits are per kernel: a preconditioner with smaller
+    # subdomains built afterwards must not break the earlier, larger one
+    monkeypatch.delenv("CPDDG_TMA")
+    monkeypatch.delenv("CPDDG_BLOCKINV")
+    Ps = api.Problem("sphere", h=0.1, p=3, c=1.0)
+    Ps.decompose(inputs.rcb_partition(Ps.active_cp, 200), 2, "oras", 4.0, 40.0)
+    Msmall = api.SchwarzPreconditioner.from_problem(Ps)
+    assert Msmall.stats()["max_rows"] < M.stats()["max_rows"]
+    assert np.array_equal(M.apply(xd).cpu().numpy(), z)
