@@ -420,10 +420,13 @@ struct Workspace {
         if (coop_grid == 0) {
             int per_sm = 0;
             CPDDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mgs_all, kRedThreads, 0));
-            static const int bps = [] {  // development knob: cooperative blocks per SM
-                const char* e = std::getenv("CPDDG_MGS_BPS");
-                return e ? std::max(1, std::atoi(e)) : 2;  // measured: 2 beats 4 (cheaper grid barriers)
-            }();
+            // cooperative blocks per SM: the fewest (>= 2) that keep the register
+            // kernel's slice at <= 8 elements per thread -- measured: 2 beats 4
+            // at the headline (cheaper grid barriers); larger systems need more
+            // blocks or they fall back to the streaming k_mgs_all
+            const long long per_block_sm = static_cast<long long>(sm_count()) * kRedThreads * 8;
+            int bps = static_cast<int>(std::max<long long>(2, (n + per_block_sm - 1) / per_block_sm));
+            if (const char* e = std::getenv("CPDDG_MGS_BPS")) bps = std::max(1, std::atoi(e));  // development knob
             coop_grid = std::max(1, std::min(per_sm, bps)) * sm_count();
         }
         const std::size_t need = static_cast<std::size_t>(2 * coop_grid) * (m + 2);
