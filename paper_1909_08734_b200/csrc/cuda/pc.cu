@@ -1580,15 +1580,19 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) k_solve(const in
 // The register-staged k_solve keeps one wave of factor loads in flight per
 // warp and waits, every block step, for the slowest of its warps' loads: a
 // latency-bound 4.6 TB/s.  k_solve_tma decouples the stream from the steps:
-// one CTA per SM walks its subdomains (byte-balanced at setup) and, per
-// subdomain, the forward then the backward record solve.  Every step is an
-// *item* -- the far rows (forward) or far columns (backward) its consumers
-// apply, its block record, its row descriptor -- that a producer warp copies
-// with cp.async.bulk into a 128 KB shared ring (item slots with an mbarrier
-// each), as far ahead as the ring allows and across pass and subdomain
-// boundaries.  Warp 0 solves the step's block from the record, 14 consumer
-// warps apply the staged item from shared memory; one named barrier per
-// step (the producer is not part of it).
+// one CTA per SM walks its subdomains (assigned longest-processing-time first
+// with a measured per-step cost model) and, per subdomain, the forward then
+// the backward record solve (blocks of RB = 8 rows).  Every step is an *item*
+// -- the far rows (forward) or far columns (backward) its consumers apply, its
+// block record, its row descriptor -- that one producer thread (warp 1,
+// item table prefetched one item ahead) copies with cp.async.bulk into a
+// 128 KB shared ring (6 item slots with an mbarrier each), as far ahead as the
+// ring allows and across pass and subdomain boundaries.  Warp 0 solves the
+// step's block from the record; 8 consumer warps apply the staged item from
+// shared memory; one named barrier per step (the producer is not part of it).
+// Measured: 2.43 ms per headline apply, DRAM traffic = algorithmic bytes; a
+// step (~1.8 k cycles) is bound by its instruction issue, not the stream
+// (K2-K4).
 namespace tmas {
 constexpr int RB = 8;                   // block rows (records built for it; ShapeRec8 is the fallback)
 constexpr int NB = 6;                   // item slots
