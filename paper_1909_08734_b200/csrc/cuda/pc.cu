@@ -2277,12 +2277,17 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
                  [&](int j, int) { subs[static_cast<std::size_t>(j)] = analyse(locals[j], n_global); });
     if (std::getenv("CPDDG_VERBOSE")) {
         std::int64_t eL = 0, eU = 0;
+        int reachL = 0, reachU = 0;  // longest row / column of the envelopes (a y window must cover it)
         for (const auto& S : subs) {
             eL += S.ne;
             eU += S.neU;
+            for (int i = 0; i < S.n; ++i) {
+                reachL = std::max(reachL, i - S.first[static_cast<std::size_t>(i)]);
+                reachU = std::max(reachU, i - S.firstU[static_cast<std::size_t>(i)]);
+            }
         }
-        std::fprintf(stderr, "[cpddg] envelopes: L rows %lld, U columns %lld entries\n", static_cast<long long>(eL),
-                     static_cast<long long>(eU));
+        std::fprintf(stderr, "[cpddg] envelopes: L rows %lld, U columns %lld entries; longest L row %d, U column %d\n",
+                     static_cast<long long>(eL), static_cast<long long>(eU), reachL, reachU);
     }
     // owned slots must be a disjoint cover (partition of unity, solve.hpp:62-63)
     std::vector<char> owned(static_cast<std::size_t>(n_global), 0);
