@@ -160,66 +160,137 @@ class ClockSampler:
 
 # ---------------------------------------------------------------- reference / CPU
 
-def cpu_reference(P, locs, b, iters_per_step: int, steps: int, warmup: int):
-    """Time the reference's own solve (oracle/_ref: the unmodified reference
-    headers; Eigen replaced by the oracle shim) on the host cores: the
-    reference build_problem, the reference DirectSolver on the local systems
-    (identical to the reference's own assemble_local output, bit for bit), and
-    bounded samples of the reference gmres_solve."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import ref
-    cores = os.cpu_count() or 1
-    w = WORKLOAD
-    cfg = dict(surface=w["surface"], h=w["h"], p=w["p"], c=w["c"], method=w["method"], mode="gmres",
-               gmres_restart=w["gmres_restart"], n_overlap=w["n_overlap"], n_subdomains=w["n_subdomains"],
-               alpha=w["alpha"], alpha_cross=w["alpha_cross"], rel_tol=w["rel_tol"])
-    if w["surface"] == "torus":
-        cfg.update(major_radius=w["major_radius"], minor_radius=w["minor_radius"])
-    if w["surface"] == "obj":
-        cfg.update(obj=P.obj_path)
-    t0 = time.perf_counter()
-    R = ref.RefProblem(cfg, workers=cores)
-    t_build = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    ref.set_locals(R, locs)
-    t_locals = time.perf_counter() - t0
-    samples = []
-    for k in range(warmup + steps):
-        r = ref.solve_capped(R, b, iters_per_step, WORKLOAD["rel_tol"])
-        if k >= warmup:
-            samples.append(r)
-    secs = sum(s["seconds"] for s in samples)
-    its = sum(s["iterations"] for s in samples)
-    value = R.n_active * its / secs
-    return dict(value=value, unit=UNIT, cores=cores, kind="reference",
-                sample=(f"{steps} x {iters_per_step} GMRES(50) iterations of the reference gmres_solve "
-                        f"(serial SpMV/MGS, preconditioner on a {cores}-thread ThreadPool) on the full "
-                        f"workload; setup untimed: build_problem {t_build:.1f}s, {len(locs)} local "
-                        f"factorisations {t_locals:.1f}s"),
-                seconds=secs, iterations=its)
+def _inputs_module():
+    """inputs.py (pure numpy: partition / rhs / mesh generators) loaded by file
+    path, so the reference arm never imports the product package."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("cpddg_inputs", os.path.join(ROOT, "paper_1909_08734_b200",
+                                                                               "inputs.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def static_config(w, n_active):
+    """The `config` dict both arms print (identical keys and values)."""
+    return {
+        "workload": workload_name(w), "N_A": n_active, "n_subdomains": w["n_subdomains"],
+        "partition": w["partition"] + " on closest points, then align_interfaces",
+        "rhs": {"sphere": "f = 13 u, u = x^3 - 3xy^2 at closest points",
+                "circle": "f = 2 sin(t) + 145 sin(12 t)",
+                "trig": "16 seeded modes sin(k.cp + phi), k in [-4,4]^3"}[w["rhs"]],
+        "tube_radius": "reference (p+1)/2 sqrt(d) h" if not w.get("tube_radius") else f"{w['tube_radius']:.6g} h",
+        "l2": "inputs larger than L2 (local factors streamed per preconditioner apply exceed the 126 MB L2)",
+        "parallelism": "replicas (one independent solve per GPU)",
+    }
+
+
+class RefArm:
+    """The reference's own pipeline from oracle/_ref (the unmodified reference
+    headers compiled against the Eigen/GTest shims) on the host cores:
+    build_problem (band, E, A), the partition file through load_partition +
+    align_interfaces, build_subdomains, assemble_local and the DirectSolver
+    factorisations on the reference ThreadPool (ref.RefProblem.decompose =
+    pipeline.hpp:186-216), then bounded samples of the reference gmres_solve.
+    Nothing of the device path is loaded: the partition and right-hand side
+    come from inputs.py (numpy) applied to the reference band's own closest
+    points."""
+
+    def __init__(self, w, workers=None):
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import numpy as np
+        import ref
+        self.ref, self.np, self.w = ref, np, w
+        self.cores = workers or os.cpu_count() or 1
+        I = _inputs_module()
+        cfg = dict(surface=w["surface"], h=w["h"], p=w["p"], c=w["c"], method=w["method"], mode="gmres",
+                   gmres_restart=w["gmres_restart"], n_overlap=w["n_overlap"], n_subdomains=w["n_subdomains"],
+                   rel_tol=w["rel_tol"], max_iter=w["max_iter"])
+        if w["method"] == "oras":
+            cfg.update(alpha=w["alpha"], alpha_cross=w["alpha_cross"] if w["alpha_cross"] > 0 else w["alpha"])
+        if w["surface"] == "torus":
+            cfg.update(major_radius=w["major_radius"], minor_radius=w["minor_radius"])
+        if w["surface"] == "obj":
+            import tempfile
+            v, f = I.displaced_icosphere(w["subdivisions"], seed=w["mesh_seed"])
+            obj = os.path.join(tempfile.mkdtemp(prefix="cpddg_ref_mesh_"), "icosphere.obj")
+            I.write_obj(obj, v, f)
+            cfg.update(obj=obj)
+        if w.get("tube_radius"):
+            raise SystemExit("the reference has no tube-radius override (proj/include/cpdd/band.hpp:157)")
+        t0 = time.perf_counter()
+        self.R = R = ref.RefProblem(cfg, workers=self.cores)
+        self.t_build = time.perf_counter() - t0
+        cp = R.band()["cp"][: R.n_active]
+        part = I.sector_partition(cp, w["n_subdomains"]) if w["partition"] == "sector" \
+            else I.rcb_partition(cp, w["n_subdomains"])
+        self.b = {"sphere": I.rhs_sphere, "circle": I.rhs_circle,
+                  "trig": lambda q: I.rhs_trig(q, seed=2024)}[w["rhs"]](cp)
+        t0 = time.perf_counter()
+        R.decompose(part)
+        self.t_decompose = time.perf_counter() - t0
+        self.n_active = R.n_active
+        # the per-call tail of a capped solve that a real solve pays only once per
+        # restart cycle: the closing preconditioner apply (u += M V y) and three
+        # operator applies (initial residual, cycle-end residual, final true residual)
+        x = I.uniform_vector(R.n_active, 3)
+        tp, ta = [], []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            R.pc_apply(x)
+            tp.append(time.perf_counter() - t0)
+            t0 = time.perf_counter()
+            R.apply_A(x)
+            ta.append(time.perf_counter() - t0)
+        self.t_tail = statistics.median(tp) + 3 * statistics.median(ta)
+
+    def sample(self, iters):
+        """One bounded sample: the first `iters` iterations of the reference
+        gmres_solve on the workload, tail-corrected.  Returns (iterations, s)."""
+        r = self.ref.solve_capped(self.R, self.b, iters, self.w["rel_tol"])
+        return r["iterations"], max(r["seconds"] - self.t_tail, 1e-9)
+
+    def describe(self, iters, steps):
+        return (f"{steps} x the first {iters} iterations of the reference gmres_solve (GMRES({self.w['gmres_restart']}), "
+                f"serial SpMV/MGS, preconditioner on a {self.cores}-thread ThreadPool) on the full workload, each "
+                f"minus the capped call's tail (1 preconditioner + 3 operator applies = {self.t_tail:.3f} s); "
+                f"setup untimed: build_problem {self.t_build:.1f} s, load_partition + align_interfaces + "
+                f"build_subdomains + assemble_local + DirectSolver {self.t_decompose:.1f} s")
+
+
+def ref_iters_for(w, cores):
+    """Iterations per reference sample: ~5 s of CPU work per step at the headline."""
+    if w["n_subdomains"] <= 8:
+        return 16
+    return max(4, min(w["gmres_restart"], int(16 * cores / 16)))
 
 
 def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    from paper_1909_08734_b200 import api, inputs
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import ref
     if not ref.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference at build time)"}))
         return 0
-    P, part, b, obj = build_problem(WORKLOAD)
-    P.obj_path = obj
-    P.decompose(part, WORKLOAD["n_overlap"], WORKLOAD["method"], WORKLOAD["alpha"], WORKLOAD["alpha_cross"])
-    locs = [P.local(j) for j in range(P.n_sub)]
-    base = cpu_reference(P, locs, b, args.ref_iters, args.steps, args.warmup)
-    line = {"metric": METRIC, "value": base["value"], "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * base["seconds"] / args.steps, "higher_is_better": True,
+    arm = RefArm(WORKLOAD)
+    m = args.ref_iters or ref_iters_for(WORKLOAD, arm.cores)
+    for _ in range(args.warmup):
+        arm.sample(1)  # warm-up: one iteration each (page-in, thread pool spin-up)
+    its, secs = 0, 0.0
+    for _ in range(args.steps):
+        i, s = arm.sample(m)
+        its += i
+        secs += s
+    value = arm.n_active * its / secs
+    desc = arm.describe(m, args.steps)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_name(), "N_A": P.n_active}, "impl": "reference",
-            "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
-            "e2e": {"value": base["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "config": static_config(WORKLOAD, arm.n_active), "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": arm.cores, "kind": "reference", "sample": desc},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0
 
@@ -233,7 +304,8 @@ def main():
                     help="timed solves (default: 3; more for the millisecond-scale configs so host jitter averages out)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ref-iters", type=int, default=4, help="GMRES iterations per reference sample step")
+    ap.add_argument("--ref-iters", type=int, default=0,
+                    help="GMRES iterations per reference sample step (default: ~5 s of host work)")
     ap.add_argument("--cpu-baseline", default="auto", choices=["auto", "off"])
     ap.add_argument("--config", default="headline", choices=sorted(CONFIGS),
                     help="workload (default: BASELINE's headline; the others are parity / scaling cases)")
@@ -347,15 +419,11 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * t_dev / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {
-            "workload": workload_name(), "N_A": n, "N_G": P.n_ghost, "n_subdomains": P.n_sub,
-            "align_moves": moves, "gmres_iterations": iters[0], "time_to_1e-10_s": t_dev / args.steps,
-            "final_true_relative_residual": final_rel, "parallelism": f"replicas x{world}",
-            "l2": "inputs larger than L2: 12+ GB of local factors streamed per preconditioner apply",
-            "rhs": {"sphere": "f = 13 u, u = x^3 - 3xy^2 at closest points",
-                    "circle": "f = 2 sin(t) + 145 sin(12 t)",
-                    "trig": "16 seeded modes sin(k.cp + phi), k in [-4,4]^3"}[WORKLOAD["rhs"]],
-            "partition": WORKLOAD["partition"] + " on closest points, then align_interfaces",
+        "config": static_config(WORKLOAD, n),
+        "details": {
+            "N_G": P.n_ghost, "align_moves": moves, "gmres_iterations": iters[0],
+            "time_to_1e-10_s": t_dev / args.steps, "final_true_relative_residual": final_rel,
+            "replicas": world,
             "setup_s": {"problem": t_problem, "decompose": t_decomp, "factor_and_upload": t_locals,
                         "device_factor": pcs["factor_seconds"], "host_analyse": pcs["analyse_seconds"]},
             "pc": {k: pcs[k] for k in ("factor_entries", "profile_entries", "factor_bytes", "n_rows_total",
@@ -365,7 +433,9 @@ def main():
             "op_roofline_GBs": op_alg / (op_s / max(op_n, 1)) / 1e9 if op_n else None,
         },
         "roofline": {"bound": "hbm", "kernel": {1: "k_solve_dense (preconditioner apply, dense small-system mode)",
-                                                 2: "k_solve_tma (preconditioner apply, TMA-streamed record solve)"}
+                                                 2: "k_solve_tma (preconditioner apply, TMA-streamed record solve)",
+                                                 3: "k_solve_win (preconditioner apply, windowed TMA-streamed record solve)",
+                                                 4: "k_solve_win (preconditioner apply, streamed record solve, y in HBM)"}
                      .get(pcs["apply_mode"], "k_solve (preconditioner apply, record solve)"), "achieved": achieved,
                      "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": ncu_traffic() if WORKLOAD is CONFIGS["headline"] else None,
@@ -379,9 +449,12 @@ def main():
             sys.path.insert(0, os.path.join(ROOT, "oracle"))
             import ref
             if ref.available():
-                locs = [P.local(j) for j in range(P.n_sub)]
-                base = cpu_reference(P, locs, b_host, args.ref_iters, 1, 0)
-                line["cpu_baseline"] = {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")}
+                arm = RefArm(WORKLOAD)
+                m = args.ref_iters or 2 * ref_iters_for(WORKLOAD, arm.cores)  # one ~10 s sample
+                arm.sample(1)
+                its, secs = arm.sample(m)
+                line["cpu_baseline"] = {"value": arm.n_active * its / secs, "unit": UNIT, "cores": arm.cores,
+                                        "kind": "reference", "sample": arm.describe(m, 1)}
             else:
                 line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                                         "sample": "unavailable: oracle/_ref not built"}

@@ -129,7 +129,7 @@ public:
                                     sl[j].data(), sg[j].data(), L.A.row_ptr().data(), L.A.col_index().data(),
                                     L.A.values().data()};
         }
-        cpddg_pc_options opt{0, 0};
+        cpddg_pc_options opt{0, 1};  // probe every local factor, like the Python path (api.py)
         cpddg_pc* h = nullptr;
         cpddg_detail::check(cpddg_pc_create(n_global, static_cast<int>(d.size()), d.data(), &opt, &h));
         pc_.reset(h);

@@ -97,6 +97,16 @@ struct cpddg_pc {
     cpddg::DevBuf<int> tma_cta_begin, tma_cta_subs, tma_desc;
     cpddg::DevBuf<std::int64_t> tma_itbase;
     cpddg::DevBuf<unsigned char> tma_items;
+    // persistent windowed streamed solve (k_solve_win, the default): per-CTA
+    // subdomain lists, per-step items, descriptors (2 RB ints per step) and the
+    // per-row buffer ybuf (R_j r in, solution out)
+    bool win = false, win_gy = false;
+    int win_rb = 16, win_grid = 0, win_smem = 0, win_wmask = 0, win_dback = 0, win_ring = 0;
+    int win_reach_l = 0, win_reach_u = 0;
+    cpddg::DevBuf<int> win_cta_begin, win_cta_subs, win_desc;
+    cpddg::DevBuf<std::int64_t> win_itbase;
+    cpddg::DevBuf<unsigned char> win_items;
+    cpddg::DevBuf<double> ybuf;
     // small systems: dense local inverses (k_solve_dense), row-major in factor order
     bool dense = false, dense_probe = false;
     int dense_tiles = 0;

@@ -1975,6 +1975,452 @@ __global__ void __launch_bounds__(tmas::kThreads, 1) k_solve_tma(const int* __re
     }
 }
 
+// ---------------------------------------------- persistent windowed streamed solve
+//
+// k_solve_win is the default preconditioner apply.  Like k_solve_tma it is
+// persistent (one CTA per SM over LPT-balanced subdomain lists) and streams
+// every step's item -- descriptor, block record and the far rows (forward) or
+// far columns (backward) of one block -- with cp.async.bulk into a shared
+// ring, one producer thread running ahead of the solve.  What changes:
+//
+//  * the local vector y lives in a circular WINDOW of W = 2^m entries in
+//    shared memory instead of whole: row i sits in slot i & (W - 1).  W covers
+//    the longest envelope row / column (+ a few blocks), 16 KB at the
+//    headline against up to 54 KB for the whole vector, so the ring grows to
+//    ~200 KB and the block is RB = 16 rows (half the sequential steps of
+//    RB = 8 for the same bytes).  Subdomain size is no longer bounded by
+//    shared memory: rows enter and leave the window as the solve moves.
+//  * R_j r and the results travel through a per-row buffer ybuf (factor
+//    order, concatenated over subdomains): a gather kernel fills it, the
+//    forward pass overwrites it with L^-1 b, the backward pass with the
+//    solution, and a scatter kernel applies Rt_j^T.  Rows enter the window
+//    from ybuf through "helper" lanes of warp 0 (lanes RB .. 2RB-1, idle
+//    during the block solve) whose loads are issued two steps before the
+//    value is stored, so no step waits on a global load: forward step k
+//    stores block k+1's right-hand side; backward step K stores the forward
+//    result of block K - D, D blocks below the lowest row any later column
+//    update touches (D RB > longest U column).
+//  * items are placed contiguously in the ring (no wrap inside an item), so
+//    the consumers index it without masking; an item larger than the ring
+//    is read by the consumers straight from HBM (header still staged).
+//
+// Step structure per block (unchanged from k_solve_tma): warp 0 forms
+// x_k = T_kk^-1 s_k - W_k x_{k-1} from the record; the 8 consumer warps
+// apply the staged far part of the NEXT block (forward: partial dots of its
+// rows, thread per column pair, fixed butterfly; backward: its columns onto
+// every row above, thread per row pair); one named barrier per step.
+// GY = true keeps y in ybuf itself (global memory, no window): the fallback
+// for windows that do not fit shared memory.
+namespace win {
+constexpr int kConsumers = 8;                     // consumer warps 1 .. 8
+constexpr int kThreads = 32 * (kConsumers + 2);   // + warp 0 (solve, helpers) + producer warp
+constexpr int kStep = kThreads - 32;              // warps 0 .. 8: named barrier 1
+constexpr int NS = 8;                             // item slots (one mbarrier each)
+constexpr int kMaxSmem = 227 * 1024;
+struct Item {
+    const double* data;  // far rows / columns of the step's data block (contiguous)
+    long long bytes;     // 0 when the step applies nothing
+    const double* rec;   // the solved block's record
+    const int* desc;     // [0, RB): f of the data block's rows / columns (INT_MAX past n);
+                         // [RB, 2 RB): their offsets in the item's data (doubles)
+};
+static_assert(sizeof(Item) == 32, "items are 32 bytes");
+template <int RB>
+struct Geo {
+    static constexpr int TS = rec_stride(RB), kRec = rec_size(RB), kDesc = 2 * RB;
+    static constexpr int kHdr = 4 * kDesc + 8 * kRec;  // staged header: descriptor, record
+    static_assert(kHdr % 128 == 0, "item data starts 128-byte aligned");
+};
+__device__ __forceinline__ void step_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kStep) : "memory"); }
+__device__ __forceinline__ double2 lds2(unsigned a) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts2(unsigned a, double2 v) {
+    asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
+}
+}  // namespace win
+
+template <int RB, int MODE, bool GY>
+__global__ void __launch_bounds__(win::kThreads, 1) k_solve_win(const int* __restrict__ cta_begin,
+                                                                const int* __restrict__ cta_subs,
+                                                                const int* __restrict__ n_rows,
+                                                                const std::int64_t* __restrict__ vbase,
+                                                                const std::int64_t* __restrict__ itbase,
+                                                                const win::Item* __restrict__ items,
+                                                                double* ybuf, int wmask, int dback, int ring_bytes,
+                                                                int dbg) {
+    using G = win::Geo<RB>;
+    constexpr int TS = G::TS, kDesc = G::kDesc, kHdr = G::kHdr, NS = win::NS, kC = win::kConsumers;
+    using tmas::smem_u32;
+    using tmas::mbar_wait;
+    using tmas::bulk_copy;
+    using win::step_bar;
+    using win::lds2;
+    using win::sts2;
+    static_assert(RB == 8 || RB == 16, "butterfly below reduces 8 or 16 rows");
+    extern __shared__ __align__(128) unsigned char smem[];
+    unsigned char* ring = smem;
+    __shared__ __align__(8) unsigned long long mbar[NS];
+    __shared__ unsigned long long prod_start[NS];
+    __shared__ int item_pos[NS];
+    __shared__ const double* item_g[NS];
+    __shared__ volatile int done;  // steps completed (thread 0, after the step barrier)
+    __shared__ double red[2][kC][RB];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int s0 = cta_begin[blockIdx.x], s1 = cta_begin[blockIdx.x + 1];
+    constexpr bool kFwd = MODE != 2, kBwd = MODE != 1;
+    if (tid == 0) {
+        for (int q = 0; q < NS; ++q) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar[q])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        done = 0;
+    }
+    __syncthreads();
+
+    if (warp == kC + 1) {
+        // ---------------- producer (one thread): every step's item in step order
+        if (lane != 0) return;
+        const unsigned long long RING = static_cast<unsigned long long>(ring_bytes);
+        unsigned long long head = 0;  // virtual ring position (bytes)
+        int t = 0;
+        int si = s0, pass = kFwd ? 0 : 1, q = 0;
+        int nblk = si < s1 ? (n_rows[cta_subs[si]] + RB - 1) / RB : 0;
+        auto item_at = [&](int s, int ps, int qq) -> const win::Item* {
+            const int j = cta_subs[s];
+            const int nb = (n_rows[j] + RB - 1) / RB;
+            return items + itbase[j] + static_cast<std::int64_t>(ps) * nb + qq;
+        };
+        auto advance = [&]() {
+            if (++q < nblk) return;
+            q = 0;
+            if (pass == 0 && kBwd) {
+                pass = 1;
+                return;
+            }
+            pass = kFwd ? 0 : 1;
+            if (++si < s1) nblk = (n_rows[cta_subs[si]] + RB - 1) / RB;
+        };
+        win::Item cur{};
+        if (si < s1) cur = *item_at(si, pass, q);
+        while (si < s1) {
+            advance();
+            win::Item nxt{};
+            if (si < s1) nxt = *item_at(si, pass, q);  // in flight while this item is issued
+            const int slot = t % NS;
+            const bool big = kHdr + cur.bytes > ring_bytes;  // data read from HBM by the consumers
+            const unsigned long long need = (kHdr + (big ? 0 : cur.bytes) + 127) & ~127ULL;
+            unsigned long long start = head;
+            if (start % RING + need > RING) start += RING - start % RING;  // items never wrap
+            while (done < t - NS + 1) __nanosleep(64);                       // slot's previous item consumed
+            for (;;) {                                                       // ring space
+                const int d = done;
+                const unsigned long long freed = d >= t ? start : prod_start[d % NS];
+                if (start + need - freed <= RING) break;
+                __nanosleep(64);
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            prod_start[slot] = start;
+            const unsigned off = static_cast<unsigned>(start % RING);
+            item_pos[slot] = static_cast<int>(off);
+            item_g[slot] = big ? cur.data : nullptr;
+            const unsigned bar = smem_u32(&mbar[slot]);
+            const unsigned tx = static_cast<unsigned>(kHdr + (big ? 0 : cur.bytes));
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(tx) : "memory");
+            bulk_copy(smem_u32(ring + off), cur.desc, 4u * kDesc, bar);
+            bulk_copy(smem_u32(ring + off + 4 * kDesc), cur.rec, 8u * G::kRec, bar);
+            if (!big && cur.bytes > 0)
+                bulk_copy(smem_u32(ring + off + kHdr), cur.data, static_cast<unsigned>(cur.bytes), bar);
+            head = start + need;
+            cur = nxt;
+            ++t;
+        }
+        return;
+    }
+
+    // ---------------- warp 0 (block solves + helper lanes) and consumer warps 1 .. kC
+    double* ywin = reinterpret_cast<double*>(smem + ring_bytes);
+    const unsigned ywin_u = smem_u32(ywin);
+    const unsigned ring_u = smem_u32(ring);
+    const int cw = warp - 1;   // consumer warp 0 .. kC-1
+    const int ct = tid - 32;   // consumer thread 0 .. 32 kC - 1
+    const bool helper = warp == 0 && lane >= RB && lane < 2 * RB;
+    const int h = lane - RB;   // helper row within a block
+    const int li = lane & (RB - 1);  // warp 0: the block row this lane solves (lanes >= RB mirror, unused)
+    int t = 0;
+    double hv0 = 0.0, hv1 = 0.0;  // helper registers: hv[b & 1] holds block b's entering value
+    for (int si = s0; si < s1; ++si) {
+        const int j = cta_subs[si];
+        const int n = n_rows[j];
+        const int nblk = (n + RB - 1) / RB;
+        double* yb = ybuf + vbase[j];
+        double* y = GY ? yb : ywin;
+        const int wm = GY ? -1 : wmask;
+        // y of a row (rows past n read 0: the window holds zeros there, ybuf the next subdomain)
+        auto yv = [&](int row) -> double { return GY && row >= n ? 0.0 : y[row & wm]; };
+        // y of the row pair (row, row + 1), row even
+        auto y2 = [&](int row) -> double2 {
+            if constexpr (GY)
+                return make_double2(y[row], y[row + 1]);
+            else
+                return lds2(ywin_u + 8u * static_cast<unsigned>(row & wm));
+        };
+        auto ldblk = [&](int b) -> double {  // row b RB + h of ybuf (0 past the ends)
+            const int row = b * RB + h;
+            return b >= 0 && row < n ? yb[row] : 0.0;
+        };
+        if constexpr (kFwd) {
+            if (!GY && helper) {
+                ywin[h & wm] = ldblk(0);
+                hv1 = ldblk(1);
+                hv0 = ldblk(2);
+            }
+            if (warp == 0) __syncwarp();
+            for (int k = 0; k < nblk; ++k, ++t) {
+                const int slot = t % NS;
+                mbar_wait(smem_u32(&mbar[slot]), static_cast<unsigned>((t / NS) & 1));
+                const int hoff = item_pos[slot];
+                const int r0 = k * RB;
+                if (dbg & 1) {
+                    // timing experiment: stream only
+                } else if (warp == 0) {
+                    // x_k = T_kk^-1 (y_k - partial dots) - W_k x_{k-1}
+                    const double* R = reinterpret_cast<const double*>(ring + hoff + 4 * kDesc) + li * TS;
+                    const int i = r0 + li;
+                    double pk = 0.0;
+                    if (k > 0) {
+#pragma unroll
+                        for (int w = 0; w < kC; ++w) pk += red[k & 1][w][li];
+                    }
+                    const double tv = yv(i) - pk;
+                    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+                    for (int c = 0; c < RB; c += 2) {
+                        a2 = fma(R[RB + c], __shfl_sync(0xffffffffu, tv, c), a2);
+                        a3 = fma(R[RB + c + 1], __shfl_sync(0xffffffffu, tv, c + 1), a3);
+                    }
+                    if (k > 0) {
+#pragma unroll
+                        for (int c = 0; c < RB; c += 2) {
+                            const double2 xp = y2(r0 - RB + c);
+                            a0 = fma(R[c], xp.x, a0);
+                            a1 = fma(R[c + 1], xp.y, a1);
+                        }
+                    }
+                    const double x = i < n ? (a2 + a3) - (a0 + a1) : 0.0;
+                    if (lane < RB) {
+                        if (!GY || i < n) y[i & wm] = x;
+                        if (!GY && i < n) yb[i] = x;
+                    } else if (!GY && helper) {
+                        // block k+1's right-hand side into the window; block k+3's load
+                        const int b = k + 1;
+                        if (b & 1) {
+                            if (b < nblk) ywin[(b * RB + h) & wm] = hv1;
+                            hv1 = ldblk(k + 3);
+                        } else {
+                            if (b < nblk) ywin[(b * RB + h) & wm] = hv0;
+                            hv0 = ldblk(k + 3);
+                        }
+                    }
+                } else if (k + 1 < nblk) {
+                    // partial dots of block k+1's rows over columns [f_r, k RB) of the staged
+                    // far rows: thread per column pair, y read once for all RB rows
+                    const int* D = reinterpret_cast<const int*>(ring + hoff);
+                    const int lim = r0;
+                    int fr[RB], orr[RB];
+                    int fmin = lim;
+#pragma unroll
+                    for (int q = 0; q < RB; q += 4) {
+                        const int4 f4 = *reinterpret_cast<const int4*>(D + q);
+                        const int4 o4 = *reinterpret_cast<const int4*>(D + RB + q);
+                        fr[q] = f4.x, fr[q + 1] = f4.y, fr[q + 2] = f4.z, fr[q + 3] = f4.w;
+                        orr[q] = o4.x - f4.x, orr[q + 1] = o4.y - f4.y;
+                        orr[q + 2] = o4.z - f4.z, orr[q + 3] = o4.w - f4.w;
+                    }
+#pragma unroll
+                    for (int q = 0; q < RB; ++q) fmin = min(fmin, fr[q]);
+                    double acc[RB];
+#pragma unroll
+                    for (int q = 0; q < RB; ++q) acc[q] = 0.0;
+                    auto dots = [&](auto load) {
+                        for (int c = (fmin & ~1) + 2 * ct; c < lim; c += 64 * kC) {
+                            const double2 yy = y2(c);
+#pragma unroll
+                            for (int q = 0; q < RB; ++q) {
+                                if (c >= fr[q]) {
+                                    const double2 v = load(orr[q] + c);
+                                    acc[q] = fma(v.x, yy.x, acc[q]);
+                                    acc[q] = fma(v.y, yy.y, acc[q]);
+                                }
+                            }
+                        }
+                    };
+                    if (const double* g = item_g[slot])
+                        dots([&](int e) { return ld_stream(reinterpret_cast<const double2*>(g + e)); });
+                    else {
+                        const unsigned db = ring_u + static_cast<unsigned>(hoff + kHdr);
+                        dots([&](int e) { return lds2(db + 8u * static_cast<unsigned>(e)); });
+                    }
+                    // RB values over 32 lanes: halve the set at xor 16, 8, ... (the lane
+                    // bit keeps the upper half), then plain adds; fixed order, so the
+                    // result is bitwise reproducible
+#pragma unroll
+                    for (int s = 0; s < 5; ++s) {
+                        const int o = 16 >> s;
+                        const int half = RB >> (s + 1);
+                        if (half >= 1) {
+                            const bool hi = lane & o;
+#pragma unroll
+                            for (int q = 0; q < half; ++q) {
+                                const double send = hi ? acc[q] : acc[q + half];
+                                const double keep = hi ? acc[q + half] : acc[q];
+                                acc[q] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+                            }
+                        } else {
+                            acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], o);
+                        }
+                    }
+                    // row = lane bits 4, 3, ... (most significant first): (lane >> kSel) & (RB - 1)
+                    constexpr int kSel = RB == 16 ? 1 : 2;
+                    if ((lane & ((1 << kSel) - 1)) == 0) red[(k + 1) & 1][cw][(lane >> kSel) & (RB - 1)] = acc[0];
+                }
+                step_bar();
+                if (tid == 0) done = t + 1;
+            }
+        }
+        if constexpr (kBwd) {
+            // window: the last D + 2 blocks (the forward results, 0 past n)
+            if (!GY) {
+                const int lo = max(0, (nblk - 2 - dback) * RB);
+                for (int row = lo + (warp == 0 ? lane : 32 + ct); row < nblk * RB; row += win::kStep)
+                    ywin[row & wm] = row < n ? yb[row] : 0.0;
+                if (helper) {
+                    const int e = nblk - 1 - dback;
+                    if (e & 1) {
+                        hv1 = ldblk(e);
+                        hv0 = ldblk(e - 1);
+                    } else {
+                        hv0 = ldblk(e);
+                        hv1 = ldblk(e - 1);
+                    }
+                }
+                step_bar();
+            }
+            for (int K = nblk - 1; K >= 0; --K, ++t) {
+                const int slot = t % NS;
+                mbar_wait(smem_u32(&mbar[slot]), static_cast<unsigned>((t / NS) & 1));
+                const int hoff = item_pos[slot];
+                const int r0 = K * RB;
+                if (dbg & 1) {
+                } else if (warp == 0) {
+                    // x_K = U_KK^-1 y_K - W_K x_{K+1}
+                    const double* R = reinterpret_cast<const double*>(ring + hoff + 4 * kDesc) + li * TS;
+                    const int i = r0 + li;
+                    const double tv = yv(i);
+                    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+                    for (int c = 0; c < RB; c += 2) {
+                        a2 = fma(R[RB + c], __shfl_sync(0xffffffffu, tv, c), a2);
+                        a3 = fma(R[RB + c + 1], __shfl_sync(0xffffffffu, tv, c + 1), a3);
+                    }
+                    if (K + 1 < nblk) {
+#pragma unroll
+                        for (int c = 0; c < RB; c += 2) {
+                            a0 = fma(R[c], yv(r0 + RB + c), a0);
+                            a1 = fma(R[c + 1], yv(r0 + RB + c + 1), a1);
+                        }
+                    }
+                    const double x = i < n ? (a2 + a3) - (a0 + a1) : 0.0;
+                    if (lane < RB) {
+                        if (!GY || i < n) y[i & wm] = x;
+                        if (!GY && i < n) yb[i] = x;
+                    } else if (!GY && helper) {
+                        const int e = K - dback;  // entering block (forward result)
+                        if (e >= 0) {
+                            if (e & 1) {
+                                ywin[(e * RB + h) & wm] = hv1;
+                                hv1 = ldblk(e - 2);
+                            } else {
+                                ywin[(e * RB + h) & wm] = hv0;
+                                hv0 = ldblk(e - 2);
+                            }
+                        }
+                    }
+                } else if (K + 1 < nblk) {
+                    // block K+1's far columns onto rows [jmin, K RB): thread per row pair
+                    const int* D = reinterpret_cast<const int*>(ring + hoff);
+                    const int c0 = r0 + RB;
+                    int fc[RB], oc[RB];
+                    double xc[RB];
+                    int jmin = r0;
+#pragma unroll
+                    for (int c = 0; c < RB; c += 4) {
+                        const int4 f4 = *reinterpret_cast<const int4*>(D + c);
+                        const int4 o4 = *reinterpret_cast<const int4*>(D + RB + c);
+                        fc[c] = f4.x, fc[c + 1] = f4.y, fc[c + 2] = f4.z, fc[c + 3] = f4.w;
+                        oc[c] = o4.x - f4.x, oc[c + 1] = o4.y - f4.y, oc[c + 2] = o4.z - f4.z, oc[c + 3] = o4.w - f4.w;
+                    }
+#pragma unroll
+                    for (int c = 0; c < RB; ++c) jmin = fc[c] < r0 ? min(jmin, fc[c]) : jmin;
+#pragma unroll
+                    for (int c = 0; c < RB; ++c) xc[c] = yv(c0 + c);  // x of block K+1 (0 past n)
+                    auto update = [&](auto load) {
+                        for (int row = (jmin & ~1) + 2 * ct; row < r0; row += 64 * kC) {
+                            double q0 = 0.0, q1 = 0.0;
+#pragma unroll
+                            for (int c = 0; c < RB; ++c) {
+                                if (row >= fc[c]) {
+                                    const double2 v = load(oc[c] + row);
+                                    q0 = fma(v.x, xc[c], q0);
+                                    q1 = fma(v.y, xc[c], q1);
+                                }
+                            }
+                            if constexpr (GY) {
+                                y[row] -= q0;
+                                y[row + 1] -= q1;
+                            } else {
+                                const unsigned a = ywin_u + 8u * static_cast<unsigned>(row & wm);
+                                double2 yy = lds2(a);
+                                yy.x -= q0;
+                                yy.y -= q1;
+                                sts2(a, yy);
+                            }
+                        }
+                    };
+                    if (const double* g = item_g[slot])
+                        update([&](int e) { return ld_stream(reinterpret_cast<const double2*>(g + e)); });
+                    else {
+                        const unsigned db = ring_u + static_cast<unsigned>(hoff + kHdr);
+                        update([&](int e) { return lds2(db + 8u * static_cast<unsigned>(e)); });
+                    }
+                }
+                step_bar();
+                if (tid == 0) done = t + 1;
+            }
+        }
+    }
+}
+
+/** ybuf[p] = r[gidx[p]] (0 for rows outside the overlap: Dirichlet closures). */
+__global__ void k_win_gather(std::int64_t rows, const int* __restrict__ gidx, const double* __restrict__ r,
+                             double* __restrict__ ybuf) {
+    for (std::int64_t p = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; p < rows;
+         p += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const int g = gidx[p];
+        ybuf[p] = g >= 0 ? __ldg(r + g) : 0.0;
+    }
+}
+
+/** z[sidx[p]] (+)= ybuf[p] over the owned rows (Rt_j^T; disjoint writes). */
+__global__ void k_win_scatter(std::int64_t rows, const int* __restrict__ sidx, const double* __restrict__ ybuf,
+                              double* __restrict__ z, int accumulate) {
+    for (std::int64_t p = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; p < rows;
+         p += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const int s = sidx[p];
+        if (s >= 0) z[s] = accumulate ? z[s] + ybuf[p] : ybuf[p];
+    }
+}
+
 // ------------------------------------------------------ small systems: dense inverses
 //
 // For a handful of small subdomains (BASELINE config 1: 8 systems of ~400
@@ -2126,6 +2572,36 @@ void pc_apply_mode(const cpddg_pc* pc, const double* r, double* z, bool accumula
         CPDDG_CUDA(cudaGetLastError());
         return;
     }
+    if (pc->win) {
+        const int rb = pc->win_rb;
+        const std::int64_t rows = pc->rows_total;
+        const int gblocks = static_cast<int>(std::min<std::int64_t>((rows + 255) / 256, 8LL * sm_count()));
+        double* yb = pc->ybuf.get();
+        if (mode == 3) {  // probe / unit solves: r and z are already per-row (factor order)
+            CPDDG_CUDA(cudaMemcpyAsync(z, r, sizeof(double) * static_cast<std::size_t>(rows), cudaMemcpyDeviceToDevice, st));
+            yb = z;
+        } else {
+            k_win_gather<<<gblocks, 256, 0, st>>>(rows, pc->gidx.get(), r, yb);
+        }
+        const int m = mode == 3 ? 0 : mode;
+        auto pick = [&](auto rbc) {
+            constexpr int RB = decltype(rbc)::value;
+            if (pc->win_gy)
+                return m == 1 ? k_solve_win<RB, 1, true> : m == 2 ? k_solve_win<RB, 2, true> : k_solve_win<RB, 0, true>;
+            return m == 1 ? k_solve_win<RB, 1, false> : m == 2 ? k_solve_win<RB, 2, false> : k_solve_win<RB, 0, false>;
+        };
+        auto kern = rb == 8 ? pick(std::integral_constant<int, 8>{}) : pick(std::integral_constant<int, 16>{});
+        kern<<<pc->win_grid, win::kThreads, pc->win_smem, st>>>(
+            pc->win_cta_begin.get(), pc->win_cta_subs.get(), pc->n_rows.get(), pc->vbase.get(), pc->win_itbase.get(),
+            reinterpret_cast<const win::Item*>(pc->win_items.get()), yb, pc->win_wmask, pc->win_dback, pc->win_ring,
+            dbg);
+        CPDDG_CUDA(cudaGetLastError());
+        if (mode != 3) {
+            k_win_scatter<<<gblocks, 256, 0, st>>>(rows, pc->sidx.get(), yb, z, accumulate ? 1 : 0);
+            CPDDG_CUDA(cudaGetLastError());
+        }
+        return;
+    }
     if (pc->tma) {
         auto kern = mode == 1 ? k_solve_tma<1> : mode == 2 ? k_solve_tma<2> : mode == 3 ? k_solve_tma<3> : k_solve_tma<0>;
         kern<<<pc->tma_grid, tmas::kThreads, pc->tma_smem, st>>>(
@@ -2269,6 +2745,137 @@ static void setup_tma(cpddg_pc* pc, const std::vector<int>& n_rows, const std::v
     pc->tma = true;
 }
 
+/** Items, descriptors, per-CTA subdomain lists, window and ring geometry of
+ *  k_solve_win (see there) for blocks of RB rows.  Returns false (path left
+ *  off) only if not even the global-memory variant fits. */
+template <int RB>
+static bool setup_win(cpddg_pc* pc, const std::vector<int>& n_rows, const std::vector<std::int64_t>& vbase,
+                      const std::vector<int>& fL, const std::vector<int>& fU, const std::vector<std::int64_t>& rocL,
+                      const std::vector<std::int64_t>& cbL, const std::vector<std::int64_t>& rocU,
+                      const std::vector<std::int64_t>& cbU, const std::vector<std::int64_t>& rbase) {
+    using G = win::Geo<RB>;
+    constexpr int kDesc = G::kDesc;
+    const int n_sub = pc->n_sub;
+    // window: the longest far row (forward) and column (backward) plus the
+    // blocks in flight; D blocks of entering lookahead below the backward front
+    int reachL = 0, reachU = 0;
+    for (int j = 0; j < n_sub; ++j)
+        for (int i = 0; i < n_rows[static_cast<std::size_t>(j)]; ++i) {
+            const std::size_t g = static_cast<std::size_t>(vbase[static_cast<std::size_t>(j)] + i);
+            reachL = std::max(reachL, i - fL[g]);
+            reachU = std::max(reachU, i - fU[g]);
+        }
+    const int dback = (reachU + RB - 1) / RB + 1;
+    int W = 4 * RB;
+    while (W < reachL + 2 * RB || W < (dback + 3) * RB) W *= 2;
+    if (const char* e = std::getenv("CPDDG_WIN_W")) W = std::max(W, std::atoi(e));  // development: larger windows
+    const int kStatic = 4096;  // static shared memory of the kernel (mbarriers, slots, partial dots)
+    const int avail = (win::kMaxSmem - kStatic) & ~127;
+    bool gy = 8 * W > avail - 64 * 1024;  // keep at least a 64 KB ring, else y stays in ybuf
+    if (const char* e = std::getenv("CPDDG_WIN_GY")) gy = gy || std::string(e) == "1";
+    int ring = gy ? avail : (avail - 8 * W) & ~127;
+    if (const char* e = std::getenv("CPDDG_WIN_RING")) ring = std::min(ring, std::atoi(e) & ~127);
+    if (ring < 2 * G::kHdr) return false;
+
+    std::vector<std::int64_t> itbase(static_cast<std::size_t>(n_sub)), cost(static_cast<std::size_t>(n_sub), 0);
+    std::int64_t n_items = 0;
+    for (int j = 0; j < n_sub; ++j) {
+        itbase[static_cast<std::size_t>(j)] = n_items;
+        n_items += 2 * ((n_rows[static_cast<std::size_t>(j)] + RB - 1) / RB);
+    }
+    std::vector<win::Item> items(static_cast<std::size_t>(n_items));
+    std::vector<int> desc(static_cast<std::size_t>(n_items) * kDesc, INT_MAX);
+    DevBuf<int> ddesc(desc.size());
+    long long n_big = 0, max_bytes = 0;
+    // step cost model for the LPT assignment (cycles; CPDDG_WIN_COST="c0,c1" per step and per KB)
+    long long c0 = 2000, c1 = 30;
+    if (const char* e = std::getenv("CPDDG_WIN_COST")) std::sscanf(e, "%lld,%lld", &c0, &c1);
+    for (int j = 0; j < n_sub; ++j) {
+        const int n = n_rows[static_cast<std::size_t>(j)];
+        const int nblk = (n + RB - 1) / RB;
+        const std::int64_t v0 = vbase[static_cast<std::size_t>(j)];
+        for (int pass = 0; pass < 2; ++pass) {
+            const std::vector<int>& f = pass ? fU : fL;
+            const std::vector<std::int64_t>& roc = pass ? rocU : rocL;
+            const double* V = (pass ? pc->U.get() : pc->L.get()) + (pass ? cbU : cbL)[static_cast<std::size_t>(j)];
+            const double* rec = (pass ? pc->recU.get() : pc->recL.get()) + rbase[static_cast<std::size_t>(j)];
+            for (int q = 0; q < nblk; ++q) {
+                const int k = pass ? nblk - 1 - q : q;  // the block solved at this step
+                const int B = k + 1;                    // the block whose far part the step applies
+                const std::int64_t it = itbase[static_cast<std::size_t>(j)] + static_cast<std::int64_t>(pass) * nblk + q;
+                win::Item& I = items[static_cast<std::size_t>(it)];
+                I.rec = rec + static_cast<std::int64_t>(k) * rec_pitch(RB);
+                I.desc = ddesc.get() + it * kDesc;
+                I.data = V;
+                I.bytes = 0;
+                for (int c = 0; c < RB; ++c) desc[static_cast<std::size_t>(it * kDesc + RB + c)] = 0;
+                if (B < nblk) {
+                    const int lim = (B - 1) * RB;
+                    long long len = 0;
+                    for (int c = 0; c < RB && B * RB + c < n; ++c) {
+                        const int fc = f[static_cast<std::size_t>(v0 + B * RB + c)];
+                        desc[static_cast<std::size_t>(it * kDesc + c)] = fc;
+                        desc[static_cast<std::size_t>(it * kDesc + RB + c)] = static_cast<int>(len);
+                        len += std::max(0, lim - fc);
+                    }
+                    I.data = V + roc[static_cast<std::size_t>(v0 + B * RB)];
+                    I.bytes = 8 * len;
+                    max_bytes = std::max(max_bytes, I.bytes);
+                    n_big += G::kHdr + I.bytes > ring ? 1 : 0;
+                }
+                cost[static_cast<std::size_t>(j)] += c0 * 1024 + c1 * (G::kHdr + I.bytes);
+            }
+        }
+    }
+    if (std::getenv("CPDDG_VERBOSE")) {
+        std::vector<long long> sz;
+        for (const auto& I : items) sz.push_back(I.bytes);
+        std::sort(sz.begin(), sz.end());
+        std::fprintf(stderr, "[cpddg] win RB %d: items %zu, p50 %lld p99 %lld max %lld bytes, %lld from HBM (ring %d B); "
+                     "window %d rows (%s), reach L %d U %d, lookahead %d blocks\n",
+                     RB, sz.size(), sz[sz.size() / 2], sz[sz.size() * 99 / 100], sz.back(), n_big, ring, W,
+                     gy ? "global" : "shared", reachL, reachU, dback);
+    }
+    const int grid = std::min(sm_count(), n_sub);
+    std::vector<int> by_cost(static_cast<std::size_t>(n_sub));
+    std::iota(by_cost.begin(), by_cost.end(), 0);
+    std::stable_sort(by_cost.begin(), by_cost.end(),
+                     [&](int a, int b) { return cost[static_cast<std::size_t>(a)] > cost[static_cast<std::size_t>(b)]; });
+    std::vector<std::int64_t> load(static_cast<std::size_t>(grid), 0);
+    std::vector<std::vector<int>> lists(static_cast<std::size_t>(grid));
+    for (int j : by_cost) {
+        const auto m = std::min_element(load.begin(), load.end()) - load.begin();
+        lists[static_cast<std::size_t>(m)].push_back(j);
+        load[static_cast<std::size_t>(m)] += cost[static_cast<std::size_t>(j)];
+    }
+    std::vector<int> begin{0}, subs;
+    for (const auto& L : lists) {
+        subs.insert(subs.end(), L.begin(), L.end());
+        begin.push_back(static_cast<int>(subs.size()));
+    }
+    CPDDG_CUDA(cudaMemcpy(ddesc.get(), desc.data(), desc.size() * sizeof(int), cudaMemcpyHostToDevice));
+    pc->win_desc = std::move(ddesc);
+    pc->win_items.alloc(items.size() * sizeof(win::Item));
+    CPDDG_CUDA(cudaMemcpy(pc->win_items.get(), items.data(), items.size() * sizeof(win::Item), cudaMemcpyHostToDevice));
+    pc->win_itbase.upload(itbase);
+    pc->win_cta_begin.upload(begin);
+    pc->win_cta_subs.upload(subs);
+    pc->win_grid = grid;
+    pc->win_gy = gy;
+    pc->win_wmask = W - 1;
+    pc->win_dback = dback;
+    pc->win_ring = ring;
+    pc->win_smem = ring + (gy ? 0 : 8 * W);
+    pc->win_reach_l = reachL;
+    pc->win_reach_u = reachU;
+    pc->ybuf.alloc(static_cast<std::size_t>(std::max<std::int64_t>(pc->rows_total, 1)));
+    for (auto kern : {k_solve_win<RB, 0, false>, k_solve_win<RB, 1, false>, k_solve_win<RB, 2, false>,
+                      k_solve_win<RB, 0, true>, k_solve_win<RB, 1, true>, k_solve_win<RB, 2, true>})
+        raise_smem_limit(reinterpret_cast<const void*>(kern), pc->win_smem);
+    pc->win = true;
+    return true;
+}
+
 static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* locals, const cpddg_pc_options* opt) {
     if (n_global <= 0 || n_sub <= 0 || !locals) throw InternalError("empty preconditioner");
     const auto t0 = std::chrono::steady_clock::now();
@@ -2337,7 +2944,13 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
         CPDDG_CUDA(cudaMemset(pc->L.get(), 0, sizeof(double) * static_cast<std::size_t>(std::max<std::int64_t>(ebs, 1))));
         CPDDG_CUDA(cudaMemset(pc->U.get(), 0, sizeof(double) * static_cast<std::size_t>(std::max<std::int64_t>(ebsU, 1))));
         CPDDG_CUDA(cudaMemset(pc->diag.get(), 0, sizeof(double) * static_cast<std::size_t>(vb)));
+        // the workers copy on the caller's device (a new host thread starts on
+        // device 0); the legacy default stream orders those copies before
+        // k_scatter_pairs, and the synchronize below makes it explicit
+        int dev = 0;
+        CPDDG_CUDA(cudaGetDevice(&dev));
         parallel_for(n_sub, opt ? opt->workers : 0, [&](int j, int) {
+            CPDDG_CUDA(cudaSetDevice(dev));
             const HostSub& S = subs[static_cast<std::size_t>(j)];
             const std::int64_t room = pbase[static_cast<std::size_t>(j) + 1] - pbase[static_cast<std::size_t>(j)];
             std::vector<std::int64_t> dst(static_cast<std::size_t>(room));
@@ -2361,6 +2974,7 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
                 CPDDG_CUDA(cudaMemset(pval.get() + o, 0, sizeof(double) * static_cast<std::size_t>(rest)));
             }
         }
+        CPDDG_CUDA(cudaDeviceSynchronize());
         const int blocks = 4 * sm_count();
         k_scatter_pairs<<<blocks, 256>>>(pbase.back(), pdst.get(), pval.get(), pc->L.get(), pc->U.get(),
                                          pc->diag.get());
@@ -2506,18 +3120,29 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
     pc->profile_entries = ebs + ebsU + vb;
     pc->solve_smem = static_cast<int>(sizeof(double)) * pc->max_rows;
     if (const char* e = std::getenv("CPDDG_BWD_PREFETCH")) pc->bwd_prefetch = std::atoi(e);
-    if (pc->solve_smem > 200 * 1024) throw ConfigError("subdomain system too large for the shared-memory solve");
-    set_solve_smem<false, ShapeMid, false>(pc->solve_smem);
-    set_solve_smem<true, ShapeBig, false>(pc->solve_smem);
-    set_solve_smem<true, ShapeMid, false>(pc->solve_smem);
-    set_solve_smem<true, ShapeSmall, false>(pc->solve_smem);
-    set_solve_smem<true, ShapeBig, true>(pc->solve_smem);
-    set_solve_smem<true, ShapeMid, true>(pc->solve_smem);
-    set_solve_smem<true, ShapeRec, true>(pc->solve_smem);
-    set_solve_smem<false, ShapeBig, true>(pc->solve_smem);
-    set_solve_smem<false, ShapeMid, true>(pc->solve_smem);
-    set_solve_smem<false, ShapeRec, true>(pc->solve_smem);
-    set_solve_smem<false, ShapeRec8, true>(pc->solve_smem);
+    // solve path: CPDDG_SOLVE=win (default; windowed streamed solve, any
+    // subdomain size), tma (k_solve_tma, whole y in shared memory) or reg
+    // (register-staged k_solve); the last two need y in shared memory
+    const std::string solve_path = [] {
+        const char* e = std::getenv("CPDDG_SOLVE");
+        const char* t = std::getenv("CPDDG_TMA");  // round-1 switch: CPDDG_TMA=0 = register-staged
+        return e ? std::string(e) : (t && std::string(t) == "0") ? std::string("reg") : std::string("win");
+    }();
+    const bool smem_y = pc->solve_smem <= 200 * 1024;
+    if (solve_path != "win" && !smem_y)
+        throw ConfigError("subdomain system too large for the shared-memory solve (CPDDG_SOLVE=" + solve_path + ")");
+    const int solve_smem_set = std::min(pc->solve_smem, 200 * 1024);
+    set_solve_smem<false, ShapeMid, false>(solve_smem_set);
+    set_solve_smem<true, ShapeBig, false>(solve_smem_set);
+    set_solve_smem<true, ShapeMid, false>(solve_smem_set);
+    set_solve_smem<true, ShapeSmall, false>(solve_smem_set);
+    set_solve_smem<true, ShapeBig, true>(solve_smem_set);
+    set_solve_smem<true, ShapeMid, true>(solve_smem_set);
+    set_solve_smem<true, ShapeRec, true>(solve_smem_set);
+    set_solve_smem<false, ShapeBig, true>(solve_smem_set);
+    set_solve_smem<false, ShapeMid, true>(solve_smem_set);
+    set_solve_smem<false, ShapeRec, true>(solve_smem_set);
+    set_solve_smem<false, ShapeRec8, true>(solve_smem_set);
     // block shape: one CTA per subdomain, all resident in one wave
     {
         const int S = sm_count();
@@ -2532,16 +3157,21 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
     // record solve: block records from the full rows, then the rows compacted
     // to their far parts (CPDDG_BLOCKINV=0 keeps the substitution-chain solve)
     // persistent TMA-streamed solve (k_solve_tma): U by columns, records for tmas::RB
-    bool want_tma = false;
+    bool want_tma = false, want_win = false;
     {
-        const char* te = std::getenv("CPDDG_TMA");
         const int tma_smem = tmas::RING + 8 * tmas::NB * tmas::kRec + 4 * tmas::NB * tmas::kDesc + 8 * pc->max_rows;
-        want_tma = pc->blockinv && !pc->urows && pc->shape == 3 && !(te && std::string(te) == "0") &&
-                   tma_smem <= 227 * 1024;
+        const bool streamable = pc->blockinv && !pc->urows && pc->shape == 3;
+        want_win = streamable && solve_path == "win";
+        want_tma = streamable && solve_path == "tma" && tma_smem <= 227 * 1024;
         if (want_tma) pc->shape = 4;  // the streamed path's RB; ShapeRec8 if an item would not fit the ring
+        if (want_win) {
+            pc->shape = 5;
+            if (const char* e = std::getenv("CPDDG_WIN_RB")) pc->win_rb = std::atoi(e) == 8 ? 8 : 16;
+        }
+        if (!want_win && !smem_y) throw ConfigError("subdomain system too large for the shared-memory solve");
     }
     if (pc->blockinv) {
-        const int rb = pc->shape == 4 ? tmas::RB : pc->shape >= 2 ? ShapeRec::RB : ShapeMid::RB;
+        const int rb = pc->shape == 5 ? pc->win_rb : pc->shape == 4 ? tmas::RB : pc->shape >= 2 ? ShapeRec::RB : ShapeMid::RB;
         static_assert(ShapeBig::RB == ShapeMid::RB && ShapeSmall::RB == ShapeRec::RB,
                       "records are built for RB = 30 or RB = 14");
         std::vector<std::int64_t> rbase(static_cast<std::size_t>(n_sub));
@@ -2555,8 +3185,10 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
         pc->recL.alloc(static_cast<std::size_t>(std::max<std::int64_t>(rt, 1)));
         pc->recU.alloc(static_cast<std::size_t>(std::max<std::int64_t>(rt, 1)));
         const dim3 rgrid(static_cast<unsigned>(n_sub), 16);
-        auto records = rb == 30 ? k_block_records<30> : rb == 14 ? k_block_records<14> : k_block_records<tmas::RB>;
-        auto compact = rb == 30 ? k_compact_rows<30> : rb == 14 ? k_compact_rows<14> : k_compact_rows<tmas::RB>;
+        auto records = rb == 30 ? k_block_records<30> : rb == 14 ? k_block_records<14> : rb == 16 ? k_block_records<16>
+                                                                                   : k_block_records<8>;
+        auto compact = rb == 30 ? k_compact_rows<30> : rb == 14 ? k_compact_rows<14> : rb == 16 ? k_compact_rows<16>
+                                                                                  : k_compact_rows<8>;
         records<<<rgrid, 64>>>(pc->n_rows.get(), pc->vbase.get(), pc->ebase.get(), pc->first.get(), pc->roff.get(),
                                pc->L.get(), nullptr, pc->rbase.get(), pc->recL.get());
         if (pc->urows)
@@ -2564,7 +3196,7 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
                                    pc->uroff.get(), pc->U.get(), pc->drev.get(), pc->rbase.get(), pc->recU.get());
         else
             (rb == 30 ? k_block_records_upper<30> : rb == 14 ? k_block_records_upper<14>
-                                                  : k_block_records_upper<tmas::RB>)<<<rgrid, 64>>>(
+                                  : rb == 16 ? k_block_records_upper<16> : k_block_records_upper<8>)<<<rgrid, 64>>>(
                 pc->n_rows.get(), pc->vbase.get(), pc->ebaseU.get(), pc->firstU.get(), pc->roffU.get(), pc->U.get(),
                 pc->dinv.get(), pc->rbase.get(), pc->recU.get());
         CPDDG_CUDA(cudaGetLastError());
@@ -2639,6 +3271,11 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
         }
         pc->far_entries = nL + nU;
         if (want_tma) setup_tma(pc.get(), n_rows, vbase, first, firstU, rocL, cbL, rocU, cbU, rbase);
+        if (want_win) {
+            const bool ok = pc->win_rb == 8 ? setup_win<8>(pc.get(), n_rows, vbase, first, firstU, rocL, cbL, rocU, cbU, rbase)
+                                            : setup_win<16>(pc.get(), n_rows, vbase, first, firstU, rocL, cbL, rocU, cbU, rbase);
+            if (!ok) throw ConfigError("preconditioner blocks do not fit the streamed solve's shared memory");
+        }
     }
     // factor probe (cpddg_pc_options::check_residual): solve A_j z = A_j x_probe
     // on the device for every subdomain and check the residual on the host --
@@ -2811,7 +3448,7 @@ int cpddg_pc_stats_get(const cpddg_pc* pc, cpddg_pc_stats* st) {
         st->factor_seconds = pc->factor_seconds;
         st->analyse_seconds = pc->analyse_seconds;
         st->max_probe_residual = pc->max_probe_residual;
-        st->apply_mode = pc->dense ? 1 : pc->tma ? 2 : 0;
+        st->apply_mode = pc->dense ? 1 : pc->tma ? 2 : pc->win ? (pc->win_gy ? 4 : 3) : 0;
     });
 }
 

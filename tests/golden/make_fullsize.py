@@ -8,6 +8,19 @@ residuals and a strided sample of the solution into fullsize_reference.json /
 fullsize_<name>.npz.  CPU only; minutes per configuration.
 
     python tests/golden/make_fullsize.py torus|trimesh|torus_ras_stationary
+    python tests/golden/make_fullsize.py headline [oras|ras|oras_std]
+
+The `headline` mode (BASELINE config 3: sphere h=0.0125, 256 RCB, N_O=3) runs
+the reference's OWN pipeline end to end -- build_problem, load_partition +
+align_interfaces, build_subdomains, assemble_local and DirectSolver
+(ref.RefProblem.decompose, proj/include/cpdd/pipeline.hpp:186-216), then
+gmres_solve (solve.hpp:128-214) -- with no input from this repository's setup
+code: the partition is inputs.rcb_partition on the reference band's own
+closest points and the right-hand side inputs.rhs_sphere on them.  It stores
+the aligned-label hash, A x and M x on uniform_vector(N_A, 11) (strided
+samples plus the componentwise-scale row sums sum_j |A_ij x_j|), and the
+solution (strided sample, norms), in fullsize_headline_<method>.npz and
+fullsize_reference.json.
 """
 import json
 import os
@@ -83,5 +96,68 @@ def main(name):
     print(key, rec)
 
 
+HEADLINE = {
+    # BASELINE config 3 runs: ORAS with the modified cross-point condition, RAS,
+    # and ORAS with the standard Robin condition (alpha_cross = alpha)
+    "oras": dict(method="oras", alpha=4.0, alpha_cross=40.0, max_iter=2000),
+    "ras": dict(method="ras", max_iter=2000),
+    "oras_std": dict(method="oras", alpha=4.0, alpha_cross=4.0, max_iter=2000),
+}
+HEADLINE_STRIDE = 97
+
+
+def label_hash(labels) -> str:
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(labels, np.int32).tobytes()).hexdigest()
+
+
+def headline(which):
+    w = HEADLINE[which]
+    cfg = dict(surface="sphere", h=0.0125, p=3, c=1.0, method=w["method"], mode="gmres", gmres_restart=50,
+               n_overlap=3, n_subdomains=256, rel_tol=1e-10, max_iter=w["max_iter"])
+    if w["method"] == "oras":
+        cfg.update(alpha=w["alpha"], alpha_cross=w["alpha_cross"])
+    t0 = time.time()
+    R = ref.RefProblem(cfg, workers=os.cpu_count())
+    cp = R.band()["cp"][: R.n_active]
+    part = inputs.rcb_partition(cp, 256)
+    aligned, moves = R.decompose(part)
+    t1 = time.time()
+    n = R.n_active
+    x = inputs.uniform_vector(n, 11)
+    Ax = R.apply_A(x)
+    ptr, col, val = R.csr("A")
+    scale = np.add.reduceat(np.abs(val) * np.abs(x[col]), ptr[:-1].astype(np.int64))
+    del ptr, col, val
+    Mx = R.pc_apply(x)
+    b = inputs.rhs_sphere(cp)
+    t2 = time.time()
+    out = R.solve(b)
+    t3 = time.time()
+    u = out["u"]
+    S = HEADLINE_STRIDE
+    rec = dict(n_active=n, n_ghost=R.n_ghost, align_moves=moves, label_sha256=label_hash(aligned),
+               n_subdomains=R.n_sub, iterations=out["iterations"], converged=out["converged"],
+               final_rel_residual=out["final_true_residual"] / float(np.linalg.norm(b)),
+               u_norm2=float(np.linalg.norm(u)), u_norm_inf=float(np.abs(u).max()),
+               Ax_norm2=float(np.linalg.norm(Ax)), Mx_norm2=float(np.linalg.norm(Mx)),
+               sample_stride=S, probe_seed=11, cfg=cfg,
+               _how=(f"tests/golden/make_fullsize.py headline {which}: oracle/_ref own pipeline "
+                     f"(build_problem, align_interfaces, build_subdomains, assemble_local, DirectSolver; "
+                     f"{os.cpu_count()} threads) {t1 - t0:.0f} s, A x / M x {t2 - t1:.0f} s, "
+                     f"gmres_solve {t3 - t2:.0f} s"))
+    path = os.path.join(HERE, "fullsize_reference.json")
+    d = json.load(open(path))
+    d.setdefault("headline_refpipeline", {})[which] = rec
+    json.dump(d, open(path, "w"), indent=2)
+    np.savez_compressed(os.path.join(HERE, f"fullsize_headline_{which}.npz"), u_sample=u[::S], Ax_sample=Ax[::S],
+                        Ax_scale_sample=scale[::S], Mx_sample=Mx[::S], residuals=np.asarray(out["residuals"]))
+    print(which, {k: v for k, v in rec.items() if k != "cfg"})
+
+
 if __name__ == "__main__":
-    main(sys.argv[1])
+    if sys.argv[1] == "headline":
+        for which in (sys.argv[2:] or list(HEADLINE)):
+            headline(which)
+    else:
+        main(sys.argv[1])

@@ -244,7 +244,7 @@ def test_dense_small_system_mode_matches_envelope_solve(monkeypatch):
     g, cfg, P, A, M, torch = _setup("circle_oras_gmres")
     monkeypatch.setenv("CPDDG_DENSE", "0")
     Me = api.SchwarzPreconditioner.from_problem(P)
-    assert M.stats()["apply_mode"] == 1 and Me.stats()["apply_mode"] in (0, 2)  # envelope: register or streamed
+    assert M.stats()["apply_mode"] == 1 and Me.stats()["apply_mode"] in (0, 2, 3)  # envelope: register or streamed
     x = torch.from_numpy(g["x"]).cuda()
     zd, ze = M.apply(x).cpu().numpy(), Me.apply(x).cpu().numpy()
     assert np.linalg.norm(zd - ze) <= 1e-12 * np.linalg.norm(ze)
@@ -303,14 +303,21 @@ def test_run_solve_pipeline_with_files(tmp_path):
 
 
 def test_streamed_record_and_chain_solves_agree(monkeypatch):
-    """The three preconditioner solve paths give the same A_j^-1 (to 1e-12)
-    and the same GMRES iteration count, and match the oracle restatement
-    (SuperLU per subdomain) at the usual 1e-9: the persistent TMA-streamed
-    record solve (k_solve_tma, default when there are more subdomains than
-    SMs), the register-staged record solve (CPDDG_TMA=0) and the
-    substitution-chain solve on reversed U rows (CPDDG_BLOCKINV=0); also the
-    streamed path's fallback when an item would not fit its ring.  Sphere
-    h = 0.05 cut into 256 RCB parts, so the streamed path is the one taken."""
+    """Every preconditioner solve path gives the same A_j^-1 (to 1e-12) and the
+    same GMRES iteration count, and matches the oracle restatement (SuperLU per
+    subdomain) at the usual 1e-9:
+
+    * k_solve_win, the default: windowed, TMA-streamed record solve, RB = 16
+      (apply_mode 3); also with RB = 8, with y kept in global memory
+      (CPDDG_WIN_GY=1, apply_mode 4: the path for windows larger than shared
+      memory), and with a ring so small that every item's data is read from
+      HBM (CPDDG_WIN_RING);
+    * k_solve_tma (CPDDG_SOLVE=tma, whole y in shared memory, RB = 8) and its
+      register-staged fallback when an item would not fit its ring;
+    * the register-staged record solve (CPDDG_SOLVE=reg) and the
+      substitution-chain solve on reversed U rows (CPDDG_BLOCKINV=0).
+
+    Sphere h = 0.05 cut into 256 RCB parts, so the streamed paths are taken."""
     import torch
 
     import cpdd_oracle as O
@@ -318,35 +325,46 @@ def test_streamed_record_and_chain_solves_agree(monkeypatch):
     P = api.Problem("sphere", h=0.05, p=3, c=1.0)
     P.decompose(inputs.rcb_partition(P.active_cp, 256), 2, "oras", 4.0, 40.0)
     A = api.DeviceHelmholtz.from_problem(P)
-    M = api.SchwarzPreconditioner.from_problem(P)
-    assert M.stats()["apply_mode"] == 2
-    monkeypatch.setenv("CPDDG_TMA_RING_LIMIT", "1024")  # every item "too large": ShapeRec8 fallback
-    Mf = api.SchwarzPreconditioner.from_problem(P)
-    monkeypatch.delenv("CPDDG_TMA_RING_LIMIT")
-    monkeypatch.setenv("CPDDG_TMA", "0")
-    Mr = api.SchwarzPreconditioner.from_problem(P)
-    monkeypatch.setenv("CPDDG_BLOCKINV", "0")
-    Mc = api.SchwarzPreconditioner.from_problem(P)
-    assert Mr.stats()["apply_mode"] == 0 and Mc.stats()["apply_mode"] == 0
+
+    def build(**env):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        m = api.SchwarzPreconditioner.from_problem(P)
+        for k in env:
+            monkeypatch.delenv(k)
+        return m
+
+    M = build()
+    assert M.stats()["apply_mode"] == 3
+    variants = {
+        "win_rb8": (build(CPDDG_WIN_RB="8"), 3),
+        "win_global_y": (build(CPDDG_WIN_GY="1"), 4),
+        "win_items_from_hbm": (build(CPDDG_WIN_RING="9216"), 3),
+        "tma": (build(CPDDG_SOLVE="tma"), 2),
+        "tma_fallback": (build(CPDDG_SOLVE="tma", CPDDG_TMA_RING_LIMIT="1024"), 0),
+        "reg": (build(CPDDG_SOLVE="reg"), 0),
+        "chain": (build(CPDDG_SOLVE="reg", CPDDG_BLOCKINV="0"), 0),
+    }
+    for name, (m, mode) in variants.items():
+        assert m.stats()["apply_mode"] == mode, name
     x = inputs.uniform_vector(P.n_active, 11)
     xd = torch.from_numpy(x).cuda()
-    z, zr, zc = (m.apply(xd).cpu().numpy() for m in (M, Mr, Mc))
+    z = M.apply(xd).cpu().numpy()
+    zc = variants["chain"][0].apply(xd).cpu().numpy()
     nz = np.linalg.norm(zc)
-    assert np.linalg.norm(z - zc) <= 1e-12 * nz and np.linalg.norm(zr - zc) <= 1e-12 * nz
+    for name, (m, _) in variants.items():
+        assert np.linalg.norm(m.apply(xd).cpu().numpy() - zc) <= 1e-12 * nz, name
+    assert np.linalg.norm(z - zc) <= 1e-12 * nz
     assert np.array_equal(z, M.apply(xd).cpu().numpy())  # bitwise reproducible
-    assert Mf.stats()["apply_mode"] == 0
-    zf = Mf.apply(xd).cpu().numpy()
-    assert np.linalg.norm(zf - zc) <= 1e-12 * nz
     locs = [P.local(j) for j in range(P.n_sub)]
     z_ref = O.schwarz_apply(locs, x)
     assert np.linalg.norm(z - z_ref) <= 1e-9 * np.linalg.norm(z_ref)
     b = torch.from_numpy(inputs.rhs_sphere(P.active_cp)).cuda()
-    its = [api.gmres_solve(A, b, m, 1e-10, 1000, 50).log.iterations for m in (M, Mr, Mc)]
-    assert its[0] == its[1] == its[2]
+    its = [api.gmres_solve(A, b, m, 1e-10, 1000, 50).log.iterations
+           for m in [M] + [v[0] for v in variants.values()]]
+    assert len(set(its)) == 1, its
     # kernel shared-memory limits are per kernel: a preconditioner with smaller
     # subdomains built afterwards must not break the earlier, larger one
-    monkeypatch.delenv("CPDDG_TMA")
-    monkeypatch.delenv("CPDDG_BLOCKINV")
     Ps = api.Problem("sphere", h=0.1, p=3, c=1.0)
     Ps.decompose(inputs.rcb_partition(Ps.active_cp, 200), 2, "oras", 4.0, 40.0)
     Msmall = api.SchwarzPreconditioner.from_problem(Ps)
