@@ -1,0 +1,21 @@
+#!/usr/bin/env bash
+# Regenerates the committed profiles of a round on a B200 (run under gpurun):
+#   bash scripts/profile_round.sh TAG
+# 1. the headline bench line (no profiler), 2. the ncu launch list of the same
+# command, 3. one ncu --set full capture of the preconditioner apply
+# (k_solve_win) and of the operator.  Outputs under gpurun_out/TAG_*.
+set -u
+TAG=${1:-r02}
+OUT=gpurun_out
+mkdir -p $OUT
+timeout 900 python bench.py --steps 5 --warmup 3 > $OUT/${TAG}_bench.json 2> $OUT/${TAG}_bench.err
+echo "bench rc=$?"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file $OUT/${TAG}_launches.csv \
+    python bench.py --steps 1 --warmup 3 --cpu-baseline off > $OUT/${TAG}_ncu_bench.log 2>&1
+echo "launch list rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_solve_win -s 2 -c 1 \
+    -o $OUT/${TAG}_k_solve_win -f python scripts/profile_pc_mode.py 0 > $OUT/${TAG}_ncu_pc.log 2>&1
+echo "pc capture rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_extend|k_helm|k_op" -s 4 -c 2 \
+    -o $OUT/${TAG}_op -f python scripts/profile_kernels.py > $OUT/${TAG}_ncu_op.log 2>&1
+echo "op capture rc=$?"
