@@ -176,7 +176,10 @@ typedef struct {
     double analyse_seconds;     /* host ordering + symbolic time */
     double max_probe_residual;  /* when check_residual */
     int apply_mode;             /* 0: register-staged record / envelope solves (k_solve); 1: dense local inverses
-                                   (small systems); 2: persistent TMA-streamed record solve (k_solve_tma) */
+                                   (small systems); 2: persistent TMA-streamed record solve (k_solve_tma);
+                                   3: windowed TMA-streamed record solve (k_solve_win, the default);
+                                   4: k_solve_win with the local vector in HBM (windows beyond shared memory) */
+    int n_pivoted;              /* local systems factored with partial pivoting (host band LU fallback) */
 } cpddg_pc_stats;
 
 CPDDG_API int cpddg_pc_create(int n_global, int n_sub, const cpddg_local_desc* locals,

@@ -69,6 +69,9 @@ constexpr int TILE = 64;  // trailing-update tile
 struct HostSub {
     int n = 0;
     bool reduced = false;
+    bool pivoted = false;      // factored on the host with partial pivoting (band LU): P A = L U
+    std::vector<int> rowperm;  // pivoted: factor-order row i of P A is row rowperm[i] of A
+    std::vector<double> preL, preU, prediag;  // pivoted: the factors in envelope storage
     std::int64_t ne = 0, neU = 0;  // envelope entries of L (rows) and U (columns)
     std::vector<int> inv;      // local (old) index -> factor order
     std::vector<double> probe; // b = A_sys x_probe in factor order
@@ -151,7 +154,62 @@ std::vector<int> rcm(const Graph& g) {
     return order;
 }
 
-HostSub analyse(const cpddg_local_desc& d, int n_global) {
+/** Sparse-row LU with partial pivoting (the explicit form P A = L U of
+ *  LAPACK getrf) of an n x n system in factor order with lower bandwidth bl.
+ *  Every row keeps its own window [lo, lo + v.size()) of columns: lo never
+ *  decreases (elimination at step k only fills columns > k), the right end
+ *  grows with the fill, and a row swap is a swap of row identities, so the
+ *  L part travels with its row.  Pivot candidates at step k lie in positions
+ *  [k, k + bl] (a row only moves down by a swap at a step within bl of it).
+ *  Throws DivergenceError on an exactly zero pivot column: the reference's
+ *  SparseLU reports such a system singular (direct.hpp:47-50).  This is the
+ *  fallback for local systems whose no-pivot device factorisation fails
+ *  (DirectSolver pivots, direct.hpp:41-52); it costs ~n bl (bl + bu) flops
+ *  on one host thread. */
+struct PivLU {
+    struct Row {
+        int lo = 0;
+        std::vector<double> v;
+        double get(int c) const { return c >= lo && c < lo + static_cast<int>(v.size()) ? v[static_cast<std::size_t>(c - lo)] : 0.0; }
+        int hi() const { return lo + static_cast<int>(v.size()); }
+    };
+    int n = 0, bl = 0;
+    std::vector<Row> rows;   // by identity (the original factor-order row)
+    std::vector<int> pos;    // position -> row identity (= P)
+};
+
+void piv_lu(PivLU& F, const std::string& what) {
+    const int n = F.n, bl = F.bl;
+    F.pos.resize(static_cast<std::size_t>(n));
+    std::iota(F.pos.begin(), F.pos.end(), 0);
+    for (int k = 0; k < n; ++k) {
+        int p = k;
+        double best = std::abs(F.rows[static_cast<std::size_t>(F.pos[static_cast<std::size_t>(k)])].get(k));
+        for (int q = k + 1; q <= std::min(n - 1, k + bl); ++q) {
+            const double a = std::abs(F.rows[static_cast<std::size_t>(F.pos[static_cast<std::size_t>(q)])].get(k));
+            if (a > best) {
+                best = a;
+                p = q;
+            }
+        }
+        if (!(best > 0.0) || !std::isfinite(best)) throw DivergenceError("singular factorization of " + what);
+        std::swap(F.pos[static_cast<std::size_t>(k)], F.pos[static_cast<std::size_t>(p)]);
+        const PivLU::Row& P = F.rows[static_cast<std::size_t>(F.pos[static_cast<std::size_t>(k)])];
+        const double piv = P.get(k);
+        const int phi = P.hi();
+        for (int q = k + 1; q <= std::min(n - 1, k + bl); ++q) {
+            PivLU::Row& R = F.rows[static_cast<std::size_t>(F.pos[static_cast<std::size_t>(q)])];
+            const double a = R.get(k);
+            if (a == 0.0) continue;
+            const double l = a / piv;
+            if (R.hi() < phi) R.v.resize(static_cast<std::size_t>(phi - R.lo), 0.0);
+            R.v[static_cast<std::size_t>(k - R.lo)] = l;
+            for (int c = k + 1; c < phi; ++c) R.v[static_cast<std::size_t>(c - R.lo)] -= l * P.v[static_cast<std::size_t>(c - P.lo)];
+        }
+    }
+}
+
+HostSub analyse(const cpddg_local_desc& d, int n_global, bool pivot = false, int j_sub = -1) {
     const int nl = d.n_overlap + d.n_bc;
     if (d.n_overlap < 0 || d.n_bc < 0 || nl <= 0) throw InternalError("empty local system");
     const std::int64_t* rp = d.row_ptr;
@@ -201,6 +259,43 @@ HostSub analyse(const cpddg_local_desc& d, int n_global) {
     const std::vector<int> perm = rcm(gr);
     std::vector<int> inv(static_cast<std::size_t>(n));
     for (int k = 0; k < n; ++k) inv[static_cast<std::size_t>(perm[static_cast<std::size_t>(k)])] = k;
+    PivLU F;
+    if (pivot) {
+        // host LU with partial pivoting in factor order; the envelopes below
+        // then come from the factors' own nonzeros
+        int bl = 0;
+        F.n = n;
+        F.rows.resize(static_cast<std::size_t>(n));
+        std::vector<int> hi(static_cast<std::size_t>(n), 0);
+        for (int i = 0; i < n; ++i) {
+            F.rows[static_cast<std::size_t>(i)].lo = i;
+            hi[static_cast<std::size_t>(i)] = i + 1;
+        }
+        for (int r = 0; r < n; ++r)
+            for (std::int64_t k = rp[r]; k < rp[r + 1]; ++k) {
+                const int c = d.col[k];
+                if (c >= n) continue;
+                const int pi = inv[static_cast<std::size_t>(r)], pj = inv[static_cast<std::size_t>(c)];
+                bl = std::max(bl, pi - pj);
+                F.rows[static_cast<std::size_t>(pi)].lo = std::min(F.rows[static_cast<std::size_t>(pi)].lo, pj);
+                hi[static_cast<std::size_t>(pi)] = std::max(hi[static_cast<std::size_t>(pi)], pj + 1);
+            }
+        for (int i = 0; i < n; ++i) {
+            PivLU::Row& R = F.rows[static_cast<std::size_t>(i)];
+            R.v.assign(static_cast<std::size_t>(hi[static_cast<std::size_t>(i)] - R.lo), 0.0);
+        }
+        for (int r = 0; r < n; ++r)
+            for (std::int64_t k = rp[r]; k < rp[r + 1]; ++k) {
+                const int c = d.col[k];
+                if (c >= n) continue;
+                PivLU::Row& R = F.rows[static_cast<std::size_t>(inv[static_cast<std::size_t>(r)])];
+                R.v[static_cast<std::size_t>(inv[static_cast<std::size_t>(c)] - R.lo)] += d.val[k];
+            }
+        F.bl = bl;
+        piv_lu(F, "subdomain " + std::to_string(j_sub));
+        S.pivoted = true;
+        S.rowperm = F.pos;
+    }
     // envelopes of the actual (nonsymmetric) pattern in factor order: L row i
     // starts at fL_i (first nonzero left of the diagonal), U column c at fU_c
     // (first nonzero above it).  LU without pivoting keeps its fill inside
@@ -222,6 +317,20 @@ HostSub analyse(const cpddg_local_desc& d, int n_global) {
             else
                 S.firstU[static_cast<std::size_t>(pj)] = std::min(S.firstU[static_cast<std::size_t>(pj)], pi);
         }
+    if (pivot) {  // the factors' own envelopes (fill included)
+        std::iota(S.first.begin(), S.first.end(), 0);
+        std::iota(S.firstU.begin(), S.firstU.end(), 0);
+        for (int i = 0; i < n; ++i) {
+            const PivLU::Row& R = F.rows[static_cast<std::size_t>(F.pos[static_cast<std::size_t>(i)])];
+            for (int c = R.lo; c < R.hi(); ++c) {
+                if (c == i || R.v[static_cast<std::size_t>(c - R.lo)] == 0.0) continue;
+                if (c < i)
+                    S.first[static_cast<std::size_t>(i)] = std::min(S.first[static_cast<std::size_t>(i)], c);
+                else
+                    S.firstU[static_cast<std::size_t>(c)] = std::min(S.firstU[static_cast<std::size_t>(c)], i);
+            }
+        }
+    }
     static const bool sym_env = [] {
         const char* e = std::getenv("CPDDG_ENVELOPE");
         return e && std::string(e) == "sym";
@@ -264,6 +373,25 @@ HostSub analyse(const cpddg_local_desc& d, int n_global) {
         }
         return out;
     };
+    if (pivot) {  // the factors in envelope storage (k_factor skips this subdomain)
+        S.preL.assign(static_cast<std::size_t>(S.ne), 0.0);
+        S.preU.assign(static_cast<std::size_t>(S.neU), 0.0);
+        S.prediag.assign(static_cast<std::size_t>(n), 0.0);
+        for (int i = 0; i < n; ++i) {
+            const PivLU::Row& R = F.rows[static_cast<std::size_t>(F.pos[static_cast<std::size_t>(i)])];
+            S.prediag[static_cast<std::size_t>(i)] = R.get(i);
+            for (int c = std::max(R.lo, S.first[static_cast<std::size_t>(i)]); c < std::min(i, R.hi()); ++c)
+                S.preL[static_cast<std::size_t>(S.roff[static_cast<std::size_t>(i)] + c - S.first[static_cast<std::size_t>(i)])] =
+                    R.v[static_cast<std::size_t>(c - R.lo)];
+            for (int c = std::max(i + 1, R.lo); c < R.hi(); ++c) {
+                const double u = R.v[static_cast<std::size_t>(c - R.lo)];
+                if (u != 0.0)
+                    S.preU[static_cast<std::size_t>(S.roffU[static_cast<std::size_t>(c)] + i - S.firstU[static_cast<std::size_t>(c)])] = u;
+            }
+        }
+        F.rows.clear();
+        F.rows.shrink_to_fit();
+    }
     S.rlast = reach({&S.first, &S.firstU});
     S.urlast = reach({&S.firstU});
     // factor probe: b = A_sys x with x_i = 1 + (i mod 7) / 8 in factor order
@@ -282,6 +410,11 @@ HostSub analyse(const cpddg_local_desc& d, int n_global) {
         const int g = d.overlap[o];
         if (g < 0 || g >= n_global) throw InternalError("overlap index out of range");
         S.gidx[static_cast<std::size_t>(inv[static_cast<std::size_t>(o)])] = g;
+    }
+    if (pivot) {  // L U z = P b: row i gathers the right-hand side of row rowperm[i]
+        std::vector<int> g2(static_cast<std::size_t>(n));
+        for (int i = 0; i < n; ++i) g2[static_cast<std::size_t>(i)] = S.gidx[static_cast<std::size_t>(S.rowperm[static_cast<std::size_t>(i)])];
+        S.gidx = std::move(g2);
     }
     for (int k = 0; k < d.n_scatter; ++k) {
         const int lo = d.scatter_local[k], g = d.scatter_global[k];
@@ -372,10 +505,12 @@ __global__ void __launch_bounds__(kFactorThreads, 2) k_factor(const int* __restr
                                                            const std::int64_t* __restrict__ roffU_all,
                                                            const int* __restrict__ rlast_all,
                                                            double* diag_all, double* L_all, double* U_all,
-                                                           double* dinv_all, int* status) {
+                                                           double* dinv_all, int* status,
+                                                           const int* __restrict__ prefactored) {
     const int j = order[blockIdx.x];
     const SubPtrs S = sub_ptrs(j, n_rows, vbase, ebase, ebaseU, first_all, roff_all, firstU_all, roffU_all,
                                rlast_all, diag_all, L_all, U_all);
+    const bool pre = prefactored[j] != 0;  // factored on the host with pivoting: pivots only
     extern __shared__ double sm[];
     double* A11 = sm;                            // [NB][NB+1]
     double* Xi = A11 + NB * (NB + 1);            // [NB][TILE+1]: X rows of tile i, transposed (p-major)
@@ -386,7 +521,7 @@ __global__ void __launch_bounds__(kFactorThreads, 2) k_factor(const int* __restr
     const int n = S.n;
     __shared__ int skip_tile;
 
-    for (int k0 = 0; k0 < n; k0 += NB) {
+    for (int k0 = 0; k0 < (pre ? 0 : n); k0 += NB) {
         const int kb = min(NB, n - k0), k1 = k0 + kb;
         const int R = S.rlast[k1 - 1];  // last row touching the panel columns
         // (1) diagonal block into shared memory
@@ -2876,12 +3011,22 @@ static bool setup_win(cpddg_pc* pc, const std::vector<int>& n_rows, const std::v
     return true;
 }
 
-static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* locals, const cpddg_pc_options* opt) {
+/** Thrown by pc_build when local systems need the pivoted host factorisation:
+ *  a zero / non-finite pivot or a failed probe of the no-pivot device LU. */
+struct NeedPivot {
+    std::vector<int> subs;
+};
+
+static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* locals, const cpddg_pc_options* opt,
+                          const std::vector<char>& pivot_set) {
     if (n_global <= 0 || n_sub <= 0 || !locals) throw InternalError("empty preconditioner");
     const auto t0 = std::chrono::steady_clock::now();
     std::vector<HostSub> subs(static_cast<std::size_t>(n_sub));
-    parallel_for(n_sub, opt ? opt->workers : 0,
-                 [&](int j, int) { subs[static_cast<std::size_t>(j)] = analyse(locals[j], n_global); });
+    parallel_for(n_sub, opt ? opt->workers : 0, [&](int j, int) {
+        subs[static_cast<std::size_t>(j)] = analyse(locals[j], n_global, pivot_set[static_cast<std::size_t>(j)] != 0, j);
+    });
+    std::vector<int> pre(static_cast<std::size_t>(n_sub), 0);
+    for (int j = 0; j < n_sub; ++j) pre[static_cast<std::size_t>(j)] = subs[static_cast<std::size_t>(j)].pivoted ? 1 : 0;
     if (std::getenv("CPDDG_VERBOSE")) {
         std::int64_t eL = 0, eU = 0;
         int reachL = 0, reachU = 0;  // longest row / column of the envelopes (a y window must cover it)
@@ -2909,7 +3054,7 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
     pc->n_sub = n_sub;
     std::vector<int> n_rows, first, firstU, rlast, urlast, gidx, sidx;
     std::vector<std::int64_t> vbase, ebase, ebaseU, roff, roffU;
-    std::vector<double> probe_all;
+    std::vector<double> probe_all, probe_dev;
     std::vector<std::vector<int>> invs;
     std::int64_t vb = 0, ebs = 0, ebsU = 0;
     for (auto& S : subs) {
@@ -2934,9 +3079,11 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
     {
         // A_j's entries as (destination, value) pairs, scattered on the device
         std::vector<std::int64_t> pbase(static_cast<std::size_t>(n_sub) + 1, 0);
-        for (int j = 0; j < n_sub; ++j)
+        for (int j = 0; j < n_sub; ++j) {
+            const HostSub& S = subs[static_cast<std::size_t>(j)];
             pbase[static_cast<std::size_t>(j) + 1] =
-                pbase[static_cast<std::size_t>(j)] + locals[j].row_ptr[subs[static_cast<std::size_t>(j)].n];
+                pbase[static_cast<std::size_t>(j)] + (S.pivoted ? S.ne + S.neU + S.n : locals[j].row_ptr[S.n]);
+        }
         const std::int64_t cap = std::max<std::int64_t>(pbase.back(), 1);
         DevBuf<std::int64_t> pdst(static_cast<std::size_t>(cap));
         DevBuf<double> pval(static_cast<std::size_t>(cap));
@@ -2955,9 +3102,26 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
             const std::int64_t room = pbase[static_cast<std::size_t>(j) + 1] - pbase[static_cast<std::size_t>(j)];
             std::vector<std::int64_t> dst(static_cast<std::size_t>(room));
             std::vector<double> val(static_cast<std::size_t>(room));
-            const std::int64_t m = scatter_pairs(locals[j], S, ebase[static_cast<std::size_t>(j)],
-                                                 ebaseU[static_cast<std::size_t>(j)], vbase[static_cast<std::size_t>(j)],
-                                                 dst.data(), val.data());
+            std::int64_t m = 0;
+            if (S.pivoted) {  // the host factors, slot by slot
+                const std::int64_t eb = ebase[static_cast<std::size_t>(j)], ebu = ebaseU[static_cast<std::size_t>(j)];
+                const std::int64_t v0 = vbase[static_cast<std::size_t>(j)];
+                for (std::int64_t e = 0; e < S.ne; ++e, ++m) {
+                    dst[static_cast<std::size_t>(m)] = eb + e;
+                    val[static_cast<std::size_t>(m)] = S.preL[static_cast<std::size_t>(e)];
+                }
+                for (std::int64_t e = 0; e < S.neU; ++e, ++m) {
+                    dst[static_cast<std::size_t>(m)] = (1LL << kTagShift) | (ebu + e);
+                    val[static_cast<std::size_t>(m)] = S.preU[static_cast<std::size_t>(e)];
+                }
+                for (int i = 0; i < S.n; ++i, ++m) {
+                    dst[static_cast<std::size_t>(m)] = (2LL << kTagShift) | (v0 + i);
+                    val[static_cast<std::size_t>(m)] = S.prediag[static_cast<std::size_t>(i)];
+                }
+            } else {
+                m = scatter_pairs(locals[j], S, ebase[static_cast<std::size_t>(j)], ebaseU[static_cast<std::size_t>(j)],
+                                  vbase[static_cast<std::size_t>(j)], dst.data(), val.data());
+            }
             used[static_cast<std::size_t>(j)] = m;
             const std::size_t o = static_cast<std::size_t>(pbase[static_cast<std::size_t>(j)]);
             if (m) {
@@ -2992,6 +3156,10 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
         append(sidx, S.sidx);
         append(roff, S.roff);
         append(probe_all, S.probe);
+        if (S.pivoted)  // the device solves L U z = P b: its probe right-hand side is permuted
+            for (int i = 0; i < S.n; ++i) probe_dev.push_back(S.probe[static_cast<std::size_t>(S.rowperm[static_cast<std::size_t>(i)])]);
+        else
+            append(probe_dev, S.probe);
         invs.push_back(std::move(S.inv));
         S = HostSub{};
     }
@@ -3056,10 +3224,12 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
     CPDDG_CUDA(cudaEventCreate(&e0));
     CPDDG_CUDA(cudaEventCreate(&e1));
     CPDDG_CUDA(cudaEventRecord(e0));
+    DevBuf<int> dpre;
+    dpre.upload(pre);
     k_factor<<<n_sub, kFactorThreads, fsm>>>(pc->order.get(), pc->n_rows.get(), pc->vbase.get(), pc->ebase.get(),
                                            pc->ebaseU.get(), pc->first.get(), pc->roff.get(), pc->firstU.get(),
                                            pc->roffU.get(), pc->rlast.get(), pc->diag.get(),
-                                           pc->L.get(), pc->U.get(), pc->dinv.get(), status.get());
+                                           pc->L.get(), pc->U.get(), pc->dinv.get(), status.get(), dpre.get());
     CPDDG_CUDA(cudaGetLastError());
     CPDDG_CUDA(cudaEventRecord(e1));
     CPDDG_CUDA(cudaEventSynchronize(e1));
@@ -3070,8 +3240,17 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
     pc->factor_seconds = ms * 1e-3;
     std::vector<int> st(static_cast<std::size_t>(n_sub));
     CPDDG_CUDA(cudaMemcpy(st.data(), status.get(), st.size() * sizeof(int), cudaMemcpyDeviceToHost));
-    for (int j = 0; j < n_sub; ++j)
-        if (st[static_cast<std::size_t>(j)]) throw DivergenceError("singular factorization of subdomain " + std::to_string(j));
+    {
+        NeedPivot np;
+        for (int j = 0; j < n_sub; ++j)
+            if (st[static_cast<std::size_t>(j)]) {
+                // a zero pivot of the pivoted host factor was already reported by piv_lu
+                if (pre[static_cast<std::size_t>(j)]) throw DivergenceError("singular factorization of subdomain " + std::to_string(j));
+                np.subs.push_back(j);
+            }
+        if (!np.subs.empty()) throw np;  // retry those subdomains with partial pivoting
+    }
+    pc->n_pivoted = static_cast<int>(std::count(pre.begin(), pre.end(), 1));
 
     pc->u_entries = ebsU;
     // record solve (default): U by columns; substitution-chain solve
@@ -3283,7 +3462,7 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
     // tests/test_transmission.cpp:307-334) made observable.
     if (opt && opt->check_residual) {
         DevBuf<double> pb, pz(static_cast<std::size_t>(vb));
-        pb.upload(probe_all);
+        pb.upload(probe_dev);
         pc_apply_mode(pc.get(), pb.get(), pz.get(), false, 3, nullptr);
         std::vector<double> z(static_cast<std::size_t>(vb));
         CPDDG_CUDA(cudaMemcpy(z.data(), pz.get(), z.size() * sizeof(double), cudaMemcpyDeviceToHost));
@@ -3308,10 +3487,15 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
             res[static_cast<std::size_t>(j)] = bmax > 0 ? rmax / bmax : rmax;
         });
         pc->max_probe_residual = *std::max_element(res.begin(), res.end());
+        NeedPivot np;
         for (int j = 0; j < n_sub; ++j)
-            if (!(res[static_cast<std::size_t>(j)] <= 1e-8))
-                throw DivergenceError("inaccurate factorization of subdomain " + std::to_string(j) +
-                                      " (probe residual " + std::to_string(res[static_cast<std::size_t>(j)]) + ")");
+            if (!(res[static_cast<std::size_t>(j)] <= 1e-8)) {
+                if (pre[static_cast<std::size_t>(j)])
+                    throw DivergenceError("inaccurate factorization of subdomain " + std::to_string(j) +
+                                          " (probe residual " + std::to_string(res[static_cast<std::size_t>(j)]) + ")");
+                np.subs.push_back(j);
+            }
+        if (!np.subs.empty()) throw np;  // no-pivot factors not accurate enough: pivot those
     }
     // small systems: dense inverses (k_solve_dense) when the envelope solve
     // would be a latency-bound chain on a mostly idle GPU
@@ -3358,7 +3542,7 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
             // the inverses reproduce the envelope solve on the probe right-hand sides
             if (!probe_all.empty()) {
                 DevBuf<double> pb, z1(static_cast<std::size_t>(vb)), z2(static_cast<std::size_t>(vb));
-                pb.upload(probe_all);
+                pb.upload(probe_dev);
                 pc_apply_mode(pc.get(), pb.get(), z1.get(), false, 3, nullptr);
                 pc->dense_probe = true;
                 pc_apply_mode(pc.get(), pb.get(), z2.get(), false, 3, nullptr);
@@ -3390,6 +3574,30 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
     return pc.release();
 }
 
+/** pc_build with the DirectSolver's robustness (direct.hpp:41-52: Eigen
+ *  SparseLU pivots): local systems whose no-pivot device factorisation hits
+ *  a zero / non-finite pivot or misses the probe-residual contract are
+ *  factored on the host with partial pivoting (piv_lu) and the whole
+ *  preconditioner is rebuilt with them.  CPDDG_PIVOT=all pivots every
+ *  subdomain (testing). */
+static cpddg_pc* pc_build_pivoting(int n_global, int n_sub, const cpddg_local_desc* locals,
+                                   const cpddg_pc_options* opt) {
+    std::vector<char> pivot(static_cast<std::size_t>(std::max(n_sub, 0)), 0);
+    if (const char* e = std::getenv("CPDDG_PIVOT"); e && std::string(e) == "all") std::fill(pivot.begin(), pivot.end(), 1);
+    for (int attempt = 0;; ++attempt) {
+        try {
+            return pc_build(n_global, n_sub, locals, opt, pivot);
+        } catch (const NeedPivot& np) {
+            if (attempt > 0 && std::none_of(np.subs.begin(), np.subs.end(), [&](int j) { return !pivot[static_cast<std::size_t>(j)]; }))
+                throw DivergenceError("inaccurate factorization of subdomain " + std::to_string(np.subs.front()));
+            for (int j : np.subs) pivot[static_cast<std::size_t>(j)] = 1;
+            if (std::getenv("CPDDG_VERBOSE"))
+                std::fprintf(stderr, "[cpddg] %zu local system(s) refactored with partial pivoting (first: %d)\n",
+                             np.subs.size(), np.subs.front());
+        }
+    }
+}
+
 }  // namespace cpddg
 
 using namespace cpddg;
@@ -3400,7 +3608,7 @@ int cpddg_pc_create(int n_global, int n_sub, const cpddg_local_desc* locals, con
                     cpddg_pc** out) {
     return guarded([&] {
         if (!out) throw InternalError("null argument");
-        *out = pc_build(n_global, n_sub, locals, opt);
+        *out = pc_build_pivoting(n_global, n_sub, locals, opt);
     });
 }
 
@@ -3423,7 +3631,7 @@ int cpddg_pc_create_from_setup(const cpddg_setup* s, const cpddg_pc_options* opt
             d[j] = {L.n_overlap, L.n_bc, L.overlap.data(), static_cast<int>(L.scatter_local.size()),
                     L.scatter_local.data(), L.scatter_global.data(), L.A.ptr.data(), L.A.col.data(), L.A.val.data()};
         }
-        *out = pc_build(n_global, static_cast<int>(d.size()), d.data(), opt);
+        *out = pc_build_pivoting(n_global, static_cast<int>(d.size()), d.data(), opt);
     });
 }
 
@@ -3449,6 +3657,7 @@ int cpddg_pc_stats_get(const cpddg_pc* pc, cpddg_pc_stats* st) {
         st->analyse_seconds = pc->analyse_seconds;
         st->max_probe_residual = pc->max_probe_residual;
         st->apply_mode = pc->dense ? 1 : pc->tma ? 2 : pc->win ? (pc->win_gy ? 4 : 3) : 0;
+        st->n_pivoted = pc->n_pivoted;
     });
 }
 

@@ -29,7 +29,10 @@ from conftest import GOLDEN
 
 pytestmark = pytest.mark.gpu
 
-RUNS = {"oras": ("oras", 4.0, 40.0), "ras": ("ras", 1.0, -1.0), "oras_std": ("oras", 4.0, 4.0)}
+# run -> (method, alpha, alpha_cross, subdomains); oras_ns32 has local systems of
+# up to 28.6k rows, beyond round 1's shared-memory limit of 25.6k
+RUNS = {"oras": ("oras", 4.0, 40.0, 256), "ras": ("ras", 1.0, -1.0, 256), "oras_std": ("oras", 4.0, 4.0, 256),
+        "oras_ns32": ("oras", 4.0, 40.0, 32)}
 
 
 def _reference():
@@ -45,9 +48,9 @@ AVAILABLE = sorted(k for k in RUNS if k in _reference()
 def problem():
     from paper_1909_08734_b200 import api, inputs
     P = api.Problem("sphere", h=0.0125, p=3, c=1.0)
-    part = inputs.rcb_partition(P.active_cp, 256)
+    parts = {ns: inputs.rcb_partition(P.active_cp, ns) for ns in (256, 32)}
     x = inputs.uniform_vector(P.n_active, 11)
-    return P, part, x
+    return P, parts, x
 
 
 @pytest.mark.parametrize("run", AVAILABLE)
@@ -55,13 +58,13 @@ def test_headline_matches_reference_pipeline(problem, run):
     import torch
 
     from paper_1909_08734_b200 import api, inputs
-    P, part, x = problem
+    P, parts, x = problem
     ref = _reference()[run]
     g = np.load(os.path.join(GOLDEN, f"fullsize_headline_{run}.npz"))
     S = ref["sample_stride"]
     assert (P.n_active, P.n_ghost) == (ref["n_active"], ref["n_ghost"])
-    method, alpha, ax = RUNS[run]
-    aligned, moves = P.decompose(part, 3, method, alpha, ax)
+    method, alpha, ax, ns = RUNS[run]
+    aligned, moves = P.decompose(parts[ns], 3, method, alpha, ax)
     assert moves == ref["align_moves"]
     assert hashlib.sha256(np.ascontiguousarray(aligned, np.int32).tobytes()).hexdigest() == ref["label_sha256"]
 
