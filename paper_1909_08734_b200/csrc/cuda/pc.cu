@@ -3310,7 +3310,8 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
     const bool smem_y = pc->solve_smem <= 200 * 1024;
     if (solve_path != "win" && !smem_y)
         throw ConfigError("subdomain system too large for the shared-memory solve (CPDDG_SOLVE=" + solve_path + ")");
-    const int solve_smem_set = std::min(pc->solve_smem, 200 * 1024);
+    // the shared-memory-y kernels can only run (and only need their limit raised) when y fits
+    const int solve_smem_set = smem_y ? pc->solve_smem : 1;
     set_solve_smem<false, ShapeMid, false>(solve_smem_set);
     set_solve_smem<true, ShapeBig, false>(solve_smem_set);
     set_solve_smem<true, ShapeMid, false>(solve_smem_set);
