@@ -56,13 +56,21 @@ CONFIGS = {
                     alpha=4.0, alpha_cross=40.0, gmres_restart=50, rel_tol=1e-10, max_iter=2000,
                     partition="rcb", rhs="trig", subdivisions=6, mesh_seed=5),
 }
+# North-star scale points: the headline with BASELINE's
+# sqrt(17) h tube radius (663,454 DOF), and the "~2.6M DOF" sphere at 256
+# subdomains -- h = 0.0063 with the sqrt(17) h radius (the paper's h = 1/200
+# size, with p = 3).  Not in the reference (no radius override):
+# device-only scale runs.
+CONFIGS["headline_r17"] = dict(CONFIGS["headline"], tube_radius_h=17 ** 0.5)
+CONFIGS["sphere2p6m"] = dict(CONFIGS["headline"], h=0.0063, tube_radius_h=17 ** 0.5)
 WORKLOAD = CONFIGS["headline"]
 FALLBACK_HBM_GBS = 6650.0
 
 
 def workload_name(w=None):
     w = w or WORKLOAD
-    return (f"{w['surface']}_h{w['h']}_p{w['p']}_{w['partition']}{w['n_subdomains']}_no{w['n_overlap']}_"
+    r = f"_r{w['tube_radius_h']:.4g}h" if w.get("tube_radius_h") else ""
+    return (f"{w['surface']}_h{w['h']}{r}_p{w['p']}_{w['partition']}{w['n_subdomains']}_no{w['n_overlap']}_"
             f"{w['method']}_a{w['alpha']:g}_ax{w['alpha_cross']:g}_gmres{w['gmres_restart']}_tol{w['rel_tol']:g}")
 
 
@@ -76,7 +84,8 @@ def build_problem(w):
         obj = os.path.join(tempfile.mkdtemp(prefix="cpddg_mesh_"), "icosphere.obj")
         inputs.write_obj(obj, v, f)
     P = api.Problem(w["surface"], h=w["h"], p=w["p"], c=w["c"], major_radius=w.get("major_radius", 2 / 3),
-                    minor_radius=w.get("minor_radius", 1 / 3), obj_path=obj)
+                    minor_radius=w.get("minor_radius", 1 / 3), obj_path=obj,
+                    tube_radius=w.get("tube_radius_h", 0.0) * w["h"])
     cp = P.active_cp
     part = inputs.sector_partition(cp, w["n_subdomains"]) if w["partition"] == "sector" \
         else inputs.rcb_partition(cp, w["n_subdomains"])
@@ -179,7 +188,7 @@ def static_config(w, n_active):
         "rhs": {"sphere": "f = 13 u, u = x^3 - 3xy^2 at closest points",
                 "circle": "f = 2 sin(t) + 145 sin(12 t)",
                 "trig": "16 seeded modes sin(k.cp + phi), k in [-4,4]^3"}[w["rhs"]],
-        "tube_radius": "reference (p+1)/2 sqrt(d) h" if not w.get("tube_radius") else f"{w['tube_radius']:.6g} h",
+        "tube_radius": "reference (p+1)/2 sqrt(d) h" if not w.get("tube_radius_h") else f"{w['tube_radius_h']:.6g} h",
         "l2": "inputs larger than L2 (local factors streamed per preconditioner apply exceed the 126 MB L2)",
         "parallelism": "replicas (one independent solve per GPU)",
     }
@@ -216,7 +225,7 @@ class RefArm:
             obj = os.path.join(tempfile.mkdtemp(prefix="cpddg_ref_mesh_"), "icosphere.obj")
             I.write_obj(obj, v, f)
             cfg.update(obj=obj)
-        if w.get("tube_radius"):
+        if w.get("tube_radius_h"):
             raise SystemExit("the reference has no tube-radius override (proj/include/cpdd/band.hpp:157)")
         t0 = time.perf_counter()
         self.R = R = ref.RefProblem(cfg, workers=self.cores)

@@ -2880,6 +2880,60 @@ static void setup_tma(cpddg_pc* pc, const std::vector<int>& n_rows, const std::v
     pc->tma = true;
 }
 
+/** Window geometry of k_solve_win for blocks of RB rows: W (power of two)
+ *  covers the longest far row (forward) and the D-block entering lookahead
+ *  below the backward front (D RB > longest U column); the ring takes the
+ *  rest of shared memory, or all of it when the window goes to HBM. */
+struct WinGeometry {
+    int W = 0, dback = 0, ring = 0;
+    bool gy = false;
+};
+static WinGeometry win_geometry(int rb, int reachL, int reachU) {
+    WinGeometry g;
+    g.dback = (reachU + rb - 1) / rb + 1;
+    g.W = 4 * rb;
+    while (g.W < reachL + 2 * rb || g.W < (g.dback + 3) * rb) g.W *= 2;
+    if (const char* e = std::getenv("CPDDG_WIN_W")) g.W = std::max(g.W, std::atoi(e));  // development: larger windows
+    const int kStatic = 4096;  // static shared memory of the kernel (mbarriers, slots, partial dots)
+    const int avail = (win::kMaxSmem - kStatic) & ~127;
+    g.gy = 8 * g.W > avail - 64 * 1024;  // keep at least a 64 KB ring, else y stays in ybuf
+    if (const char* e = std::getenv("CPDDG_WIN_GY")) g.gy = g.gy || std::string(e) == "1";
+    g.ring = g.gy ? avail : (avail - 8 * g.W) & ~127;
+    if (const char* e = std::getenv("CPDDG_WIN_RING")) g.ring = std::min(g.ring, std::atoi(e) & ~127);
+    return g;
+}
+
+/** Block size of k_solve_win: RB = 16 halves the sequential steps of RB = 8
+ *  (1.89 vs 2.44 ms per headline apply, where the largest RB = 16 item is
+ *  170 KB of a 212 KB ring) but doubles the items; when more than 0.5 % of
+ *  the RB = 16 items would come near the ring size (long envelope rows:
+ *  large subdomains), RB = 8 keeps the stream in the ring instead of reading
+ *  those items from HBM (2.7x slower per byte, measured). */
+static int win_choose_rb(const std::vector<int>& n_rows, const std::vector<std::int64_t>& vbase,
+                         const std::vector<int>& fL, const std::vector<int>& fU) {
+    constexpr int RB = 16;
+    int reachL = 0, reachU = 0;
+    std::int64_t items = 0, large = 0;
+    for (std::size_t j = 0; j < n_rows.size(); ++j)
+        for (int i = 0; i < n_rows[j]; ++i) {
+            reachL = std::max(reachL, i - fL[static_cast<std::size_t>(vbase[j] + i)]);
+            reachU = std::max(reachU, i - fU[static_cast<std::size_t>(vbase[j] + i)]);
+        }
+    const WinGeometry g = win_geometry(RB, reachL, reachU);
+    for (std::size_t j = 0; j < n_rows.size(); ++j) {
+        const int n = n_rows[j], nblk = (n + RB - 1) / RB;
+        for (const auto* f : {&fL, &fU})
+            for (int B = 1; B < nblk; ++B) {
+                long long len = 0;
+                for (int i = B * RB; i < std::min(n, B * RB + RB); ++i)
+                    len += std::max(0, (B - 1) * RB - (*f)[static_cast<std::size_t>(vbase[j] + i)]);
+                ++items;
+                large += win::Geo<RB>::kHdr + 8 * len > g.ring * 85LL / 100 ? 1 : 0;
+            }
+    }
+    return 200 * large > items ? 8 : 16;
+}
+
 /** Items, descriptors, per-CTA subdomain lists, window and ring geometry of
  *  k_solve_win (see there) for blocks of RB rows.  Returns false (path left
  *  off) only if not even the global-memory variant fits. */
@@ -2900,16 +2954,9 @@ static bool setup_win(cpddg_pc* pc, const std::vector<int>& n_rows, const std::v
             reachL = std::max(reachL, i - fL[g]);
             reachU = std::max(reachU, i - fU[g]);
         }
-    const int dback = (reachU + RB - 1) / RB + 1;
-    int W = 4 * RB;
-    while (W < reachL + 2 * RB || W < (dback + 3) * RB) W *= 2;
-    if (const char* e = std::getenv("CPDDG_WIN_W")) W = std::max(W, std::atoi(e));  // development: larger windows
-    const int kStatic = 4096;  // static shared memory of the kernel (mbarriers, slots, partial dots)
-    const int avail = (win::kMaxSmem - kStatic) & ~127;
-    bool gy = 8 * W > avail - 64 * 1024;  // keep at least a 64 KB ring, else y stays in ybuf
-    if (const char* e = std::getenv("CPDDG_WIN_GY")) gy = gy || std::string(e) == "1";
-    int ring = gy ? avail : (avail - 8 * W) & ~127;
-    if (const char* e = std::getenv("CPDDG_WIN_RING")) ring = std::min(ring, std::atoi(e) & ~127);
+    const WinGeometry geo = win_geometry(RB, reachL, reachU);
+    const int dback = geo.dback, W = geo.W, ring = geo.ring;
+    const bool gy = geo.gy;
     if (ring < 2 * G::kHdr) return false;
 
     std::vector<std::int64_t> itbase(static_cast<std::size_t>(n_sub)), cost(static_cast<std::size_t>(n_sub), 0);
@@ -3346,6 +3393,7 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
         if (want_tma) pc->shape = 4;  // the streamed path's RB; ShapeRec8 if an item would not fit the ring
         if (want_win) {
             pc->shape = 5;
+            pc->win_rb = win_choose_rb(n_rows, vbase, first, firstU);
             if (const char* e = std::getenv("CPDDG_WIN_RB")) pc->win_rb = std::atoi(e) == 8 ? 8 : 16;
         }
         if (!want_win && !smem_y) throw ConfigError("subdomain system too large for the shared-memory solve");
