@@ -84,6 +84,15 @@ constexpr int kExtTile = 256;      // max band nodes per staged-extension tile (
 #define CPDDG_EXT_CAP 4096
 #endif
 constexpr int kExtStageCap = CPDDG_EXT_CAP; // max staged x entries per tile (8 B of shared memory each)
+// grouped extension (k_extend_grouped): chunks of kGrpThreads threads (two
+// band nodes of one stencil base each) touching <= kGrpMax bases; a base's
+// 4x4x4 x block sits at stride kGrpSS doubles, its axis-0 slices at stride
+// kGrpAS (the pads put up to 8 bases' 16-byte words in distinct shared banks)
+constexpr int kGrpThreads = 128;
+constexpr int kHelmNodes = 2;  // active nodes per thread of k_helm_pdl
+constexpr int kGrpMax = 36;
+constexpr int kGrpSS = 82;
+constexpr int kGrpAS = 18;
 
 // Fixed-order block sum: warp shuffles (xor tree) then warp 0 over the 8
 // warp partials.  Deterministic for a fixed blockDim.

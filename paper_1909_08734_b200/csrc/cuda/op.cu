@@ -24,6 +24,7 @@
 
 #include <cmath>
 #include <numeric>
+#include <string>
 
 namespace cpddg {
 
@@ -126,12 +127,13 @@ __device__ __forceinline__ void weights_p3(double t, double* w) {
     w[1] = (t0 * t2 * t3) * 0.5;
     w[2] = -(t0 * t1 * t3) * 0.5;
     w[3] = (t0 * t1 * t2) * (1.0 / 6.0);
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-        if (fabs(t - j) < 1e-12) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) w[k] = (k == j) ? 1.0 : 0.0;
-        }
+    // exact hit: at most one |t - j| < 1e-12; branch-free selects
+    const bool h0 = fabs(t0) < 1e-12, h1 = fabs(t1) < 1e-12, h2 = fabs(t2) < 1e-12, h3 = fabs(t3) < 1e-12;
+    const bool any = h0 || h1 || h2 || h3;
+    w[0] = h0 ? 1.0 : (any ? 0.0 : w[0]);
+    w[1] = h1 ? 1.0 : (any ? 0.0 : w[1]);
+    w[2] = h2 ? 1.0 : (any ? 0.0 : w[2]);
+    w[3] = h3 ? 1.0 : (any ? 0.0 : w[3]);
 }
 
 /** v = E x for p = 3 with four threads per band node (one per offset a of
@@ -249,6 +251,177 @@ __global__ void __launch_bounds__(kExtTile, CPDDG_EXT_MINB) k_extend_staged(int 
         part[a] = __dmul_rn(w0[a], sa);
     }
     v[__ldg(perm + k)] = (part[0] + part[1]) + (part[2] + part[3]);  // k is the tile slot
+}
+
+/** v = E x for d = 3, p = 3, grouped by stencil base: band nodes sorted by
+ *  their stencil base (~8.6 nodes share one at the headline: the nodes along
+ *  a surface normal have nearly the same closest point), two nodes of one
+ *  base per thread; chunk c is the threads' slot pairs [c kGrpNodes,
+ *  (c+1) kGrpNodes) and touches <= kGrpMax bases whose 16 run starts sit at
+ *  a fixed stride.  A CTA stages the 64 x values of each of its bases ONCE
+ *  into shared memory (~7.5 values per node instead of 64); each thread
+ *  reads its base's 4x4x4 block once (128-bit loads; the lanes of one base
+ *  read the same words) and contracts it against both nodes' weights.
+ *  Summation order is k_extend_p3's ((p0 + p1) + (p2 + p3)), so v is
+ *  bit-identical; v is written in band order (the neighbour gathers of
+ *  k_helm stay coalesced along lattice lines).
+ *
+ *  Persistent and software-pipelined (one chunk at a time is load-latency
+ *  bound: run starts -> x gather -> shared -> compute): while chunk c is
+ *  contracted, the x values of the CTA's next chunk are in flight by
+ *  cp.async into the other stage buffer, and the run starts and offsets of
+ *  the chunk after that are in flight into registers. */
+__global__ void __launch_bounds__(kGrpThreads, 4) k_extend_grouped(int nchunks, int ns, const double* __restrict__ t,
+                                                                const unsigned char* __restrict__ gslot,
+                                                                const int* __restrict__ perm,
+                                                                const int* __restrict__ grp_lines,
+                                                                const double* __restrict__ x,
+                                                                double* __restrict__ v) {
+    __shared__ __align__(16) double xs[2][kGrpMax * kGrpSS];
+    constexpr int NT = kGrpThreads, RUNS = kGrpMax * 16, RW = RUNS / (NT / 32), UR = (RW + 31) / 32;
+    static_assert(RW % 8 == 0, "runs per warp must be a multiple of 8");
+    const int G = gridDim.x, lane = threadIdx.x & 31, wr0 = (threadIdx.x >> 5) * RW;
+    int o[UR];  // run starts of this warp's runs wr0 + lane + 32 k
+    double2 tt[3];
+    int gs = 0;
+    int2 pp = make_int2(-1, -1);
+    auto load_meta = [&](int c) {  // run starts, offsets, base slot, band codes of chunk c (registers)
+#pragma unroll
+        for (int u = 0; u < UR; ++u) {
+            const int r = wr0 + lane + 32 * u;
+            o[u] = (c < nchunks && lane + 32 * u < RW) ? __ldg(grp_lines + static_cast<std::size_t>(c) * RUNS + r) : -1;
+        }
+        if (c < nchunks) {
+            const int th = c * kGrpThreads + threadIdx.x;  // slots 2 th, 2 th + 1
+#pragma unroll
+            for (int a = 0; a < 3; ++a) tt[a] = __ldg(reinterpret_cast<const double2*>(t + static_cast<std::size_t>(a) * ns) + th);
+            gs = __ldg(gslot + th);
+            pp = __ldg(reinterpret_cast<const int2*>(perm) + th);
+        }
+    };
+    // x values of the chunk whose run starts are in o: lanes 4q..4q+3 copy
+    // the 4 consecutive values of one run (8 runs, 256 contiguous shared bytes
+    // per instruction), the run start shuffled from the lane that loaded it
+    // x values of the chunk whose run starts are in o: lanes 4q..4q+3 copy
+    // the 4 consecutive values of one run (8 runs, 256 contiguous shared bytes
+    // per instruction), the run start shuffled from the lane that loaded it.
+    // Warp-local run rl = 8 j + lane / 4 is base wr0 / 16 + j / 2, axis-0
+    // offset 2 (j % 2) + lane / 16, axis-1 offset (lane / 4) % 4.
+    static_assert(RW % 16 == 0, "a warp's runs must cover whole bases");
+    const unsigned lane_off = static_cast<unsigned>(
+        ((wr0 >> 4) * kGrpSS + (lane >> 4) * kGrpAS + ((lane >> 2) & 3) * 4 + (lane & 3)) * sizeof(double));
+    const unsigned xs_base = static_cast<unsigned>(__cvta_generic_to_shared(&xs[0][0]));
+    auto issue_stage = [&](int buf) {
+        const unsigned b0 = xs_base + buf * (kGrpMax * kGrpSS * sizeof(double)) + lane_off;
+#pragma unroll
+        for (int j = 0; j < RW / 8; ++j) {
+            const int src = __shfl_sync(0xffffffffu, o[(8 * j) / 32], (8 * j + (lane >> 2)) & 31);
+            const unsigned dst = b0 + ((j >> 1) * kGrpSS + (j & 1) * 2 * kGrpAS) * sizeof(double);
+            if (src >= 0)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(x + src + (lane & 3)) : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    int c = blockIdx.x;
+    load_meta(c);
+    issue_stage(0);
+    double2 tc[3] = {tt[0], tt[1], tt[2]};
+    int gc = gs;
+    int2 pc = pp;
+    load_meta(c + G);
+    for (int it = 0; c < nchunks; ++it, c += G) {
+        issue_stage((it + 1) & 1);  // chunk c + G (empty group past the end)
+        const double2 tn[3] = {tt[0], tt[1], tt[2]};
+        const int gn = gs;
+        const int2 pn = pp;
+        load_meta(c + 2 * G);
+        double wl[2][4], w1[2][4], w0[2][4];
+        weights_p3(tc[2].x, wl[0]);
+        weights_p3(tc[1].x, w1[0]);
+        weights_p3(tc[0].x, w0[0]);
+        weights_p3(tc[2].y, wl[1]);
+        weights_p3(tc[1].y, w1[1]);
+        weights_p3(tc[0].y, w0[1]);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        __syncthreads();
+        double part[2][4];
+        const unsigned X0 = xs_base + ((it & 1) * (kGrpMax * kGrpSS) + gc * kGrpSS) * sizeof(double);
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            double sa[2] = {0.0, 0.0};
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                double2 lo, hi;
+                const unsigned ad = X0 + (a * kGrpAS + b * 4) * sizeof(double);
+                asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(lo.x), "=d"(lo.y) : "r"(ad));
+                asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(hi.x), "=d"(hi.y) : "r"(ad + 16));
+#pragma unroll
+                for (int n = 0; n < 2; ++n) {
+                    double s4 = fma(wl[n][0], lo.x, 0.0);
+                    s4 = fma(wl[n][1], lo.y, s4);
+                    s4 = fma(wl[n][2], hi.x, s4);
+                    s4 = fma(wl[n][3], hi.y, s4);
+                    sa[n] = fma(w1[n][b], s4, sa[n]);
+                }
+            }
+#pragma unroll
+            for (int n = 0; n < 2; ++n) part[n][a] = __dmul_rn(w0[n][a], sa[n]);
+        }
+        if (pc.x >= 0) v[pc.x] = (part[0][0] + part[0][1]) + (part[0][2] + part[0][3]);
+        if (pc.y >= 0) v[pc.y] = (part[1][0] + part[1][1]) + (part[1][2] + part[1][3]);
+        __syncthreads();  // cur is refilled two iterations on
+#pragma unroll
+        for (int a = 0; a < 3; ++a) tc[a] = tn[a];
+        gc = gn;
+        pc = pn;
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+#if __CUDA_ARCH__ >= 900
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+
+/** y = cg x - ih2 sum_k v[nbr_k], kHelmNodes active nodes per thread
+ *  (strided by the block size: coalesced, and all of a thread's loads are
+ *  independent).  Launched with programmatic stream serialization after the
+ *  extension: the neighbour codes and x are loaded before griddepcontrol.wait,
+ *  so their latency overlaps the extension's tail; only the v gathers wait. */
+template <int D>
+__global__ void __launch_bounds__(256) k_helm_pdl(int na, double cg, double ih2, const int* __restrict__ nbr,
+                                                  const double* __restrict__ v, const double* __restrict__ x,
+                                                  double* __restrict__ y) {
+    constexpr int K = kHelmNodes;
+    const int i0 = blockIdx.x * (K * 256) + threadIdx.x;
+    int nb[K][2 * D];
+    double xi[K];
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+        const int i = i0 + q * 256;
+        xi[q] = 0.0;
+        if (i < na) {
+#pragma unroll
+            for (int k = 0; k < 2 * D; ++k) nb[q][k] = __ldg(nbr + static_cast<std::size_t>(k) * na + i);
+            xi[q] = __ldg(x + i);
+        }
+    }
+#if __CUDA_ARCH__ >= 900
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+    double vv[K][2 * D];
+#pragma unroll
+    for (int q = 0; q < K; ++q)
+        if (i0 + q * 256 < na)
+#pragma unroll
+            for (int k = 0; k < 2 * D; ++k) vv[q][k] = v[nb[q][k]];  // written by the preceding kernel: no __ldg
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+        const int i = i0 + q * 256;
+        if (i >= na) continue;
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < 2 * D; ++k) s += vv[q][k];
+        y[i] = cg * xi[q] - ih2 * s;
+    }
 }
 
 /** y = cg x - ih2 sum v[nbr]; if b != nullptr: y <- b - y and partial ||y||^2. */
@@ -388,6 +561,60 @@ static void build_stage(cpddg_op* op, const std::vector<int>& lines, const std::
     CPDDG_CUDA(cudaFuncSetAttribute(k_extend_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, op->ext_smem));
 }
 
+/** Slots of the grouped extension (k_extend_grouped): band nodes sorted by
+ *  stencil base (the run start of offset (0, 0), an active ordinal unique to
+ *  the base), then by code, taken two of one base per thread; chunks of
+ *  kGrpThreads threads touching <= kGrpMax bases (a chunk closes early,
+ *  padded with idle threads, when one more base would not fit; a base cut by
+ *  a chunk boundary is staged in both). */
+static void build_groups(cpddg_op* op, const std::vector<int>& lines, const std::vector<double>& t, int nb) {
+    constexpr int R = 16;
+    std::vector<int> ord(static_cast<std::size_t>(nb));
+    std::iota(ord.begin(), ord.end(), 0);
+    std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return lines[a] < lines[b]; });
+    std::vector<int> perm;     // band code per slot (2 per thread), -1 idle
+    std::vector<int> glines;   // [chunks][kGrpMax][16], -1 unused
+    std::vector<unsigned char> gslot;  // per thread
+    int nbase = 0, used = 0;   // bases / threads of the open chunk
+    for (int q = 0; q < nb;) {
+        const int k = ord[static_cast<std::size_t>(q)];
+        const bool new_base = q == 0 || lines[k] != lines[ord[static_cast<std::size_t>(q) - 1]];
+        if (q == 0 || used == kGrpThreads || (new_base && nbase == kGrpMax)) {
+            perm.resize(perm.size() + 2 * kGrpThreads, -1);
+            gslot.resize(gslot.size() + kGrpThreads, 0);
+            glines.resize(glines.size() + kGrpMax * R, -1);
+            nbase = used = 0;
+        }
+        if (new_base || nbase == 0) {  // first node of a base, or a base continued into a new chunk
+            const std::size_t g = glines.size() - static_cast<std::size_t>(kGrpMax) * R + static_cast<std::size_t>(nbase) * R;
+            for (int l = 0; l < R; ++l) glines[g + l] = lines[static_cast<std::size_t>(l) * nb + k];
+            ++nbase;
+        }
+        const std::size_t th = gslot.size() - kGrpThreads + static_cast<std::size_t>(used++);
+        gslot[th] = static_cast<unsigned char>(nbase - 1);
+        perm[2 * th] = k;
+        ++q;
+        if (q < nb && lines[ord[static_cast<std::size_t>(q)]] == lines[k]) {  // second node of the same base
+            perm[2 * th + 1] = ord[static_cast<std::size_t>(q)];
+            ++q;
+        }
+    }
+    const std::size_t ns = perm.size();
+    std::vector<double> ts(3 * ns, 0.0);
+    for (std::size_t sl = 0; sl < ns; ++sl)
+        if (perm[sl] >= 0)
+            for (int a = 0; a < 3; ++a) ts[static_cast<std::size_t>(a) * ns + sl] = t[static_cast<std::size_t>(a) * nb + perm[sl]];
+    op->grp_t.upload(ts);
+    op->grp_slot.upload(gslot);
+    op->grp_perm.upload(perm);
+    op->grp_lines.upload(glines);
+    op->grp_chunks = static_cast<int>(gslot.size() / kGrpThreads);
+    op->grp_slots = static_cast<int>(ns);
+    int per_sm = 0;
+    CPDDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_extend_grouped, kGrpThreads, 0));
+    op->grp_grid = std::max(1, std::min(op->grp_chunks, std::max(1, per_sm) * sm_count()));
+}
+
 template <int D>
 static void build_tables(cpddg_op* op, const Ix<D>* ix, const Vec<D>* cp, const LatticeMap& map) {
     const int nb = op->na + op->ng, p = op->p, Q = p + 1;
@@ -436,7 +663,16 @@ static void build_tables(cpddg_op* op, const Ix<D>* ix, const Vec<D>* cp, const 
         }
     }
     if constexpr (D == 3) {
-        if (p == 3 && !std::getenv("CPDDG_EXT_GATHER")) build_stage(op, lines, t, nb);
+        // default: grouped by stencil base; CPDDG_EXT=staged / CPDDG_EXT_GATHER=1
+        // keep the round-1 tiled-stage and gather kernels (same v bits)
+        const char* ext = std::getenv("CPDDG_EXT");
+        if (p == 3 && !std::getenv("CPDDG_EXT_GATHER")) {
+            if (ext && std::string(ext) == "staged") {
+                build_stage(op, lines, t, nb);
+            } else {
+                build_groups(op, lines, t, nb);
+            }
+        }
     }
     op->t.upload(t);
     op->lines.upload(lines);
@@ -449,6 +685,9 @@ static void build_tables(cpddg_op* op, const Ix<D>* ix, const Vec<D>* cp, const 
     op->streamed_bytes = 16LL * op->na + (8LL * D + 4LL * nlines) * nb + 16LL * nb + 8LL * D * op->na;
     if (op->ext_tiles)  // staged: 16-bit run starts + one int per staged x
         op->streamed_bytes += (2LL - 4LL) * nlines * nb + 4LL * static_cast<long long>(op->stage_idx.size());
+    if (op->grp_chunks)  // grouped: t + one byte per slot, kGrpMax x 16 run starts per chunk
+        op->streamed_bytes = 16LL * op->na + (8LL * D + 4) * op->grp_slots + op->grp_slots / 2 + 16LL * nb +
+                             8LL * D * op->na + 4LL * static_cast<long long>(op->grp_lines.size());
 }
 
 template <int D>
@@ -456,7 +695,11 @@ static void launch_apply(const cpddg_op* op, const double* x, const double* b, d
                          cudaStream_t st) {
     const int nb = op->na + op->ng;
     const int thr = 256;
-    if (op->ext_tiles) {
+    if (op->grp_chunks) {
+        k_extend_grouped<<<op->grp_grid, kGrpThreads, 0, st>>>(op->grp_chunks, op->grp_slots, op->grp_t.get(),
+                                                                  op->grp_slot.get(), op->grp_perm.get(),
+                                                                  op->grp_lines.get(), x, op->v.get());
+    } else if (op->ext_tiles) {
         k_extend_staged<<<op->ext_tiles, kExtTile, op->ext_smem, st>>>(nb, op->ext_t.get(), op->lines16.get(),
                                                                        op->ext_perm.get(), op->tile_k0.get(),
                                                                        op->stage_base.get(), op->stage_idx.get(), x,
@@ -475,7 +718,20 @@ static void launch_apply(const cpddg_op* op, const double* x, const double* b, d
     CPDDG_CUDA(cudaGetLastError());
     const int rb = reduction_blocks();
     const int grid = std::min(rb, (op->na + kRedThreads - 1) / kRedThreads);
-    if (b)
+    if (!b && op->grp_chunks) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((op->na + kHelmNodes * 256 - 1) / (kHelmNodes * 256));
+        cfg.blockDim = dim3(256);
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        CPDDG_CUDA(cudaLaunchKernelEx(&cfg, k_helm_pdl<D>, op->na, op->cg, op->ih2,
+                                      static_cast<const int*>(op->nbr.get()), static_cast<const double*>(op->v.get()),
+                                      x, y));
+    } else if (b)
         k_helm<D, true><<<rb, kRedThreads, 0, st>>>(op->na, op->cg, op->ih2, op->nbr.get(), op->v.get(), x,
                                                     b, y, op->red.partials.get(), op->red.counter.get(), rn2);
     else

@@ -41,6 +41,13 @@ struct cpddg_op {
     cpddg::DevBuf<double> ext_t;                    // [d][N_B] stencil offsets in slot order
     cpddg::DevBuf<int> stage_base;                  // [tiles+1] first entry of each tile's stage list
     cpddg::DevBuf<int> stage_idx;                   // stage list: active ordinal of each staged x
+    // grouped extension (d = 3, p = 3, the default): band nodes sorted by
+    // stencil base, two of one base per thread (slots 2 th, 2 th + 1)
+    int grp_chunks = 0, grp_slots = 0, grp_grid = 0;  // chunks of kGrpThreads threads (idle slots padded)
+    cpddg::DevBuf<double> grp_t;                    // [d][slots] stencil offsets in slot order
+    cpddg::DevBuf<unsigned char> grp_slot;          // [threads] base of each thread within its chunk
+    cpddg::DevBuf<int> grp_perm;                    // [slots] band code of each slot, -1 idle
+    cpddg::DevBuf<int> grp_lines;                   // [chunks][kGrpMax][16] run starts of the chunk's bases, -1 unused
     cpddg::DevBuf<double> rn2;  // scalar slot for ||b - A x||^2
     cpddg::ReduceWork red;
     std::int64_t alg_bytes = 0, streamed_bytes = 0;
