@@ -69,6 +69,9 @@ typedef struct {
     double tube_radius;   /* <= 0: reference (p+1)/2 sqrt(d) h (interp.hpp:95-98) */
     double c;             /* Helmholtz shift (SolverConfig::c, solve.hpp:31) */
     int workers;          /* host threads for setup; 0 = all */
+    int device_setup;     /* 1: band + closest points (cpddg_setup_create) and alignment + subdomain
+                             sets (cpddg_setup_decompose) built on the current CUDA device,
+                             bit-identical to the host setup; 0: host */
 } cpddg_problem_desc;
 
 /** build_band_tube + build_extension + assemble_helmholtz

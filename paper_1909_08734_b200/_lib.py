@@ -26,7 +26,8 @@ class cpddg_problem_desc(C.Structure):
     _fields_ = [("dim", C.c_int), ("surface", C.c_int), ("radius", C.c_double),
                 ("major_radius", C.c_double), ("minor_radius", C.c_double),
                 ("obj_path", C.c_char_p), ("h", C.c_double), ("p", C.c_int),
-                ("tube_radius", C.c_double), ("c", C.c_double), ("workers", C.c_int)]
+                ("tube_radius", C.c_double), ("c", C.c_double), ("workers", C.c_int),
+                ("device_setup", C.c_int)]
 
 
 class cpddg_band_desc(C.Structure):

@@ -56,12 +56,14 @@ def _stream():
 
 class Problem:
     """Band, E and A of one configuration (BuiltProblem, pipeline.hpp:73-84),
-    plus the decomposition once `decompose` ran.  Host-side and bit-exact
-    with the reference."""
+    plus the decomposition once `decompose` ran.  Bit-exact with the
+    reference; device_setup=True builds the band / closest points and the
+    alignment / subdomain sets on the GPU (bit-identical to the host path)."""
 
     def __init__(self, surface: str = "sphere", h: float = 0.05, p: int = 3, c: float = 1.0,
                  radius: float = 1.0, major_radius: float = 2.0 / 3.0, minor_radius: float = 1.0 / 3.0,
-                 obj_path: str | None = None, tube_radius: float = 0.0, workers: int = 0):
+                 obj_path: str | None = None, tube_radius: float = 0.0, workers: int = 0,
+                 device_setup: bool = False):
         if surface not in SURFACES:
             from .errors import ConfigError
             raise ConfigError(_lib.ERR_CONFIG, f"unknown surface '{surface}'")
@@ -71,7 +73,8 @@ class Problem:
         d = _lib.cpddg_problem_desc(dim=self.dim, surface=SURFACES[surface], radius=radius,
                                     major_radius=major_radius, minor_radius=minor_radius,
                                     obj_path=self._obj, h=h, p=p, tube_radius=tube_radius, c=c,
-                                    workers=workers)
+                                    workers=workers, device_setup=int(bool(device_setup)))
+        self.device_setup = bool(device_setup)
         self._h = C.c_void_p()
         self._destroy = lib().cpddg_setup_destroy
         t0 = time.perf_counter()

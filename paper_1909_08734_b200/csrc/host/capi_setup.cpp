@@ -56,12 +56,18 @@ void create_impl(const cpddg_problem_desc& d, cpddg_setup* s) {
         }
     }
     const auto t0 = std::chrono::steady_clock::now();
-    I->band = build_band_tube<D>(S, d.h, d.p, d.tube_radius, d.workers);
+    if (d.device_setup)
+        I->band = build_band_device<D>(S, d.h, d.p, d.tube_radius, &I->dev);
+    else
+        I->band = build_band_tube<D>(S, d.h, d.p, d.tube_radius, d.workers);
     const auto t1 = std::chrono::steady_clock::now();
     I->E = build_extension<D>(I->band, d.workers);
     const auto t2 = std::chrono::steady_clock::now();
     I->A = assemble_helmholtz<D>(I->band, I->E, d.c, d.workers);
     const auto t3 = std::chrono::steady_clock::now();
+    I->t_band = std::chrono::duration<double>(t1 - t0).count();
+    I->t_E = std::chrono::duration<double>(t2 - t1).count();
+    I->t_A = std::chrono::duration<double>(t3 - t2).count();
     if (std::getenv("CPDDG_VERBOSE"))
         std::fprintf(stderr, "[cpddg] setup: band %.3f s, E %.3f s, A %.3f s\n",
                      std::chrono::duration<double>(t1 - t0).count(), std::chrono::duration<double>(t2 - t1).count(),
@@ -139,6 +145,7 @@ int cpddg_setup_create(const cpddg_problem_desc* desc, cpddg_setup** out) {
         auto s = std::make_unique<cpddg_setup>();
         s->dim = desc->dim;
         s->workers = desc->workers;
+        s->device_setup = desc->device_setup;
         s->c = desc->c;
         if (desc->dim == 2)
             create_impl<2>(*desc, s.get());

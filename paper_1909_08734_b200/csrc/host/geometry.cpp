@@ -310,6 +310,38 @@ Vec<3> TriMesh::feature_normal(int tri, int feat) const {
     return len > 1e-300 ? divide<3>(n, len) : face_n_[tri];
 }
 
+TriMeshTables TriMesh::tables() const {
+    TriMeshTables T;
+    for (const auto& v : verts_) T.verts.insert(T.verts.end(), v.begin(), v.end());
+    for (const auto& v : vert_n_) T.vert_n.insert(T.vert_n.end(), v.begin(), v.end());
+    for (std::size_t t = 0; t < tris_.size(); ++t) {
+        const auto& f = tris_[t];
+        T.tris.insert(T.tris.end(), f.begin(), f.end());
+        T.face_n.insert(T.face_n.end(), face_n_[t].begin(), face_n_[t].end());
+        T.face_ok.push_back(static_cast<unsigned char>(face_ok_[t]));
+        const std::uint64_t ek[3] = {edge_key(f[0], f[1]), edge_key(f[0], f[2]), edge_key(f[1], f[2])};
+        for (std::uint64_t k : ek) {
+            auto it = edge_n_.find(k);
+            const Vec<3> e = it == edge_n_.end() ? Vec<3>{0, 0, 0} : it->second;
+            T.edge_n.insert(T.edge_n.end(), e.begin(), e.end());
+        }
+    }
+    std::vector<std::uint64_t> keys;
+    keys.reserve(cells_.size());
+    for (const auto& kv : cells_) keys.push_back(kv.first);
+    std::sort(keys.begin(), keys.end());
+    T.cell_start.push_back(0);
+    for (std::uint64_t k : keys) {
+        const auto& l = cells_.at(k);
+        T.cell_tris.insert(T.cell_tris.end(), l.begin(), l.end());
+        T.cell_start.push_back(static_cast<int>(T.cell_tris.size()));
+    }
+    T.cell_keys = std::move(keys);
+    T.cell = cell_;
+    T.max_ring = max_ring_;
+    return T;
+}
+
 // geometry.hpp:190-212: expanding cube rings around the query's cell, with
 // the same visiting order (i, j, k nested, shell cells only) and the same
 // stopping rule, so ties resolve to the same triangle.

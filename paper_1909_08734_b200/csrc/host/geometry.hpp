@@ -124,6 +124,23 @@ struct Surface {
     double curvature_bound() const;  // < 0: unknown (triangle meshes)
 };
 
+/** Flattened TriMesh tables for the device closest-point query
+ *  (setup_dev.cu): per triangle its vertices, face normal, validity and the
+ *  three edge pseudo-normals (edges ab, ac, bc = features 3, 4, 5); the
+ *  spatial hash as cell keys (sorted) with CSR triangle lists in the hash's
+ *  insertion order. */
+struct TriMeshTables {
+    std::vector<double> verts, vert_n;   // 3 per vertex
+    std::vector<int> tris;               // 3 per triangle
+    std::vector<double> face_n;          // 3 per triangle
+    std::vector<double> edge_n;          // 9 per triangle
+    std::vector<unsigned char> face_ok;  // 1 per triangle
+    std::vector<std::uint64_t> cell_keys;
+    std::vector<int> cell_start, cell_tris;
+    double cell = 1.0;
+    int max_ring = 0;
+};
+
 /** Triangulated surface (geometry.hpp:120-409): uniform spatial hash, angle-
  *  weighted vertex/edge pseudo-normals, nearest triangle by expanding rings. */
 class TriMesh {
@@ -134,6 +151,7 @@ public:
     const std::vector<Vec<3>>& vertices() const { return verts_; }
     const std::vector<std::array<int, 3>>& triangles() const { return tris_; }
     int degenerate_count() const { return n_degenerate_; }
+    TriMeshTables tables() const;
 
 private:
     std::vector<Vec<3>> verts_;

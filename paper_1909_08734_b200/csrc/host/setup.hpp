@@ -4,6 +4,7 @@
 
 #include "../../../include/cpddg.h"
 #include "decomp.hpp"
+#include "setup_dev.hpp"
 
 #include <memory>
 #include <string>
@@ -11,6 +12,7 @@
 struct cpddg_setup {
     int dim = 0;
     int workers = 0;
+    int device_setup = 0;
     double c = 1.0;
     std::unique_ptr<void, void (*)(void*)> impl{nullptr, [](void*) {}};
 };
@@ -27,6 +29,8 @@ struct SetupImpl {
     bool robin = false;
     std::vector<Subdomain<D>> subs;
     std::vector<LocalSystem> locals;
+    std::shared_ptr<DevBand> dev;  // device band (device_setup)
+    double t_band = 0, t_E = 0, t_A = 0, t_align = 0, t_sets = 0, t_local = 0;  // phase seconds
 };
 
 template <int D>

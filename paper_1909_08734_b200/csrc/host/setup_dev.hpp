@@ -1,0 +1,21 @@
+// Device setup entry points (csrc/cuda/setup_dev.cu), callable from the host
+// setup: the band with its closest points, and the interface alignment and
+// subdomain index sets, built on the GPU and bit-identical to the host
+// restatement (band.cpp, decomp.cpp).
+#pragma once
+
+#include "decomp.hpp"
+
+#include <memory>
+
+namespace cpddg {
+
+struct DevBand;  // device band of a setup (setup_dev.cuh)
+
+/** build_band_tube (band.hpp:150-182) on the device; the host copy is
+ *  returned (with its lattice map), the device band kept in *keep. */
+template <int D>
+Band<D> build_band_device(const Surface<D>& surface, double h, int p, double tube_radius,
+                          std::shared_ptr<DevBand>* keep);
+
+}  // namespace cpddg
