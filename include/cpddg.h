@@ -99,6 +99,9 @@ enum { CPDDG_RAS = 0, CPDDG_ORAS = 1 };
 CPDDG_API int cpddg_setup_decompose(cpddg_setup* s, const int32_t* part, int n_part, int n_overlap, int method,
                           double alpha, double alpha_cross, int32_t* part_out, int* moves);
 CPDDG_API int cpddg_setup_n_subdomains(const cpddg_setup* s);
+/** Phase seconds t[6] = band, E, A (cpddg_setup_create), alignment,
+ *  subdomain sets, local systems (cpddg_setup_decompose). */
+CPDDG_API int cpddg_setup_timings(const cpddg_setup* s, double* t);
 /** counts[8] = |disjoint|, |overlap|, |final_layer|, |ghosts|, |bc|,
  *  fallback_count, n_lambda, #cross_flagged (Subdomain, subdomain.hpp:47-56). */
 CPDDG_API int cpddg_setup_subdomain_counts(const cpddg_setup* s, int j, int32_t* counts);

@@ -137,6 +137,13 @@ class Problem:
         self.method = method
         return out, moves.value
 
+    def phase_seconds(self) -> dict:
+        """Setup phase times of the native layer (band, E, A, alignment,
+        subdomain sets, local systems)."""
+        t = np.zeros(6)
+        check(lib().cpddg_setup_timings(self._h, t))
+        return dict(zip(("band", "E", "A", "align", "sets", "local_systems"), (float(v) for v in t)))
+
     def subdomain(self, j: int) -> dict:
         D = self.dim
         cnt = np.zeros(8, np.int32)

@@ -91,14 +91,27 @@ void decompose_impl(cpddg_setup* s, const int32_t* part, int n_part, int n_overl
     }
     I.part.assign(part, part + I.band.n_active);
     validate_partition(I.part, I.band.n_active);
-    I.moves = align_interfaces<D>(I.band, I.part, I.band.p);
     I.robin = robin;
-    I.subs = build_subdomains<D>(I.band, I.surface, I.part, I.E, n_overlap, robin, s->workers);
+    if (s->device_setup && I.dev) {
+        I.moves = decompose_device<D>(*I.dev, I.band, I.part, n_overlap, robin, I.subs, &I.t_align, &I.t_sets);
+    } else {
+        const auto t0 = std::chrono::steady_clock::now();
+        I.moves = align_interfaces<D>(I.band, I.part, I.band.p);
+        const auto t1 = std::chrono::steady_clock::now();
+        I.subs = build_subdomains<D>(I.band, I.surface, I.part, I.E, n_overlap, robin, s->workers);
+        I.t_align = std::chrono::duration<double>(t1 - t0).count();
+        I.t_sets = std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count();
+    }
+    const auto tl = std::chrono::steady_clock::now();
     TransmissionSpec spec;
     spec.robin = robin;
     spec.alpha = alpha;
     spec.alpha_cross = alpha_cross < 0 ? alpha : alpha_cross;
     I.locals = assemble_locals<D>(I.band, I.A, I.subs, spec, s->workers);
+    I.t_local = std::chrono::duration<double>(std::chrono::steady_clock::now() - tl).count();
+    if (std::getenv("CPDDG_VERBOSE"))
+        std::fprintf(stderr, "[cpddg] decompose: align %.3f s, sets %.3f s, local systems %.3f s\n", I.t_align,
+                     I.t_sets, I.t_local);
     if (part_out) std::copy(I.part.begin(), I.part.end(), part_out);
     if (moves) *moves = I.moves;
 }
@@ -154,6 +167,16 @@ int cpddg_setup_create(const cpddg_problem_desc* desc, cpddg_setup** out) {
         else
             throw ConfigError("dimension must be 2 or 3");
         *out = s.release();
+    });
+}
+
+int cpddg_setup_timings(const cpddg_setup* s, double* t) {
+    return guarded([&] {
+        if (!t) throw InternalError("null argument");
+        dispatch(s, [&](auto& I) {
+            const double v[6] = {I.t_band, I.t_E, I.t_A, I.t_align, I.t_sets, I.t_local};
+            std::copy(v, v + 6, t);
+        });
     });
 }
 

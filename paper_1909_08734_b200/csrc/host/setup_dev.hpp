@@ -18,4 +18,11 @@ template <int D>
 Band<D> build_band_device(const Surface<D>& surface, double h, int p, double tube_radius,
                           std::shared_ptr<DevBand>* keep);
 
+/** align_interfaces (partition.hpp:474-508) and build_subdomains
+ *  (subdomain.hpp:153-313) on the device for the band of `dev` (g is its host
+ *  copy); part is aligned in place; returns the move count. */
+template <int D>
+int decompose_device(const DevBand& dev, const Band<D>& g, std::vector<int>& part, int n_overlap, bool robin_ring,
+                     std::vector<Subdomain<D>>& subs, double* t_align, double* t_sets);
+
 }  // namespace cpddg

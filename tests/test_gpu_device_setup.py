@@ -55,3 +55,45 @@ def test_device_band_is_byte_identical_to_host(name):
         for which in ("E", "A"):
             for a, b in zip(H.csr(which), G.csr(which)):
                 assert a.tobytes() == b.tobytes()
+
+
+DECOMP = {
+    "circle_sectors8_ras": dict(surface="circle", h=0.0125, parts=("sectors", 8), no=2, method="ras"),
+    "circle_sectors8_oras": dict(surface="circle", h=0.0125, parts=("sectors", 8), no=2, method="oras"),
+    "sphere05_rcb64_oras": dict(surface="sphere", h=0.05, parts=("rcb", 64), no=2, method="oras"),
+    "sphere05_rcb64_ras_no3": dict(surface="sphere", h=0.05, parts=("rcb", 64), no=3, method="ras"),
+    "sphere0125_rcb256_oras_no3": dict(surface="sphere", h=0.0125, parts=("rcb", 256), no=3, method="oras"),
+    "sphere0125_rcb32_oras_no3": dict(surface="sphere", h=0.0125, parts=("rcb", 32), no=3, method="oras"),
+    "torus_h0.01_rcb512_oras": dict(surface="torus", h=0.01, major_radius=1.0, minor_radius=0.4,
+                                    parts=("rcb", 512), no=2, method="oras"),
+    "trimesh_h0.01_rcb512_oras": dict(surface="obj", h=0.01, subdiv=6, parts=("rcb", 512), no=2, method="oras"),
+}
+
+
+@pytest.mark.parametrize("name", sorted(DECOMP))
+def test_device_subdomain_sets_are_identical_to_host(name):
+    """align_interfaces + build_subdomains on the device: aligned labels, move
+    count, every index set, every boundary node (integer fields and the bits
+    of x, cp, cp_local, conormal, dq) and every local system equal the host's."""
+    from paper_1909_08734_b200 import inputs
+    w = DECOMP[name]
+    H = _problem(w, False)
+    G = _problem(w, True)
+    cp = H.active_cp
+    kind, n = w["parts"]
+    part = inputs.rcb_partition(cp, n) if kind == "rcb" else inputs.sector_partition(cp, n)
+    ah, mh = H.decompose(part, w["no"], w["method"], 4.0, 40.0)
+    ag, mg = G.decompose(part, w["no"], w["method"], 4.0, 40.0)
+    assert mg == mh and np.array_equal(ag, ah)
+    assert G.n_sub == H.n_sub
+    for j in range(H.n_sub):
+        sh, sg = H.subdomain(j), G.subdomain(j)
+        for k in ("disjoint", "overlap", "final_layer", "ghosts", "bc_int"):
+            assert np.array_equal(sh[k], sg[k]), (j, k)
+        assert sh["bc_real"].tobytes() == sg["bc_real"].tobytes(), j
+        for k in ("fallback_count", "n_lambda", "n_cross_flagged"):
+            assert sh[k] == sg[k], (j, k)
+    for j in range(0, H.n_sub, max(1, H.n_sub // 16)):
+        lh, lg = H.local(j), G.local(j)
+        for k in ("ptr", "col", "val", "scatter_local", "scatter_global"):
+            assert lh[k].tobytes() == lg[k].tobytes(), (j, k)
