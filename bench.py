@@ -74,8 +74,9 @@ def workload_name(w=None):
             f"{w['method']}_a{w['alpha']:g}_ax{w['alpha_cross']:g}_gmres{w['gmres_restart']}_tol{w['rel_tol']:g}")
 
 
-def build_problem(w):
-    """Surface, band, E, A (the device path's host setup) + partition + rhs for config w."""
+def build_problem(w, device_setup=True):
+    """Surface, band, E, A + partition + rhs for config w (band and closest
+    points on the device unless device_setup is False)."""
     from paper_1909_08734_b200 import api, inputs
     obj = None
     if w["surface"] == "obj":
@@ -85,7 +86,7 @@ def build_problem(w):
         inputs.write_obj(obj, v, f)
     P = api.Problem(w["surface"], h=w["h"], p=w["p"], c=w["c"], major_radius=w.get("major_radius", 2 / 3),
                     minor_radius=w.get("minor_radius", 1 / 3), obj_path=obj,
-                    tube_radius=w.get("tube_radius_h", 0.0) * w["h"])
+                    tube_radius=w.get("tube_radius_h", 0.0) * w["h"], device_setup=device_setup)
     cp = P.active_cp
     part = inputs.sector_partition(cp, w["n_subdomains"]) if w["partition"] == "sector" \
         else inputs.rcb_partition(cp, w["n_subdomains"])
@@ -434,7 +435,8 @@ def main():
             "time_to_1e-10_s": t_dev / args.steps, "final_true_relative_residual": final_rel,
             "replicas": world,
             "setup_s": {"problem": t_problem, "decompose": t_decomp, "factor_and_upload": t_locals,
-                        "device_factor": pcs["factor_seconds"], "host_analyse": pcs["analyse_seconds"]},
+                        "device_factor": pcs["factor_seconds"], "host_analyse": pcs["analyse_seconds"],
+                        "phases": P.phase_seconds(), "device_setup": P.device_setup},
             "pc": {k: pcs[k] for k in ("factor_entries", "profile_entries", "factor_bytes", "n_rows_total",
                                        "max_rows", "n_reduced", "max_probe_residual", "apply_mode")},
             "pc_stored_over_profile": pcs["factor_entries"] / pcs["profile_entries"],

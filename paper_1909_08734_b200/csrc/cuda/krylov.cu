@@ -13,6 +13,7 @@
 #include "../host/setup.hpp"
 #include "common.cuh"
 #include "op.cuh"
+#include "setup_dev.cuh"
 
 #include <cooperative_groups.h>
 
@@ -82,7 +83,13 @@ __global__ void __launch_bounds__(kRedThreads) k_mgs(int n, const double* __rest
  *  deterministic (fixed grid).  h[0..m+1] and ||w0||^2 land in `hout`. */
 __global__ void __launch_bounds__(kRedThreads) k_mgs_all(int n, int m, const double* const* __restrict__ V,
                                                          double* __restrict__ w, double* __restrict__ vnext,
-                                                         double* partials, double* hout, double* wn0) {
+                                                         double* partials, double* hout, double* wn0,
+                                                         const int* __restrict__ mdev, double* __restrict__ vin) {
+    if (mdev) {  // device-driven Arnoldi: step from the solver state, V_{m+1} and ||w0||^2 slot follow
+        m = *mdev;
+        vnext = const_cast<double*>(V[m + 1]);
+        wn0 = hout + m + 2;
+    }
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
     __shared__ double sh[kRedThreads / 32];
@@ -132,7 +139,11 @@ __global__ void __launch_bounds__(kRedThreads) k_mgs_all(int n, int m, const dou
     // hprev = ||w||^2 after the last pass: speculative next basis vector
     const double sub = sqrt(hprev);
     if (vnext)
-        for (int i = i0; i < n; i += stride) vnext[i] = w[i] / sub;
+        for (int i = i0; i < n; i += stride) {
+            const double v = w[i] / sub;
+            vnext[i] = v;
+            if (vin) vin[i] = v;
+        }
 }
 
 /** k_mgs_all with the thread's slice of w and of the previous basis vector
@@ -143,7 +154,13 @@ __global__ void __launch_bounds__(kRedThreads) k_mgs_all(int n, int m, const dou
 template <int EPT>
 __global__ void __launch_bounds__(kRedThreads) k_mgs_reg(int n, int m, const double* const* __restrict__ V,
                                                          double* __restrict__ w, double* __restrict__ vnext,
-                                                         double* partials, double* hout, double* wn0) {
+                                                         double* partials, double* hout, double* wn0,
+                                                         const int* __restrict__ mdev, double* __restrict__ vin) {
+    if (mdev) {
+        m = *mdev;
+        vnext = const_cast<double*>(V[m + 1]);
+        wn0 = hout + m + 2;
+    }
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
     __shared__ double sh[kRedThreads / 32];
@@ -219,7 +236,11 @@ __global__ void __launch_bounds__(kRedThreads) k_mgs_reg(int n, int m, const dou
         const int i = i0 + k * stride;
         if (i < n) {
             w[i] = wr[k];
-            if (vnext) vnext[i] = wr[k] / sub;
+            if (vnext) {
+                const double v = wr[k] / sub;
+                vnext[i] = v;
+                if (vin) vin[i] = v;
+            }
         }
     }
 }
@@ -230,7 +251,13 @@ __global__ void __launch_bounds__(kRedThreads) k_mgs_reg(int n, int m, const dou
 template <int NT>
 __global__ void __launch_bounds__(NT) k_mgs_block(int n, int m, const double* const* __restrict__ V,
                                                   double* __restrict__ w, double* __restrict__ vnext,
-                                                  double* hout, double* wn0) {
+                                                  double* hout, double* wn0, const int* __restrict__ mdev,
+                                                  double* __restrict__ vin) {
+    if (mdev) {
+        m = *mdev;
+        vnext = const_cast<double*>(V[m + 1]);
+        wn0 = hout + m + 2;
+    }
     __shared__ double sh[NT / 32];
     __shared__ double hb;
     double hprev = 0.0;
@@ -260,7 +287,11 @@ __global__ void __launch_bounds__(NT) k_mgs_block(int n, int m, const double* co
     }
     const double sub = sqrt(hprev);
     if (vnext)
-        for (int i = threadIdx.x; i < n; i += NT) vnext[i] = w[i] / sub;
+        for (int i = threadIdx.x; i < n; i += NT) {
+            const double v = w[i] / sub;
+            vnext[i] = v;
+            if (vin) vin[i] = v;
+        }
 }
 
 __global__ void k_scale(int n, const double* __restrict__ src, double s, double* __restrict__ dst) {
@@ -279,6 +310,98 @@ __global__ void k_combine(int n, int m, const double* const* __restrict__ vptr, 
 
 __global__ void k_axpy1(int n, const double* __restrict__ x, double* __restrict__ y) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) y[i] += x[i];
+}
+
+/** dst = src / s and dst2 = src / s (the first basis vector and the fixed
+ *  preconditioner input of the device-driven Arnoldi loop). */
+__global__ void k_scale2(int n, const double* __restrict__ src, double s, double* __restrict__ dst,
+                         double* __restrict__ dst2) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const double v = src[i] / s;
+        dst[i] = v;
+        dst2[i] = v;
+    }
+}
+
+/** Device state of one GMRES cycle run as a CUDA graph (layout of the
+ *  solver-state buffer, in doubles: [0, 8) this struct, then H (cap x cap,
+ *  column k = rotated Hessenberg column of step k), cs, sn (cap), g
+ *  (cap + 1), est (cap: |g_{k+1}| after step k), stamps (4 cap int64). */
+struct GState {
+    int m, total, cycle, max_iter, status, pad;
+    double target, pad2;
+};
+constexpr int kGHead = 8;
+static_assert(sizeof(GState) <= kGHead * sizeof(double), "GState layout");
+enum { kGRun = 0, kGBasisNonFinite = 1, kGEstNonFinite = 2, kGConverged = 3 };
+
+__global__ void k_gstate_init(double* gb, int cap, int total, int cycle, int max_iter, double target, double beta) {
+    GState* S = reinterpret_cast<GState*>(gb);
+    S->m = 0;
+    S->total = total;
+    S->cycle = cycle;
+    S->max_iter = max_iter;
+    S->status = kGRun;
+    S->target = target;
+    double* g = gb + kGHead + static_cast<std::size_t>(cap) * cap + 2 * cap;
+    g[0] = beta;
+}
+
+/** Arnoldi step m's Givens update on the device (the host loop of
+ *  solve.hpp:165-200 / gmres() below, same operations in the same order,
+ *  round-to-nearest intrinsics: no contraction, so the rotated estimates are
+ *  bitwise those of the host loop; hypot is glibc's algorithm, as the host's
+ *  std::hypot).  Sets the while-condition of the cycle graph: continue while
+ *  not converged, no breakdown, m < cycle and total < max_iter. */
+__global__ void k_givens(double* gb, int cap, const double* __restrict__ hd, cudaGraphConditionalHandle cond) {
+    if (threadIdx.x != 0) return;
+    GState* S = reinterpret_cast<GState*>(gb);
+    double* H = gb + kGHead;
+    double* cs = H + static_cast<std::size_t>(cap) * cap;
+    double* sn = cs + cap;
+    double* g = sn + cap;
+    double* est = g + cap + 1;
+    const int m = S->m;
+    double* h = H + static_cast<std::size_t>(m) * cap;
+    for (int i = 0; i <= m; ++i) h[i] = hd[i];
+    h[m + 1] = sqrt(hd[m + 1]);
+    const double wnorm0 = sqrt(hd[m + 2]);
+    const double subdiag = h[m + 1];
+    int status = kGRun;
+    if (!isfinite(subdiag)) {
+        status = kGBasisNonFinite;
+    } else {
+        for (int i = 0; i < m; ++i) {
+            const double t = __dadd_rn(__dmul_rn(cs[i], h[i]), __dmul_rn(sn[i], h[i + 1]));
+            h[i + 1] = __dadd_rn(__dmul_rn(-sn[i], h[i]), __dmul_rn(cs[i], h[i + 1]));
+            h[i] = t;
+        }
+        const double denom = hypot_glibc(h[m], h[m + 1]);
+        cs[m] = denom == 0 ? 1.0 : __ddiv_rn(h[m], denom);
+        sn[m] = denom == 0 ? 0.0 : __ddiv_rn(h[m + 1], denom);
+        h[m] = denom;
+        g[m + 1] = __dmul_rn(-sn[m], g[m]);
+        g[m] = __dmul_rn(cs[m], g[m]);
+        S->m = m + 1;
+        S->total += 1;
+        const double e = fabs(g[m + 1]);
+        est[m] = e;
+        if (!isfinite(e))
+            status = kGEstNonFinite;
+        else if (e <= S->target || subdiag <= __dmul_rn(1e-14, wnorm0))
+            status = kGConverged;
+    }
+    S->status = status;
+    const bool more = status == kGRun && S->m < S->cycle && S->total < S->max_iter;
+    cudaGraphSetConditional(cond, more ? 1u : 0u);
+}
+
+/** Device timestamp (profiling of the graph loop): stamps[4 m + slot]. */
+__global__ void k_stamp(const double* gb, long long* stamps, int slot) {
+    if (threadIdx.x != 0) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    stamps[4 * reinterpret_cast<const GState*>(gb)->m + slot] = static_cast<long long>(t);
 }
 
 void check_finite(double v, const char* what) {
@@ -414,9 +537,53 @@ struct Workspace {
         CPDDG_CUDA(cudaGetLastError());
         ++launches;
     }
-    DevBuf<double> mgs_partials;
-    int coop_grid = 0;
-    void mgs_all(int m, double* w, double* vnext, double* hout, double* wn0) {
+    // persistent (KrylovCache): the cycle graph keeps pointers into them
+    DevBuf<double>& mgs_partials = kc.mgs_partials;
+    int& coop_grid = kc.coop_grid;
+    /** mgs_all with the step read from *mdev on the device (V_{m+1} and the
+     *  ||w0||^2 slot follow from it; the new basis vector is also copied to
+     *  vin): the launch parameters do not depend on the step, so it can sit
+     *  in a captured loop body.  The basis table must cover V_0..V_{cap}. */
+    void mgs_all_dev(int mmax, double* w, double* hout, const int* mdev, double* vin) {
+        mgs_all(mmax, w, nullptr, hout, nullptr, mdev, vin);
+    }
+    void mgs_all(int m, double* w, double* vnext, double* hout, double* wn0, const int* mdev = nullptr,
+                 double* vin = nullptr) {
+        prepare_mgs(m);
+        int nn = n, mm = m;
+        const double* const* vpd = kc.vptr.get();
+        if (n <= kSmallMgs) {
+            k_mgs_block<1024><<<1, 1024, 0, st>>>(nn, mm, vpd, w, vnext, hout, wn0, mdev, vin);
+            CPDDG_CUDA(cudaGetLastError());
+            ++launches;
+            return;
+        }
+        double* part = mgs_partials.get();
+        void* args[] = {&nn, &mm, &vpd, &w, &vnext, &part, &hout, &wn0, &mdev, &vin};
+        // register-resident w: up to 8 elements per thread of the cooperative grid
+        static const bool streamed = [] {
+            const char* e = std::getenv("CPDDG_MGS");  // development: "stream" = k_mgs_all
+            return e && std::string(e) == "stream";
+        }();
+        const long long threads = static_cast<long long>(coop_grid) * kRedThreads;
+        const int ept = static_cast<int>((n + threads - 1) / threads);
+        const void* kern = reinterpret_cast<const void*>(k_mgs_all);
+        if (!streamed && ept <= 8)
+            kern = ept <= 1   ? reinterpret_cast<const void*>(k_mgs_reg<1>)
+                   : ept <= 2 ? reinterpret_cast<const void*>(k_mgs_reg<2>)
+                   : ept <= 4 ? reinterpret_cast<const void*>(k_mgs_reg<4>)
+                              : reinterpret_cast<const void*>(k_mgs_reg<8>);
+        if (kern != reinterpret_cast<const void*>(k_mgs_all)) {
+            int per_sm = 0;  // the whole grid must be resident
+            CPDDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRedThreads, 0));
+            if (per_sm * sm_count() < coop_grid) kern = reinterpret_cast<const void*>(k_mgs_all);
+        }
+        CPDDG_CUDA(cudaLaunchCooperativeKernel(kern, dim3(coop_grid), dim3(kRedThreads), args, 0, st));
+        ++launches;
+    }
+    /** Cooperative grid size, per-pass partials (m + 2 passes) and the basis
+     *  pointer table for steps up to m. */
+    void prepare_mgs(int m) {
         if (coop_grid == 0) {
             int per_sm = 0;
             CPDDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mgs_all, kRedThreads, 0));
@@ -440,36 +607,16 @@ struct Workspace {
             CPDDG_CUDA(cudaMemcpy(kc.vptr.get(), vp.data(), sizeof(double*) * vp.size(), cudaMemcpyHostToDevice));
             kc.vptr_valid = static_cast<int>(vp.size());
         }
-        int nn = n, mm = m;
-        const double* const* vpd = kc.vptr.get();
-        if (n <= kSmallMgs) {
-            k_mgs_block<1024><<<1, 1024, 0, st>>>(nn, mm, vpd, w, vnext, hout, wn0);
-            CPDDG_CUDA(cudaGetLastError());
-            ++launches;
-            return;
-        }
-        double* part = mgs_partials.get();
-        void* args[] = {&nn, &mm, &vpd, &w, &vnext, &part, &hout, &wn0};
-        // register-resident w: up to 8 elements per thread of the cooperative grid
-        static const bool streamed = [] {
-            const char* e = std::getenv("CPDDG_MGS");  // development: "stream" = k_mgs_all
-            return e && std::string(e) == "stream";
-        }();
-        const long long threads = static_cast<long long>(coop_grid) * kRedThreads;
-        const int ept = static_cast<int>((n + threads - 1) / threads);
-        const void* kern = reinterpret_cast<const void*>(k_mgs_all);
-        if (!streamed && ept <= 8)
-            kern = ept <= 1   ? reinterpret_cast<const void*>(k_mgs_reg<1>)
-                   : ept <= 2 ? reinterpret_cast<const void*>(k_mgs_reg<2>)
-                   : ept <= 4 ? reinterpret_cast<const void*>(k_mgs_reg<4>)
-                              : reinterpret_cast<const void*>(k_mgs_reg<8>);
-        if (kern != reinterpret_cast<const void*>(k_mgs_all)) {
-            int per_sm = 0;  // the whole grid must be resident
-            CPDDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRedThreads, 0));
-            if (per_sm * sm_count() < coop_grid) kern = reinterpret_cast<const void*>(k_mgs_all);
-        }
-        CPDDG_CUDA(cudaLaunchCooperativeKernel(kern, dim3(coop_grid), dim3(kRedThreads), args, 0, st));
-        ++launches;
+    }
+    /** Upload the full basis pointer table (V_0 .. V_{mmax} and beyond). */
+    void refresh_vptr(int mmax) {
+        for (int k = 0; k <= mmax; ++k) basis(k);
+        std::vector<const double*> vp(kc.V.size());
+        for (std::size_t k = 0; k < kc.V.size(); ++k) vp[k] = kc.V[k].get();
+        if (kc.vptr.size() < vp.size()) kc.vptr.alloc(vp.size() + 64);
+        CPDDG_CUDA(cudaMemcpyAsync(kc.vptr.get(), vp.data(), sizeof(double*) * vp.size(), cudaMemcpyHostToDevice, st));
+        CPDDG_CUDA(cudaStreamSynchronize(st));
+        kc.vptr_valid = static_cast<int>(vp.size());
     }
     void scale(const double* src, double s, double* dst) {
         k_scale<<<grid, kRedThreads, 0, st>>>(n, src, s, dst);
@@ -499,11 +646,235 @@ void record(cpddg_log* log, const std::vector<double>& res, int iters, bool conv
 
 }  // namespace
 
+/** Build (or reuse) the cycle graph: a while-conditional node whose body is
+ *  one Arnoldi step with device-resident control -- z = M^-1 vin, w = A z,
+ *  the cooperative MGS (step m read from the state; V_{m+1} also into vin)
+ *  and k_givens, which sets the loop condition.  A GMRES(cycle) cycle is one
+ *  graph launch: no host round trip per step. */
+static void ensure_cycle_graph(cpddg_op* op, cpddg_pc* pc, Workspace& ws, int cycle, int cap, bool prof) {
+    KrylovCache& kc = op->kc;
+    ws.refresh_vptr(cycle);  // fixed addresses for V_0..V_cycle, table uploaded before any capture
+    if (kc.vin.size() < static_cast<std::size_t>(ws.n)) kc.vin.alloc(static_cast<std::size_t>(ws.n));
+    const std::size_t gsz0 = kGHead + static_cast<std::size_t>(cap) * cap + 2 * cap + (cap + 1) + cap + 4 * cap;
+    if (kc.gstate.size() < gsz0) kc.gstate.alloc(gsz0);
+    ws.prepare_mgs(cycle);  // cooperative grid and partials allocated before any capture
+    // every device address the captured body uses: a reallocation forces a rebuild
+    const std::vector<const void*> sig{pc, kc.scal.get(), kc.vptr.get(), kc.gstate.get(), kc.w.get(), kc.tmp.get(),
+                                       kc.vin.get(), kc.V[0].get(), kc.mgs_partials.get()};
+    if (kc.gexec && kc.gcycle == cycle && kc.gprof == (prof ? 1 : 0) && kc.gn == ws.n && kc.gsig == sig) return;
+    if (kc.gexec) {
+        cudaGraphExecDestroy(kc.gexec);
+        kc.gexec = nullptr;
+    }
+    if (kc.graph) {
+        cudaGraphDestroy(kc.graph);
+        kc.graph = nullptr;
+    }
+    if (!kc.gstream) CPDDG_CUDA(cudaStreamCreateWithFlags(&kc.gstream, cudaStreamNonBlocking));
+    const int n = ws.n;
+    const std::size_t gsz = gsz0;
+    CPDDG_CUDA(cudaGraphCreate(&kc.graph, 0));
+    cudaGraphConditionalHandle cond;
+    CPDDG_CUDA(cudaGraphConditionalHandleCreate(&cond, kc.graph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = cond;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    CPDDG_CUDA(cudaGraphAddNode(&node, kc.graph, nullptr, 0, &np));
+    cudaGraph_t body = np.conditional.phGraph_out[0];
+    cudaStream_t cs = kc.gstream;
+    double* gb = kc.gstate.get();
+    const int* mdev = reinterpret_cast<const int*>(gb);  // GState::m
+    long long* stamps = reinterpret_cast<long long*>(gb + kGHead + static_cast<std::size_t>(cap) * cap + 2 * cap +
+                                                     (cap + 1) + cap);
+    double* hd = ws.kc.scal.get();
+    CPDDG_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    const cudaStream_t saved = ws.st;
+    ws.st = cs;
+    try {
+        if (prof) k_stamp<<<1, 32, 0, cs>>>(gb, stamps, 0);
+        const double* z = kc.vin.get();
+        if (pc) {
+            pc_apply(pc, kc.vin.get(), kc.tmp.get(), false, cs);
+            z = kc.tmp.get();
+        }
+        if (prof) k_stamp<<<1, 32, 0, cs>>>(gb, stamps, 1);
+        op_apply(op, z, kc.w.get(), cs, false);
+        if (prof) k_stamp<<<1, 32, 0, cs>>>(gb, stamps, 2);
+        ws.mgs_all_dev(cycle, kc.w.get(), hd, mdev, kc.vin.get());
+        k_givens<<<1, 32, 0, cs>>>(gb, cap, hd, cond);
+        CPDDG_CUDA(cudaGetLastError());
+    } catch (...) {
+        ws.st = saved;
+        cudaGraph_t dummy;
+        cudaStreamEndCapture(cs, &dummy);
+        throw;
+    }
+    ws.st = saved;
+    CPDDG_CUDA(cudaStreamEndCapture(cs, &body));
+    CPDDG_CUDA(cudaGraphInstantiate(&kc.gexec, kc.graph, 0));
+    // the MGS partials may have been (re)allocated by the captured launch
+    kc.gsig = {pc, kc.scal.get(), kc.vptr.get(), kc.gstate.get(), kc.w.get(), kc.tmp.get(),
+               kc.vin.get(), kc.V[0].get(), kc.mgs_partials.get()};
+    kc.gpc = pc;
+    kc.gcycle = cycle;
+    kc.gprof = prof ? 1 : 0;
+    kc.gn = n;
+    if (kc.ghost_n < gsz) {
+        if (kc.ghost) cudaFreeHost(kc.ghost);
+        CPDDG_CUDA(cudaMallocHost(&kc.ghost, sizeof(double) * gsz));
+        kc.ghost_n = gsz;
+    }
+}
+
+/** solve.hpp:128-214 with each restart cycle run as one graph launch
+ *  (ensure_cycle_graph).  Same arithmetic as the host loop below, in the
+ *  same order: residual histories and solutions are bitwise identical
+ *  (tests/test_gpu_parity.py::test_graph_gmres_matches_host_loop). */
+static void gmres_graph(cpddg_op* op, cpddg_pc* pc, const double* b, double* u, const cpddg_solve_params& prm,
+                        cpddg_log* log, cudaStream_t st) {
+    const int n = op->na;
+    const int max_iter = prm.max_iter;
+    const int cycle = std::max(1, std::min(prm.restart > 0 ? prm.restart : max_iter, max_iter));
+    Workspace ws(n, st, op->kc);
+    const int cap = cycle + 2;
+    ws.reserve(cap);
+    const bool prof = prm.profile_kernels != 0;
+    ensure_cycle_graph(op, pc, ws, cycle, cap, prof);
+    KrylovCache& kc = op->kc;
+    double* gb = kc.gstate.get();
+    double* nd = ws.kc.scal.get() + cap;  // [1] ||r||^2
+    DevBuf<double>& r = ws.kc.r;
+    DevBuf<double>& tmp = ws.kc.tmp;
+    KernelTimer kt(op->kc.events);
+    kt.on = prof;
+    kt.st = st;
+    Timer timer(st);
+    CPDDG_CUDA(cudaMemsetAsync(u, 0, sizeof(double) * n, st));
+    CPDDG_CUDA(cudaMemcpyAsync(r.get(), b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    double* hp = ws.kc.host;
+    auto fetch = [&](const double* dev, int cnt) {
+        CPDDG_CUDA(cudaMemcpyAsync(hp, dev, sizeof(double) * cnt, cudaMemcpyDeviceToHost, st));
+        CPDDG_CUDA(cudaStreamSynchronize(st));
+    };
+    ws.mgs(nullptr, nullptr, r.get(), nullptr, nd + 1, nullptr);
+    fetch(nd + 1, 1);
+    double rnorm = std::sqrt(hp[0]);
+    std::vector<double> residuals{rnorm};
+    const double beta0 = rnorm;
+    int total = 0;
+    bool converged = false;
+    if (beta0 == 0.0) {
+        record(log, residuals, 0, true, 0.0, timer.stop(), ws.launches);
+        return;
+    }
+    const double target = prm.rel_tol * beta0;
+    const std::size_t off_cs = kGHead + static_cast<std::size_t>(cap) * cap;
+    const std::size_t off_g = off_cs + 2 * cap, off_est = off_g + cap + 1, off_st = off_est + cap;
+    const std::size_t gsz = off_st + 4 * cap;
+    double pc_graph_s = 0, op_graph_s = 0;
+    std::int64_t pc_graph_n = 0, op_graph_n = 0;
+    std::vector<const double*> vptr_h(static_cast<std::size_t>(cap));
+    while (total < max_iter && !converged) {
+        const double beta = rnorm;
+        check_finite(beta, "gmres residual");
+        if (beta <= target) {
+            converged = true;
+            break;
+        }
+        k_scale2<<<ws.grid, kRedThreads, 0, st>>>(n, r.get(), beta, ws.basis(0), kc.vin.get());
+        k_gstate_init<<<1, 1, 0, st>>>(gb, cap, total, cycle, max_iter, target, beta);
+        CPDDG_CUDA(cudaGetLastError());
+        CPDDG_CUDA(cudaGraphLaunch(kc.gexec, st));
+        ws.launches += 2;
+        CPDDG_CUDA(cudaMemcpyAsync(kc.ghost, gb, sizeof(double) * gsz, cudaMemcpyDeviceToHost, st));
+        CPDDG_CUDA(cudaStreamSynchronize(st));
+        const GState* S = reinterpret_cast<const GState*>(kc.ghost);
+        const int m = S->m;
+        ws.launches += static_cast<std::int64_t>(m) * (4 + (prof ? 3 : 0));
+        total = S->total;
+        for (int k = 0; k < m; ++k) residuals.push_back(kc.ghost[off_est + k]);
+        if (S->status == kGBasisNonFinite) throw DivergenceError("gmres basis norm is not finite");
+        if (S->status == kGEstNonFinite) throw DivergenceError("gmres residual estimate is not finite");
+        if (prof) {
+            const long long* stp = reinterpret_cast<const long long*>(kc.ghost + off_st);
+            for (int k = 0; k < m; ++k) {
+                pc_graph_s += 1e-9 * static_cast<double>(stp[4 * k + 1] - stp[4 * k]);
+                op_graph_s += 1e-9 * static_cast<double>(stp[4 * k + 2] - stp[4 * k + 1]);
+            }
+            pc_graph_n += pc ? m : 0;
+            op_graph_n += m;
+        }
+        converged = S->status == kGConverged;
+        if (m > 0) {
+            const double* H = kc.ghost + kGHead;
+            const double* g = kc.ghost + off_g;
+            std::vector<double> y(static_cast<std::size_t>(m), 0.0);
+            for (int i = m - 1; i >= 0; --i) {
+                double sacc = g[i];
+                for (int k = i + 1; k < m; ++k) sacc -= H[static_cast<std::size_t>(k) * cap + i] * y[static_cast<std::size_t>(k)];
+                if (H[static_cast<std::size_t>(i) * cap + i] == 0.0)
+                    throw DivergenceError("gmres encountered a singular projection");
+                y[static_cast<std::size_t>(i)] = sacc / H[static_cast<std::size_t>(i) * cap + i];
+            }
+            double* yh = ws.kc.host + 2 * (cap + 4);
+            for (int k = 0; k < m; ++k) {
+                vptr_h[static_cast<std::size_t>(k)] = ws.basis(k);
+                yh[k] = y[static_cast<std::size_t>(k)];
+            }
+            CPDDG_CUDA(cudaMemcpyAsync(ws.kc.vptr.get(), vptr_h.data(), sizeof(double*) * m, cudaMemcpyHostToDevice, st));
+            CPDDG_CUDA(cudaMemcpyAsync(ws.kc.yd.get(), yh, sizeof(double) * m, cudaMemcpyHostToDevice, st));
+            k_combine<<<ws.grid, kRedThreads, 0, st>>>(n, m, ws.kc.vptr.get(), ws.kc.yd.get(), tmp.get());
+            CPDDG_CUDA(cudaGetLastError());
+            ++ws.launches;
+            if (pc) {
+                kt.time(true, [&] { pc_apply(pc, tmp.get(), u, true, st); });
+            } else {
+                k_axpy1<<<ws.grid, kRedThreads, 0, st>>>(n, tmp.get(), u);
+                CPDDG_CUDA(cudaGetLastError());
+            }
+            ++ws.launches;
+            CPDDG_CUDA(cudaStreamSynchronize(st));
+            // (the update rewrote entries 0..m-1 of the pointer table with the
+            // same basis pointers the graph's MGS reads)
+        }
+        kt.time(false, [&] { op_residual(op, b, u, r.get(), nd + 1, st); });
+        ws.launches += 2;
+        fetch(nd + 1, 1);
+        kt.collect();
+        rnorm = std::sqrt(hp[0]);
+    }
+    const double secs = timer.stop();
+    kt.collect();
+    kt.pc_s += pc_graph_s;
+    kt.pc_n += pc_graph_n;
+    kt.op_s += op_graph_s;
+    kt.op_n += op_graph_n;
+    record(log, residuals, total, converged, rnorm, secs, ws.launches, &kt);
+}
+
 // solve.hpp:128-214
 static void gmres(cpddg_op* op, cpddg_pc* pc, const double* b, double* u, const cpddg_solve_params& prm,
                   cpddg_log* log, cudaStream_t st) {
     const int n = op->na;
     if (pc && pc->n_global != n) throw InternalError("preconditioner size does not match the operator");
+    {
+        // default: device-driven cycles (one CUDA graph launch per restart
+        // cycle); CPDDG_GMRES_GRAPH=0 or CPDDG_GMRES_SYNC=1 select the host
+        // loop.  Kernel profiling (per-launch CUDA events) runs the host loop
+        // unless CPDDG_GMRES_GRAPH=1 (then device timestamps in the graph)
+        const char* ge = std::getenv("CPDDG_GMRES_GRAPH");
+        const char* se = std::getenv("CPDDG_GMRES_SYNC");
+        const bool forced = ge && std::string(ge) == "1";
+        const bool host_loop = (ge && std::string(ge) == "0") || (se && std::string(se) == "1") ||
+                               (prm.profile_kernels && !forced);
+        if (!host_loop && prm.max_iter > 0) {
+            gmres_graph(op, pc, b, u, prm, log, st);
+            return;
+        }
+    }
     const int max_iter = prm.max_iter;
     const int cycle = prm.restart > 0 ? prm.restart : max_iter;
     Workspace ws(n, st, op->kc);

@@ -692,7 +692,7 @@ static void build_tables(cpddg_op* op, const Ix<D>* ix, const Vec<D>* cp, const 
 
 template <int D>
 static void launch_apply(const cpddg_op* op, const double* x, const double* b, double* y, double* rn2,
-                         cudaStream_t st) {
+                         cudaStream_t st, bool pdl = true) {
     const int nb = op->na + op->ng;
     const int thr = 256;
     if (op->grp_chunks) {
@@ -727,7 +727,7 @@ static void launch_apply(const cpddg_op* op, const double* x, const double* b, d
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
-        cfg.numAttrs = 1;
+        cfg.numAttrs = pdl ? 1 : 0;
         CPDDG_CUDA(cudaLaunchKernelEx(&cfg, k_helm_pdl<D>, op->na, op->cg, op->ih2,
                                       static_cast<const int*>(op->nbr.get()), static_cast<const double*>(op->v.get()),
                                       x, y));
@@ -741,11 +741,11 @@ static void launch_apply(const cpddg_op* op, const double* x, const double* b, d
     CPDDG_CUDA(cudaGetLastError());
 }
 
-void op_apply(const cpddg_op* op, const double* x, double* y, cudaStream_t st) {
+void op_apply(const cpddg_op* op, const double* x, double* y, cudaStream_t st, bool pdl) {
     if (op->dim == 2)
-        launch_apply<2>(op, x, nullptr, y, nullptr, st);
+        launch_apply<2>(op, x, nullptr, y, nullptr, st, pdl);
     else
-        launch_apply<3>(op, x, nullptr, y, nullptr, st);
+        launch_apply<3>(op, x, nullptr, y, nullptr, st, pdl);
 }
 
 void op_residual(const cpddg_op* op, const double* b, const double* x, double* r, double* rn2_dev,

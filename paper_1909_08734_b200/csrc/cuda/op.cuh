@@ -18,9 +18,28 @@ struct KrylovCache {
     int host_cap = 0;
     cpddg::ReduceWork red;
     std::vector<cudaEvent_t> events;  // per-launch timing events (profile_kernels), created once
+    // device-driven GMRES cycle: a CUDA graph whose while-node body is one
+    // Arnoldi step (preconditioner, operator, MGS, Givens); rebuilt when the
+    // preconditioner, the cycle length or the profiling mode changes
+    cpddg::DevBuf<double> mgs_partials;  // per-pass block partials of the cooperative MGS
+    int coop_grid = 0;
+    cpddg::DevBuf<double> gstate;     // GState + H + cs + sn + g + est + stamps
+    cpddg::DevBuf<double> vin;        // the step's preconditioner input (= V_m)
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t gexec = nullptr;
+    cudaStream_t gstream = nullptr;   // capture stream
+    const void* gpc = nullptr;
+    int gcycle = -1, gprof = -1, gn = -1;
+    std::vector<const void*> gsig;    // device addresses captured in the body
+    double* ghost = nullptr;          // pinned copy of the state after a cycle
+    std::size_t ghost_n = 0;
     ~KrylovCache() {
         if (host) cudaFreeHost(host);
+        if (ghost) cudaFreeHost(ghost);
         for (auto e : events) cudaEventDestroy(e);
+        if (gexec) cudaGraphExecDestroy(gexec);
+        if (graph) cudaGraphDestroy(graph);
+        if (gstream) cudaStreamDestroy(gstream);
     }
 };
 
@@ -124,7 +143,9 @@ struct cpddg_pc {
 };
 
 namespace cpddg {
-void op_apply(const cpddg_op* op, const double* x, double* y, cudaStream_t st);
+/** y = A x.  pdl: launch the Helmholtz kernel as a programmatic dependent
+ *  of the extension (off inside captured graphs). */
+void op_apply(const cpddg_op* op, const double* x, double* y, cudaStream_t st, bool pdl = true);
 /** r = b - A x and ||r||^2 into *rn2_dev (device scalar). */
 void op_residual(const cpddg_op* op, const double* b, const double* x, double* r, double* rn2_dev,
                  cudaStream_t st);

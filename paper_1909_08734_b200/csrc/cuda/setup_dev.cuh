@@ -95,31 +95,44 @@ __device__ __forceinline__ double ddist(const double* a, const double* b) {
     return dnorm<D>(d);
 }
 
-/** glibc's hypot (>= 2.35, dbl-64 without FMA: Borges' corrected
- *  algorithm), which the host's std::hypot calls; valid for the lattice
- *  range (no huge / tiny scaling branch is reachable).  Verified against
- *  std::hypot on 12 M lattice points. */
-__device__ __forceinline__ double hypot_glibc(double x, double y) {
-    double ax = fabs(x), ay = fabs(y);
-    if (ax < ay) {
-        const double t = ax;
-        ax = ay;
-        ay = t;
-    }
-    if (ay <= ax * 0x1p-54) return ax + ay;
-    double h = sqrt(ax * ax + ay * ay);
+/** glibc's hypot (>= 2.35, sysdeps dbl-64 without FMA: Borges' corrected
+ *  algorithm), which the host's std::hypot calls.  Written with explicit
+ *  round-to-nearest intrinsics, so it is exact in any translation unit
+ *  (no FMA contraction).  The common path is verified against std::hypot on
+ *  12 M lattice points; the scaling branches restate glibc's
+ *  published structure (huge > 2^511, tiny < 2^-511). */
+__device__ __forceinline__ double hypot_kernel(double ax, double ay) {
+    double h = sqrt(__dadd_rn(__dmul_rn(ax, ax), __dmul_rn(ay, ay)));
     double t1, t2;
-    if (h <= 2.0 * ay) {
-        const double delta = h - ay;
-        t1 = ax * (2.0 * delta - ax);
-        t2 = (delta - 2.0 * (ax - ay)) * delta;
+    if (h <= __dmul_rn(2.0, ay)) {
+        const double delta = __dsub_rn(h, ay);
+        t1 = __dmul_rn(ax, __dsub_rn(__dmul_rn(2.0, delta), ax));
+        t2 = __dmul_rn(__dsub_rn(delta, __dmul_rn(2.0, __dsub_rn(ax, ay))), delta);
     } else {
-        const double delta = h - ax;
-        t1 = 2.0 * delta * (ax - 2.0 * ay);
-        t2 = (4.0 * delta - ay) * ay + delta * delta;
+        const double delta = __dsub_rn(h, ax);
+        t1 = __dmul_rn(__dmul_rn(2.0, delta), __dsub_rn(ax, __dmul_rn(2.0, ay)));
+        t2 = __dadd_rn(__dmul_rn(__dsub_rn(__dmul_rn(4.0, delta), ay), ay), __dmul_rn(delta, delta));
     }
-    h -= (t1 + t2) / (2.0 * h);
-    return h;
+    return __dsub_rn(h, __ddiv_rn(__dadd_rn(t1, t2), __dmul_rn(2.0, h)));
+}
+__device__ __forceinline__ double hypot_glibc(double x, double y) {
+    if (!isfinite(x) || !isfinite(y)) {
+        if ((isinf(x) || isinf(y))) return __longlong_as_double(0x7ff0000000000000LL);
+        return __dadd_rn(x, y);
+    }
+    x = fabs(x);
+    y = fabs(y);
+    double ax = x < y ? y : x, ay = x < y ? x : y;
+    if (ax > 0x1p+511) {
+        if (ay <= __dmul_rn(ax, 0x1p-54)) return __dadd_rn(ax, ay);
+        return __ddiv_rn(hypot_kernel(__dmul_rn(ax, 0x1p-600), __dmul_rn(ay, 0x1p-600)), 0x1p-600);
+    }
+    if (ay < 0x1p-511) {
+        if (ax >= __ddiv_rn(ay, 0x1p-54)) return __dadd_rn(ax, ay);
+        return __dmul_rn(hypot_kernel(__ddiv_rn(ax, 0x1p-600), __ddiv_rn(ay, 0x1p-600)), 0x1p-600);
+    }
+    if (ay <= __dmul_rn(ax, 0x1p-54)) return __dadd_rn(ax, ay);
+    return hypot_kernel(ax, ay);
 }
 
 /** round_cp (geometry.cpp; reference geometry.hpp:56-63, 88-93). */

@@ -285,6 +285,47 @@ def test_pipelined_gmres_matches_synchronous_loop(monkeypatch):
         assert torch.equal(a.u, s.u)
 
 
+@pytest.mark.parametrize("name", ["circle_oras_gmres", "sphere05_oras_gmres", "sphere05_ras_gmres"])
+def test_graph_gmres_matches_host_loop(name, monkeypatch):
+    """Device-driven cycles (one CUDA graph launch per restart cycle: the
+    Arnoldi step's Givens update, convergence and breakdown tests on the
+    device, a while-conditional node) reproduce the host-driven loop
+    (CPDDG_GMRES_GRAPH=0) bit for bit: residual histories, iteration counts,
+    solutions; with restarts and with the profiling stamps."""
+    g, cfg, P, A, M, torch = _setup(name)
+    from paper_1909_08734_b200 import api
+    b = torch.from_numpy(g["b"]).cuda()
+    for restart in (50, 7):
+        d = api.gmres_solve(A, b, M, 1e-10, 500, restart)
+        monkeypatch.setenv("CPDDG_GMRES_GRAPH", "1")  # profiled graph: device timestamps
+        dp = api.gmres_solve(A, b, M, 1e-10, 500, restart, profile=True)
+        monkeypatch.setenv("CPDDG_GMRES_GRAPH", "0")
+        h = api.gmres_solve(A, b, M, 1e-10, 500, restart)
+        monkeypatch.delenv("CPDDG_GMRES_GRAPH")
+        assert d.log.iterations == h.log.iterations and d.log.converged == h.log.converged
+        assert np.array_equal(np.asarray(d.log.residuals), np.asarray(h.log.residuals))
+        assert torch.equal(d.u, h.u) and torch.equal(d.u, dp.u)
+        assert d.log.final_true_residual == h.log.final_true_residual
+        kt = dp.log.kernel_times
+        assert kt["pc_launches"] >= dp.log.iterations and kt["pc_seconds"] > 0 and kt["op_seconds"] > 0
+
+
+def test_graph_gmres_short_cycles_and_max_iter(monkeypatch):
+    """Cycle and max_iter limits inside the graph loop: max_iter reached in the
+    middle of a cycle (not converged), restart 1, and max_iter = 1."""
+    g, cfg, P, A, M, torch = _setup("sphere05_oras_gmres")
+    from paper_1909_08734_b200 import api
+    b = torch.from_numpy(g["b"]).cuda()
+    for restart, mi in ((50, 13), (1, 9), (5, 1), (3, 8)):
+        d = api.gmres_solve(A, b, M, 1e-10, mi, restart)
+        monkeypatch.setenv("CPDDG_GMRES_GRAPH", "0")
+        h = api.gmres_solve(A, b, M, 1e-10, mi, restart)
+        monkeypatch.delenv("CPDDG_GMRES_GRAPH")
+        assert d.log.iterations == h.log.iterations == mi and not d.log.converged
+        assert np.array_equal(np.asarray(d.log.residuals), np.asarray(h.log.residuals))
+        assert torch.equal(d.u, h.u)
+
+
 def test_run_solve_pipeline_with_files(tmp_path):
     """run_solve (pipeline.hpp:183-241) fed through a partition file and an rhs
     file, writing the reference's output files."""
