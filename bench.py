@@ -104,6 +104,21 @@ def peaks():
     return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
+def oracle_lu_ratio(w, stored):
+    """Stored factor entries / sum of nnz(L + U) of the oracle's SuperLU-COLAMD
+    factors (profiles/r02_factor_format.json, scripts/oracle_lu_fill.py;
+    SURVEY.md 8(d)), when the committed figure is for this workload."""
+    p = os.path.join(ROOT, "profiles", "r02_factor_format.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as fh:
+        d = json.load(fh)
+    if d.get("config") != workload_name(w):
+        return None
+    return {"ratio_entries": stored / d["sum_nnz_LU"], "oracle_sum_nnz_LU": d["sum_nnz_LU"],
+            "ratio_bytes_vs_12B_per_nz": 8.0 * stored / (12.0 * d["sum_nnz_LU"]), "source": "profiles/r02_factor_format.json"}
+
+
 def ncu_traffic():
     """DRAM bytes per k_solve launch from the committed ncu --set full capture."""
     p = os.path.join(ROOT, "profiles", "ncu_k_solve.json")
@@ -440,6 +455,7 @@ def main():
             "pc": {k: pcs[k] for k in ("factor_entries", "profile_entries", "factor_bytes", "n_rows_total",
                                        "max_rows", "n_reduced", "max_probe_residual", "apply_mode")},
             "pc_stored_over_profile": pcs["factor_entries"] / pcs["profile_entries"],
+            "pc_stored_over_oracle_lu": oracle_lu_ratio(WORKLOAD, pcs["factor_entries"]),
             "kernel_ms": {"pc_apply_avg": 1e3 * avg_pc, "op_apply_avg": 1e3 * op_s / max(op_n, 1)},
             "op_roofline_GBs": op_alg / (op_s / max(op_n, 1)) / 1e9 if op_n else None,
         },
