@@ -1,0 +1,38 @@
+"""North-star scale points: the headline sphere
+at the BASELINE tube radius sqrt(17) h (663,454 DOF) against the oracle
+restatement's full solve (tests/golden/make_scale_points.py: iteration count,
+solution sample to 1e-8), with the device setup (band, alignment and
+subdomain sets on the GPU)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+
+def test_headline_sqrt17h_matches_oracle():
+    import torch
+
+    from paper_1909_08734_b200 import api, inputs
+    path = os.path.join(GOLDEN, "scale_points.json")
+    if not os.path.exists(path):
+        pytest.skip("no scale-point reference (tests/golden/make_scale_points.py)")
+    ref = json.load(open(path))["headline_r17"]
+    sample = np.load(os.path.join(GOLDEN, "scale_headline_r17.npz"))["u_sample"]
+    P = api.Problem("sphere", h=0.0125, p=3, c=1.0, tube_radius=17 ** 0.5 * 0.0125, device_setup=True)
+    assert (P.n_active, P.n_ghost) == (ref["n_active"], ref["n_ghost"])
+    cp = P.active_cp
+    _, moves = P.decompose(inputs.rcb_partition(cp, 256), 3, "oras", 4.0, 40.0)
+    assert moves == ref["align_moves"]
+    A = api.DeviceHelmholtz.from_problem(P)
+    M = api.SchwarzPreconditioner.from_problem(P)
+    b_host = inputs.rhs_sphere(cp)
+    r = api.gmres_solve(A, torch.from_numpy(b_host).cuda(), M, 1e-10, 2000, 50)
+    assert r.log.converged and abs(r.log.iterations - ref["iterations"]) <= 2
+    u = r.u.cpu().numpy()
+    assert np.max(np.abs(u[::ref["sample_stride"]] - sample)) <= 1e-8 * ref["u_norm_inf"]
+    assert abs(np.linalg.norm(u) - ref["u_norm2"]) <= 1e-8 * ref["u_norm2"]
