@@ -396,6 +396,44 @@ __global__ void k_givens(double* gb, int cap, const double* __restrict__ hd, cud
     cudaGraphSetConditional(cond, more ? 1u : 0u);
 }
 
+/** Stationary iteration state (stationary_graph): [0, 8) this struct, then
+ *  the residual history (max_iter + 1 entries). */
+struct SState {
+    int it, max_iter, status, pad;
+    double r0, target;
+};
+enum { kSRun = 0, kSNonFinite = 1, kSDiverged = 2, kSConverged = 3 };
+
+/** One stationary step's checks on the device (solve.hpp:112-121, the host
+ *  loop's order): rn = sqrt(||r||^2), finite, divergence (> 1e8 r0),
+ *  convergence (<= rel_tol r0); sets the loop condition. */
+__global__ void k_stat_check(double* sb, const double* __restrict__ rn2, cudaGraphConditionalHandle cond) {
+    if (threadIdx.x != 0) return;
+    SState* S = reinterpret_cast<SState*>(sb);
+    const double rn = sqrt(*rn2);
+    const int it = S->it + 1;
+    S->it = it;
+    sb[8 + it] = rn;
+    int status = kSRun;
+    if (!isfinite(rn))
+        status = kSNonFinite;
+    else if (rn > __dmul_rn(1e8, S->r0))
+        status = kSDiverged;
+    else if (rn <= S->target)
+        status = kSConverged;
+    S->status = status;
+    cudaGraphSetConditional(cond, (status == kSRun && it < S->max_iter) ? 1u : 0u);
+}
+
+__global__ void k_sstate_init(double* sb, int max_iter, double r0, double target) {
+    SState* S = reinterpret_cast<SState*>(sb);
+    S->it = 0;
+    S->max_iter = max_iter;
+    S->status = kSRun;
+    S->r0 = r0;
+    S->target = target;
+}
+
 /** Device timestamp (profiling of the graph loop): stamps[4 m + slot]. */
 __global__ void k_stamp(const double* gb, long long* stamps, int slot) {
     if (threadIdx.x != 0) return;
@@ -1050,12 +1088,103 @@ static void gmres(cpddg_op* op, cpddg_pc* pc, const double* b, double* u, const 
     record(log, residuals, total, converged, rnorm, secs, ws.launches, &kt);
 }
 
+/** solve.hpp:95-123 as one CUDA-graph launch: a while-conditional node whose
+ *  body is u += M r, r = b - A u with ||r||^2, and the device checks
+ *  (k_stat_check).  The graph is built per call (b, u are captured); the
+ *  residual history comes back once at the end.  Bitwise equal to the host
+ *  loop below (tests/test_gpu_parity.py::test_graph_stationary_matches_host_loop). */
+static void stationary_graph(cpddg_op* op, cpddg_pc* pc, const double* b, double* u, const cpddg_solve_params& prm,
+                             cpddg_log* log, cudaStream_t st) {
+    const int n = op->na;
+    Workspace ws(n, st, op->kc);
+    ws.reserve(2);
+    KrylovCache& kc = op->kc;
+    DevBuf<double>& r = ws.kc.r;
+    double* rn2 = ws.kc.scal.get();
+    Timer timer(st);
+    CPDDG_CUDA(cudaMemsetAsync(u, 0, sizeof(double) * n, st));
+    CPDDG_CUDA(cudaMemcpyAsync(r.get(), b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    ws.mgs(nullptr, nullptr, r.get(), nullptr, rn2, nullptr);
+    double* hp = ws.kc.host;
+    CPDDG_CUDA(cudaMemcpyAsync(hp, rn2, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CPDDG_CUDA(cudaStreamSynchronize(st));
+    const double r0 = std::sqrt(hp[0]);
+    std::vector<double> residuals{r0};
+    if (r0 == 0.0) {
+        record(log, residuals, 0, true, 0.0, timer.stop(), ws.launches);
+        return;
+    }
+    const std::size_t ssz = 8 + static_cast<std::size_t>(prm.max_iter) + 1;
+    DevBuf<double> sb(ssz);
+    if (!kc.gstream) CPDDG_CUDA(cudaStreamCreateWithFlags(&kc.gstream, cudaStreamNonBlocking));
+    cudaGraph_t graph;
+    CPDDG_CUDA(cudaGraphCreate(&graph, 0));
+    cudaGraphExec_t exec = nullptr;
+    struct Guard {
+        cudaGraph_t& g;
+        cudaGraphExec_t& e;
+        ~Guard() {
+            if (e) cudaGraphExecDestroy(e);
+            cudaGraphDestroy(g);
+        }
+    } guard{graph, exec};
+    cudaGraphConditionalHandle cond;
+    CPDDG_CUDA(cudaGraphConditionalHandleCreate(&cond, graph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = cond;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    CPDDG_CUDA(cudaGraphAddNode(&node, graph, nullptr, 0, &np));
+    cudaGraph_t body = np.conditional.phGraph_out[0];
+    cudaStream_t cs = kc.gstream;
+    CPDDG_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    try {
+        pc_apply(pc, r.get(), u, true, cs);
+        op_residual(op, b, u, r.get(), rn2, cs);
+        k_stat_check<<<1, 32, 0, cs>>>(sb.get(), rn2, cond);
+        CPDDG_CUDA(cudaGetLastError());
+    } catch (...) {
+        cudaGraph_t dummy;
+        cudaStreamEndCapture(cs, &dummy);
+        throw;
+    }
+    CPDDG_CUDA(cudaStreamEndCapture(cs, &body));
+    CPDDG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    k_sstate_init<<<1, 1, 0, st>>>(sb.get(), prm.max_iter, r0, prm.rel_tol * r0);
+    CPDDG_CUDA(cudaGetLastError());
+    if (prm.max_iter > 0) CPDDG_CUDA(cudaGraphLaunch(exec, st));
+    std::vector<double> hs(ssz);
+    CPDDG_CUDA(cudaMemcpyAsync(hs.data(), sb.get(), sizeof(double) * ssz, cudaMemcpyDeviceToHost, st));
+    CPDDG_CUDA(cudaStreamSynchronize(st));
+    const SState* S = reinterpret_cast<const SState*>(hs.data());
+    const int iters = S->it;
+    for (int k = 1; k <= iters; ++k) residuals.push_back(hs[8 + static_cast<std::size_t>(k)]);
+    ws.launches += 2 + static_cast<std::int64_t>(iters) * 4;
+    if (S->status == kSNonFinite) throw DivergenceError("stationary residual is not finite");
+    if (S->status == kSDiverged) throw DivergenceError("stationary iteration diverged");
+    const double rn = residuals.back();
+    const double secs = timer.stop();
+    record(log, residuals, iters, S->status == kSConverged, iters ? rn : r0, secs, ws.launches);
+}
+
 // solve.hpp:95-123
 static void stationary(cpddg_op* op, cpddg_pc* pc, const double* b, double* u, const cpddg_solve_params& prm,
                        cpddg_log* log, cudaStream_t st) {
     const int n = op->na;
     if (!pc) throw InternalError("stationary iteration needs a preconditioner");
     if (pc->n_global != n) throw InternalError("preconditioner size does not match the operator");
+    {
+        // default: one graph launch for the whole iteration (see gmres() for the switches)
+        const char* ge = std::getenv("CPDDG_GMRES_GRAPH");
+        const bool forced = ge && std::string(ge) == "1";
+        const bool host_loop = (ge && std::string(ge) == "0") || (prm.profile_kernels && !forced);
+        if (!host_loop) {
+            stationary_graph(op, pc, b, u, prm, log, st);
+            return;
+        }
+    }
     Workspace ws(n, st, op->kc);
     ws.reserve(2);
     struct {

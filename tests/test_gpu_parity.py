@@ -310,6 +310,23 @@ def test_graph_gmres_matches_host_loop(name, monkeypatch):
         assert kt["pc_launches"] >= dp.log.iterations and kt["pc_seconds"] > 0 and kt["op_seconds"] > 0
 
 
+@pytest.mark.parametrize("name", ["circle_ras_stationary", "sphere10_oras_stationary"])
+def test_graph_stationary_matches_host_loop(name, monkeypatch):
+    """The stationary iteration as one graph launch (device checks, while
+    node) reproduces the host-driven loop bit for bit."""
+    g, cfg, P, A, M, torch = _setup(name)
+    from paper_1909_08734_b200 import api
+    b = torch.from_numpy(g["b"]).cuda()
+    for mi in (int(cfg.get("max_iter", 500)), 7, 0):
+        d = api.stationary_solve(A, b, M, 1e-10, mi)
+        monkeypatch.setenv("CPDDG_GMRES_GRAPH", "0")
+        h = api.stationary_solve(A, b, M, 1e-10, mi)
+        monkeypatch.delenv("CPDDG_GMRES_GRAPH")
+        assert d.log.iterations == h.log.iterations and d.log.converged == h.log.converged
+        assert np.array_equal(np.asarray(d.log.residuals), np.asarray(h.log.residuals))
+        assert torch.equal(d.u, h.u) and d.log.final_true_residual == h.log.final_true_residual
+
+
 def test_graph_gmres_short_cycles_and_max_iter(monkeypatch):
     """Cycle and max_iter limits inside the graph loop: max_iter reached in the
     middle of a cycle (not converged), restart 1, and max_iter = 1."""
