@@ -89,7 +89,7 @@ constexpr int kExtStageCap = CPDDG_EXT_CAP; // max staged x entries per tile (8 
 // 4x4x4 x block sits at stride kGrpSS doubles, its axis-0 slices at stride
 // kGrpAS (the pads put up to 8 bases' 16-byte words in distinct shared banks)
 constexpr int kGrpThreads = 128;
-constexpr int kHelmNodes = 2;  // active nodes per thread of k_helm_pdl
+constexpr int kUnionMax = 768;   // staged x values per chunk of k_extend_union
 constexpr int kGrpMax = 36;
 constexpr int kGrpSS = 82;
 constexpr int kGrpAS = 18;

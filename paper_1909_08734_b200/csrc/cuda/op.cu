@@ -381,47 +381,150 @@ __global__ void __launch_bounds__(kGrpThreads, 4) k_extend_grouped(int nchunks, 
 #endif
 }
 
-/** y = cg x - ih2 sum_k v[nbr_k], kHelmNodes active nodes per thread
- *  (strided by the block size: coalesced, and all of a thread's loads are
- *  independent).  Launched with programmatic stream serialization after the
- *  extension: the neighbour codes and x are loaded before griddepcontrol.wait,
- *  so their latency overlaps the extension's tail; only the v gathers wait. */
+/** v = E x for d = 3, p = 3, grouped by stencil base with a UNION stage:
+ *  slots as k_extend_grouped (two nodes of one stencil base per thread,
+ *  chunks of kGrpThreads threads), but a chunk stages the union of its
+ *  bases' x runs -- consecutive bases share most of their lattice lines, so
+ *  ~2.8 staged values per node instead of 64 per base (11 per node) -- as one
+ *  sorted list of active ordinals at a fixed stride (coalesced cp.async,
+ *  mostly consecutive sources); each base addresses its 16 runs by 16-bit
+ *  offsets into the stage.  Same pipeline (next chunk's x in flight by
+ *  cp.async, the one after's tables in registers) and the same summation
+ *  order: v is bit-identical to the gather kernel. */
+__global__ void __launch_bounds__(kGrpThreads, 4) k_extend_union(int nchunks, int ns, const double* __restrict__ t,
+                                                              const unsigned char* __restrict__ gslot,
+                                                              const int* __restrict__ perm,
+                                                              const int* __restrict__ stage,
+                                                              const unsigned short* __restrict__ roff,
+                                                              const double* __restrict__ x,
+                                                              double* __restrict__ v) {
+    __shared__ __align__(16) double xs[2][kUnionMax];
+    constexpr int NT = kGrpThreads, UR = kUnionMax / NT;
+    const int G = gridDim.x;
+    int o[UR];
+    double2 tt[3];
+    uint4 ro[2];
+    int2 pp = make_int2(-1, -1);
+    auto load_meta = [&](int c) {
+        if (c >= nchunks) {
+#pragma unroll
+            for (int u = 0; u < UR; ++u) o[u] = -1;
+            return;
+        }
+#pragma unroll
+        for (int u = 0; u < UR; ++u) o[u] = __ldg(stage + static_cast<std::size_t>(c) * kUnionMax + threadIdx.x + u * NT);
+        const int th = c * kGrpThreads + threadIdx.x;  // slots 2 th, 2 th + 1
+#pragma unroll
+        for (int a = 0; a < 3; ++a) tt[a] = __ldg(reinterpret_cast<const double2*>(t + static_cast<std::size_t>(a) * ns) + th);
+        const int gs = __ldg(gslot + th);
+        const uint4* rp = reinterpret_cast<const uint4*>(roff + (static_cast<std::size_t>(c) * kGrpMax + gs) * 16);
+        ro[0] = __ldg(rp);
+        ro[1] = __ldg(rp + 1);
+        pp = __ldg(reinterpret_cast<const int2*>(perm) + th);
+    };
+    const unsigned xs_base = static_cast<unsigned>(__cvta_generic_to_shared(&xs[0][0]));
+    auto issue_stage = [&](int buf) {
+        const unsigned b0 = xs_base + static_cast<unsigned>((buf * kUnionMax + threadIdx.x) * 8);
+#pragma unroll
+        for (int u = 0; u < UR; ++u)
+            if (o[u] >= 0)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(b0 + static_cast<unsigned>(u * NT * 8)),
+                             "l"(x + o[u])
+                             : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    int c = blockIdx.x;
+    load_meta(c);
+    issue_stage(0);
+    double2 tc[3] = {tt[0], tt[1], tt[2]};
+    uint4 rc[2] = {ro[0], ro[1]};
+    int2 pc = pp;
+    load_meta(c + G);
+    for (int it = 0; c < nchunks; ++it, c += G) {
+        issue_stage((it + 1) & 1);  // chunk c + G (nothing past the end)
+        const double2 tn[3] = {tt[0], tt[1], tt[2]};
+        const uint4 rn[2] = {ro[0], ro[1]};
+        const int2 pn = pp;
+        load_meta(c + 2 * G);
+        double wl[2][4], w1[2][4], w0[2][4];
+        weights_p3(tc[2].x, wl[0]);
+        weights_p3(tc[1].x, w1[0]);
+        weights_p3(tc[0].x, w0[0]);
+        weights_p3(tc[2].y, wl[1]);
+        weights_p3(tc[1].y, w1[1]);
+        weights_p3(tc[0].y, w0[1]);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        __syncthreads();
+        const double* X = xs[it & 1];
+        const unsigned rw[8] = {rc[0].x, rc[0].y, rc[0].z, rc[0].w, rc[1].x, rc[1].y, rc[1].z, rc[1].w};
+        double part[2][4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            double sa[2] = {0.0, 0.0};
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const int r = a * 4 + b;
+                const int off = (rw[r >> 1] >> (16 * (r & 1))) & 0xffff;
+                const double x0 = X[off], x1 = X[off + 1], x2 = X[off + 2], x3 = X[off + 3];
+#pragma unroll
+                for (int n = 0; n < 2; ++n) {
+                    double s4 = fma(wl[n][0], x0, 0.0);
+                    s4 = fma(wl[n][1], x1, s4);
+                    s4 = fma(wl[n][2], x2, s4);
+                    s4 = fma(wl[n][3], x3, s4);
+                    sa[n] = fma(w1[n][b], s4, sa[n]);
+                }
+            }
+#pragma unroll
+            for (int n = 0; n < 2; ++n) part[n][a] = __dmul_rn(w0[n][a], sa[n]);
+        }
+        if (pc.x >= 0) v[pc.x] = (part[0][0] + part[0][1]) + (part[0][2] + part[0][3]);
+        if (pc.y >= 0) v[pc.y] = (part[1][0] + part[1][1]) + (part[1][2] + part[1][3]);
+        __syncthreads();  // this buffer is refilled two iterations on
+#pragma unroll
+        for (int a = 0; a < 3; ++a) tc[a] = tn[a];
+        rc[0] = rn[0];
+        rc[1] = rn[1];
+        pc = pn;
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+#if __CUDA_ARCH__ >= 900
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+
+/** y = cg x - ih2 sum_k v[nbr_k], one active node per thread, the 2d
+ *  neighbour codes of a node contiguous ([N_A][2d], 8-byte loads: a warp's
+ *  codes are one contiguous 768-byte run).  Launched with programmatic
+ *  stream serialization after the extension: codes and x are loaded before
+ *  griddepcontrol.wait, so their latency overlaps the extension's tail; only
+ *  the v gathers wait for it.  Same summation order as k_helm. */
 template <int D>
-__global__ void __launch_bounds__(256) k_helm_pdl(int na, double cg, double ih2, const int* __restrict__ nbr,
+__global__ void __launch_bounds__(256) k_helm_pdl(int na, double cg, double ih2, const int2* __restrict__ nbr2,
                                                   const double* __restrict__ v, const double* __restrict__ x,
                                                   double* __restrict__ y) {
-    constexpr int K = kHelmNodes;
-    const int i0 = blockIdx.x * (K * 256) + threadIdx.x;
-    int nb[K][2 * D];
-    double xi[K];
+    const int i = blockIdx.x * 256 + threadIdx.x;
+    int2 nb[D];
+    double xi = 0.0;
+    if (i < na) {
 #pragma unroll
-    for (int q = 0; q < K; ++q) {
-        const int i = i0 + q * 256;
-        xi[q] = 0.0;
-        if (i < na) {
-#pragma unroll
-            for (int k = 0; k < 2 * D; ++k) nb[q][k] = __ldg(nbr + static_cast<std::size_t>(k) * na + i);
-            xi[q] = __ldg(x + i);
-        }
+        for (int k = 0; k < D; ++k) nb[k] = __ldg(nbr2 + static_cast<std::size_t>(i) * D + k);
+        xi = __ldg(x + i);
     }
 #if __CUDA_ARCH__ >= 900
     asm volatile("griddepcontrol.wait;" ::: "memory");
 #endif
-    double vv[K][2 * D];
+    if (i >= na) return;
+    double vv[2 * D];
 #pragma unroll
-    for (int q = 0; q < K; ++q)
-        if (i0 + q * 256 < na)
-#pragma unroll
-            for (int k = 0; k < 2 * D; ++k) vv[q][k] = v[nb[q][k]];  // written by the preceding kernel: no __ldg
-#pragma unroll
-    for (int q = 0; q < K; ++q) {
-        const int i = i0 + q * 256;
-        if (i >= na) continue;
-        double s = 0.0;
-#pragma unroll
-        for (int k = 0; k < 2 * D; ++k) s += vv[q][k];
-        y[i] = cg * xi[q] - ih2 * s;
+    for (int k = 0; k < D; ++k) {
+        vv[2 * k] = v[nb[k].x];  // written by the preceding kernel: no __ldg
+        vv[2 * k + 1] = v[nb[k].y];
     }
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 2 * D; ++k) s += vv[k];
+    y[i] = cg * xi - ih2 * s;
 }
 
 /** y = cg x - ih2 sum v[nbr]; if b != nullptr: y <- b - y and partial ||y||^2. */
@@ -615,6 +718,111 @@ static void build_groups(cpddg_op* op, const std::vector<int>& lines, const std:
     op->grp_grid = std::max(1, std::min(op->grp_chunks, std::max(1, per_sm) * sm_count()));
 }
 
+/** Slots and union stages of k_extend_union: band nodes sorted by stencil
+ *  base (then by code), two of one base per thread; a chunk closes when its
+ *  kGrpThreads threads are used, at kGrpMax bases, or when the next base's
+ *  runs would push the union stage past kUnionMax values (a base cut by a
+ *  chunk boundary is staged in both). */
+static void build_union(cpddg_op* op, const std::vector<int>& lines, const std::vector<double>& t, int nb) {
+    constexpr int R = 16;
+    std::vector<int> ord(static_cast<std::size_t>(nb));
+    std::iota(ord.begin(), ord.end(), 0);
+    std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return lines[a] < lines[b]; });
+    std::vector<int> perm, stage;                 // per slot / [chunks][kUnionMax]
+    std::vector<unsigned short> roff;             // [chunks][kGrpMax][16]
+    std::vector<unsigned char> gslot;             // per thread
+    std::vector<int> mark(static_cast<std::size_t>(op->na), -1), members, base_nodes;
+    int nbase = 0, used = 0, chunk = -1;
+    auto run_start = [&](int k, int l) { return lines[static_cast<std::size_t>(l) * nb + k]; };
+    auto new_values = [&](int k) {  // staged values base k would add to the open chunk
+        int add = 0;
+        for (int l = 0; l < R; ++l)
+            for (int q = 0; q < 4; ++q) {
+                const int ov = run_start(k, l) + q;
+                if (mark[static_cast<std::size_t>(ov)] != chunk) {
+                    mark[static_cast<std::size_t>(ov)] = -2 - chunk;  // provisional
+                    ++add;
+                }
+            }
+        for (int l = 0; l < R; ++l)
+            for (int q = 0; q < 4; ++q) {
+                const int ov = run_start(k, l) + q;
+                if (mark[static_cast<std::size_t>(ov)] == -2 - chunk) mark[static_cast<std::size_t>(ov)] = -1;
+            }
+        return add;
+    };
+    auto close_chunk = [&] {
+        if (chunk < 0) return;
+        std::sort(members.begin(), members.end());
+        const std::size_t s0 = static_cast<std::size_t>(chunk) * kUnionMax;
+        for (std::size_t q = 0; q < members.size(); ++q) stage[s0 + q] = members[q];
+        for (int b = 0; b < nbase; ++b)
+            for (int l = 0; l < R; ++l) {
+                const int o = run_start(base_nodes[static_cast<std::size_t>(b)], l);
+                const std::size_t pos = static_cast<std::size_t>(std::lower_bound(members.begin(), members.end(), o) - members.begin());
+                roff[(static_cast<std::size_t>(chunk) * kGrpMax + b) * R + l] = static_cast<unsigned short>(pos);
+            }
+        for (int m : members) mark[static_cast<std::size_t>(m)] = -1;
+        members.clear();
+        base_nodes.clear();
+    };
+    auto open_chunk = [&] {
+        close_chunk();
+        ++chunk;
+        perm.resize(perm.size() + 2 * kGrpThreads, -1);
+        gslot.resize(gslot.size() + kGrpThreads, 0);
+        stage.resize(stage.size() + kUnionMax, -1);
+        roff.resize(roff.size() + static_cast<std::size_t>(kGrpMax) * R, 0);
+        nbase = used = 0;
+    };
+    for (int q = 0; q < nb;) {
+        const int k = ord[static_cast<std::size_t>(q)];
+        const bool new_base = q == 0 || lines[k] != lines[ord[static_cast<std::size_t>(q) - 1]];
+        if (chunk < 0 || used == kGrpThreads || (new_base && nbase == kGrpMax) ||
+            ((new_base || nbase == 0) && static_cast<int>(members.size()) + new_values(k) > kUnionMax))
+            open_chunk();
+        if (new_base || nbase == 0) {
+            for (int l = 0; l < R; ++l)
+                for (int c = 0; c < 4; ++c) {
+                    const int ov = run_start(k, l) + c;
+                    if (mark[static_cast<std::size_t>(ov)] != chunk) {
+                        mark[static_cast<std::size_t>(ov)] = chunk;
+                        members.push_back(ov);
+                    }
+                }
+            if (static_cast<int>(members.size()) > kUnionMax)
+                throw InternalError("one stencil base exceeds the union stage");
+            base_nodes.push_back(k);
+            ++nbase;
+        }
+        const std::size_t th = gslot.size() - kGrpThreads + static_cast<std::size_t>(used++);
+        gslot[th] = static_cast<unsigned char>(nbase - 1);
+        perm[2 * th] = k;
+        ++q;
+        if (q < nb && lines[ord[static_cast<std::size_t>(q)]] == lines[k]) {
+            perm[2 * th + 1] = ord[static_cast<std::size_t>(q)];
+            ++q;
+        }
+    }
+    close_chunk();
+    const std::size_t ns = perm.size();
+    std::vector<double> ts(3 * ns, 0.0);
+    for (std::size_t sl = 0; sl < ns; ++sl)
+        if (perm[sl] >= 0)
+            for (int a = 0; a < 3; ++a) ts[static_cast<std::size_t>(a) * ns + sl] = t[static_cast<std::size_t>(a) * nb + perm[sl]];
+    op->grp_t.upload(ts);
+    op->grp_slot.upload(gslot);
+    op->grp_perm.upload(perm);
+    op->uni_stage.upload(stage);
+    op->uni_roff.upload(roff);
+    op->grp_chunks = static_cast<int>(gslot.size() / kGrpThreads);
+    op->grp_slots = static_cast<int>(ns);
+    op->uni = true;
+    int per_sm = 0;
+    CPDDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_extend_union, kGrpThreads, 0));
+    op->grp_grid = std::max(1, std::min(op->grp_chunks, std::max(1, per_sm) * sm_count()));
+}
+
 template <int D>
 static void build_tables(cpddg_op* op, const Ix<D>* ix, const Vec<D>* cp, const LatticeMap& map) {
     const int nb = op->na + op->ng, p = op->p, Q = p + 1;
@@ -669,14 +877,23 @@ static void build_tables(cpddg_op* op, const Ix<D>* ix, const Vec<D>* cp, const 
         if (p == 3 && !std::getenv("CPDDG_EXT_GATHER")) {
             if (ext && std::string(ext) == "staged") {
                 build_stage(op, lines, t, nb);
-            } else {
+            } else if (ext && std::string(ext) == "grouped") {
                 build_groups(op, lines, t, nb);
+            } else {
+                build_union(op, lines, t, nb);
             }
         }
     }
     op->t.upload(t);
     op->lines.upload(lines);
     op->nbr.upload(nbr);
+    {  // node-major copy for k_helm_pdl
+        std::vector<int> aos(nbr.size());
+        for (int i = 0; i < op->na; ++i)
+            for (int k = 0; k < 2 * D; ++k)
+                aos[static_cast<std::size_t>(i) * 2 * D + k] = nbr[static_cast<std::size_t>(k) * op->na + i];
+        op->nbr_aos.upload(aos);
+    }
     op->v.alloc(static_cast<std::size_t>(nb));
     op->nlines = nlines;
     // B_op = 16 N_A + [8d + 4 (p+1)^(d-1)] N_B + 8d N_A
@@ -685,7 +902,11 @@ static void build_tables(cpddg_op* op, const Ix<D>* ix, const Vec<D>* cp, const 
     op->streamed_bytes = 16LL * op->na + (8LL * D + 4LL * nlines) * nb + 16LL * nb + 8LL * D * op->na;
     if (op->ext_tiles)  // staged: 16-bit run starts + one int per staged x
         op->streamed_bytes += (2LL - 4LL) * nlines * nb + 4LL * static_cast<long long>(op->stage_idx.size());
-    if (op->grp_chunks)  // grouped: t + one byte per slot, kGrpMax x 16 run starts per chunk
+    if (op->uni)  // union: t + code per slot, a byte per thread, the stage list and 16-bit run offsets
+        op->streamed_bytes = 16LL * op->na + (8LL * D + 4) * op->grp_slots + op->grp_slots / 2 + 16LL * nb +
+                             8LL * D * op->na + 4LL * static_cast<long long>(op->uni_stage.size()) +
+                             2LL * static_cast<long long>(op->uni_roff.size());
+    else if (op->grp_chunks)  // grouped: t + one byte per slot, kGrpMax x 16 run starts per chunk
         op->streamed_bytes = 16LL * op->na + (8LL * D + 4) * op->grp_slots + op->grp_slots / 2 + 16LL * nb +
                              8LL * D * op->na + 4LL * static_cast<long long>(op->grp_lines.size());
 }
@@ -695,7 +916,12 @@ static void launch_apply(const cpddg_op* op, const double* x, const double* b, d
                          cudaStream_t st, bool pdl = true) {
     const int nb = op->na + op->ng;
     const int thr = 256;
-    if (op->grp_chunks) {
+    if (op->uni) {
+        k_extend_union<<<op->grp_grid, kGrpThreads, 0, st>>>(op->grp_chunks, op->grp_slots, op->grp_t.get(),
+                                                            op->grp_slot.get(), op->grp_perm.get(),
+                                                            op->uni_stage.get(), op->uni_roff.get(), x,
+                                                            op->v.get());
+    } else if (op->grp_chunks) {
         k_extend_grouped<<<op->grp_grid, kGrpThreads, 0, st>>>(op->grp_chunks, op->grp_slots, op->grp_t.get(),
                                                                   op->grp_slot.get(), op->grp_perm.get(),
                                                                   op->grp_lines.get(), x, op->v.get());
@@ -720,7 +946,7 @@ static void launch_apply(const cpddg_op* op, const double* x, const double* b, d
     const int grid = std::min(rb, (op->na + kRedThreads - 1) / kRedThreads);
     if (!b && op->grp_chunks) {
         cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3((op->na + kHelmNodes * 256 - 1) / (kHelmNodes * 256));
+        cfg.gridDim = dim3((op->na + 255) / 256);
         cfg.blockDim = dim3(256);
         cfg.stream = st;
         cudaLaunchAttribute attr[1];
@@ -729,8 +955,8 @@ static void launch_apply(const cpddg_op* op, const double* x, const double* b, d
         cfg.attrs = attr;
         cfg.numAttrs = pdl ? 1 : 0;
         CPDDG_CUDA(cudaLaunchKernelEx(&cfg, k_helm_pdl<D>, op->na, op->cg, op->ih2,
-                                      static_cast<const int*>(op->nbr.get()), static_cast<const double*>(op->v.get()),
-                                      x, y));
+                                      reinterpret_cast<const int2*>(op->nbr_aos.get()),
+                                      static_cast<const double*>(op->v.get()), x, y));
     } else if (b)
         k_helm<D, true><<<rb, kRedThreads, 0, st>>>(op->na, op->cg, op->ih2, op->nbr.get(), op->v.get(), x,
                                                     b, y, op->red.partials.get(), op->red.counter.get(), rn2);

@@ -49,6 +49,7 @@ struct cpddg_op {
     cpddg::DevBuf<double> t;    // [dim][N_B] stencil offsets g_a - base_a
     cpddg::DevBuf<int> lines;   // [(p+1)^(d-1)][N_B] first ordinal of each contiguous run
     cpddg::DevBuf<int> nbr;     // [2d][N_A] band codes of the axis neighbours
+    cpddg::DevBuf<int> nbr_aos; // [N_A][2d] the same, node-major (k_helm_pdl)
     cpddg::DevBuf<double> v;    // [N_B] extension values E x
     // staged extension (d = 3, p = 3): tiles of <= kExtTile consecutive band
     // nodes; each tile stages the x entries its stencils touch into shared
@@ -67,6 +68,11 @@ struct cpddg_op {
     cpddg::DevBuf<unsigned char> grp_slot;          // [threads] base of each thread within its chunk
     cpddg::DevBuf<int> grp_perm;                    // [slots] band code of each slot, -1 idle
     cpddg::DevBuf<int> grp_lines;                   // [chunks][kGrpMax][16] run starts of the chunk's bases, -1 unused
+    // union stage (k_extend_union, the default): same slots, per chunk the sorted
+    // union of its bases' x runs and each base's 16 run offsets into it
+    bool uni = false;
+    cpddg::DevBuf<int> uni_stage;                   // [chunks][kUnionMax] active ordinals, -1 unused
+    cpddg::DevBuf<unsigned short> uni_roff;         // [chunks][kGrpMax][16] run offsets in the stage
     cpddg::DevBuf<double> rn2;  // scalar slot for ||b - A x||^2
     cpddg::ReduceWork red;
     std::int64_t alg_bytes = 0, streamed_bytes = 0;

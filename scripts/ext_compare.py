@@ -1,4 +1,4 @@
-"""Extension kernels (grouped default, staged, gather): bit-identity and timing
+"""Extension kernels (union default, grouped, staged, gather): bit-identity and timing
 of A x at one sphere size (development aid).  Usage: ext_compare.py [h]"""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -8,7 +8,8 @@ from paper_1909_08734_b200 import api
 h = float(sys.argv[1]) if len(sys.argv) > 1 else 0.0125
 P = api.Problem("sphere", h=h, p=3, c=1.0)
 ops = {}
-for name, env in (("gather", {"CPDDG_EXT_GATHER": "1"}), ("staged", {"CPDDG_EXT": "staged"}), ("grouped", {})):
+for name, env in (("gather", {"CPDDG_EXT_GATHER": "1"}), ("staged", {"CPDDG_EXT": "staged"}),
+                  ("grouped", {"CPDDG_EXT": "grouped"}), ("union", {})):
     for k, v in env.items():
         os.environ[k] = v
     ops[name] = api.DeviceHelmholtz.from_problem(P)
@@ -16,7 +17,7 @@ for name, env in (("gather", {"CPDDG_EXT_GATHER": "1"}), ("staged", {"CPDDG_EXT"
         del os.environ[k]
 x = torch.rand(P.n_active, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(1))
 ys = {k: A.apply(x) for k, A in ops.items()}
-for k in ("staged", "grouped"):
+for k in ("staged", "grouped", "union"):
     print(f"{k} vs gather bit-identical:", bool(torch.equal(ys["gather"], ys[k])),
           "max diff", float((ys["gather"] - ys[k]).abs().max()))
 for name, A in ops.items():

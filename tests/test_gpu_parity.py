@@ -16,7 +16,7 @@ from conftest import GOLDEN
 
 pytestmark = pytest.mark.gpu
 
-CASES = sorted(f[:-4] for f in os.listdir(GOLDEN) if f.endswith(".npz") and not f.startswith("fullsize_"))
+CASES = sorted(f[:-4] for f in os.listdir(GOLDEN) if f.endswith(".npz") and not f.startswith(("fullsize_", "scale_")))
 
 
 def _setup(name):
@@ -196,10 +196,10 @@ def test_drop_in_band_descriptor_matches_setup():
 
 @pytest.mark.parametrize("h", [0.1, 0.025])
 def test_staged_extension_matches_gather_kernel(h, monkeypatch):
-    """The grouped extension kernel (d = 3, p = 3 default), the tiled staged
-    kernel (CPDDG_EXT=staged) and the plain gather kernel (CPDDG_EXT_GATHER=1,
-    read at create time) give bitwise equal A x: same weights, same summation
-    order."""
+    """The union-staged extension kernel (d = 3, p = 3 default), the
+    per-base grouped kernel (CPDDG_EXT=grouped), the tiled staged kernel
+    (CPDDG_EXT=staged) and the plain gather kernel (CPDDG_EXT_GATHER=1, read at
+    create time) give bitwise equal A x: same weights, same summation order."""
     import torch
 
     from paper_1909_08734_b200 import api, inputs
@@ -210,11 +210,13 @@ def test_staged_extension_matches_gather_kernel(h, monkeypatch):
     monkeypatch.delenv("CPDDG_EXT_GATHER")
     monkeypatch.setenv("CPDDG_EXT", "staged")
     tiled = api.DeviceHelmholtz.from_problem(P)
+    monkeypatch.setenv("CPDDG_EXT", "grouped")
+    grouped = api.DeviceHelmholtz.from_problem(P)
     x = torch.from_numpy(inputs.uniform_vector(P.n_active, 5)).cuda()
-    assert torch.equal(staged.apply(x), gather.apply(x))
-    assert torch.equal(tiled.apply(x), gather.apply(x))
-    # the grouped (default) and tiled tables were really built
-    assert len({staged.bytes()[1], gather.bytes()[1], tiled.bytes()[1]}) == 3
+    for other in (staged, tiled, grouped):
+        assert torch.equal(other.apply(x), gather.apply(x))
+    # the union (default), grouped and tiled tables were really built
+    assert len({staged.bytes()[1], gather.bytes()[1], tiled.bytes()[1], grouped.bytes()[1]}) == 4
 
 
 @pytest.mark.parametrize("name", ["sphere05_oras_gmres", "circle_ras_gmres"])
