@@ -719,6 +719,279 @@ __global__ void __launch_bounds__(kFactorThreads, 2) k_factor(const int* __restr
     if (tid == 0) status[j] = bad;
 }
 
+/** k_factor with a software-pipelined trailing update (the default; the
+ *  round-1 kernel above stays as CPDDG_FACTOR=v1).  One CTA of 512 threads
+ *  per SM and subdomain.  Per panel, the 64-row blocks of the trailing
+ *  window that carry panel entries are listed once (no per-tile skip test),
+ *  and the active tiles (bi >= bj) are walked with their four panel slices
+ *  (X_i, Y_i, X_j, Y_j: 64 rows x 32 panel columns, row-major, 36-double
+ *  stride) staged by 16-byte cp.async with zero fill outside the envelopes
+ *  into one of two shared buffers while the previous tile runs on the FP64
+ *  tensor cores; the tile's old L / U values are loaded before its MMAs and
+ *  written after.  16 warps: warp w owns rows 8 (w % 8) .. + 8 and columns
+ *  32 (w / 8) .. + 32 of the tile.  Same fragments and k order as k_factor:
+ *  the factors are bitwise identical. */
+constexpr int kF2Threads = 512;
+constexpr int kF2Stride = 36;                      // doubles per staged row (2-way conflict-free fragments)
+constexpr int kF2Arr = TILE * kF2Stride;           // one staged array
+constexpr int kF2Buf = 4 * kF2Arr;                 // X_i, Y_i, X_j, Y_j
+constexpr int kF2MaxBlk = 256;                     // trailing-window blocks (reach <= 16384 rows; else k_factor)
+__global__ void __launch_bounds__(kF2Threads, 1) k_factor2(const int* __restrict__ order,
+                                                          const int* __restrict__ n_rows,
+                                                          const std::int64_t* __restrict__ vbase,
+                                                          const std::int64_t* __restrict__ ebase,
+                                                          const std::int64_t* __restrict__ ebaseU,
+                                                          const int* __restrict__ first_all,
+                                                          const std::int64_t* __restrict__ roff_all,
+                                                          const int* __restrict__ firstU_all,
+                                                          const std::int64_t* __restrict__ roffU_all,
+                                                          const int* __restrict__ rlast_all,
+                                                          double* diag_all, double* L_all, double* U_all,
+                                                          double* dinv_all, int* status,
+                                                          const int* __restrict__ prefactored) {
+    const int j = order[blockIdx.x];
+    const SubPtrs S = sub_ptrs(j, n_rows, vbase, ebase, ebaseU, first_all, roff_all, firstU_all, roffU_all,
+                               rlast_all, diag_all, L_all, U_all);
+    const bool pre = prefactored[j] != 0;
+    extern __shared__ __align__(16) double sm[];
+    double* A11 = sm;                     // [NB][NB+1]
+    double* bufs = A11 + NB * (NB + 1);   // [2][4][TILE][kF2Stride]  (NB*(NB+1) is even: 16-byte aligned)
+    __shared__ int act[kF2MaxBlk];        // active 64-row blocks of the trailing window
+    __shared__ unsigned char actf[kF2MaxBlk];
+    __shared__ int n_act;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int n = S.n;
+    const unsigned bufs_s = static_cast<unsigned>(__cvta_generic_to_shared(bufs));
+
+    for (int k0 = 0; k0 < (pre ? 0 : n); k0 += NB) {
+        const int kb = min(NB, n - k0), k1 = k0 + kb;
+        const int R = S.rlast[k1 - 1];
+        // (1) diagonal block into shared memory
+        for (int e = tid; e < NB * NB; e += blockDim.x) {
+            const int r = e / NB, c = e % NB;
+            double v = 0.0;
+            if (r < kb && c < kb) {
+                const int gr = k0 + r, gc = k0 + c;
+                if (r == c)
+                    v = S.diag[gr];
+                else if (r > c) {
+                    const int f = S.first[gr];
+                    if (gc >= f) v = S.L[S.roff[gr] + gc - f];
+                } else {
+                    const int f = S.firstU[gc];
+                    if (gr >= f) v = S.U[S.roffU[gc] + gr - f];
+                }
+            }
+            A11[r * (NB + 1) + c] = v;
+        }
+        __syncthreads();
+        // (2) unblocked LU of the diagonal block
+        for (int p = 0; p < kb; ++p) {
+            const double piv = A11[p * (NB + 1) + p];
+            for (int r = p + 1 + tid; r < kb; r += blockDim.x) A11[r * (NB + 1) + p] /= piv;
+            __syncthreads();
+            for (int e = tid; e < (kb - p - 1) * (kb - p - 1); e += blockDim.x) {
+                const int r = p + 1 + e / (kb - p - 1), c = p + 1 + e % (kb - p - 1);
+                A11[r * (NB + 1) + c] -= A11[r * (NB + 1) + p] * A11[p * (NB + 1) + c];
+            }
+            __syncthreads();
+        }
+        for (int e = tid; e < kb * kb; e += blockDim.x) {
+            const int r = e / kb, c = e % kb;
+            const int gr = k0 + r, gc = k0 + c;
+            const double v = A11[r * (NB + 1) + c];
+            if (r == c)
+                S.diag[gr] = v;
+            else if (r > c) {
+                const int f = S.first[gr];
+                if (gc >= f) S.L[S.roff[gr] + gc - f] = v;
+            } else {
+                const int f = S.firstU[gc];
+                if (gr >= f) S.U[S.roffU[gc] + gr - f] = v;
+            }
+        }
+        // (3)+(4) panels: rows i in [k1, R]
+        for (int i = k1 + tid; i <= R; i += blockDim.x) {
+            const int f = S.first[i], fu = S.firstU[i];
+            if (f >= k1 && fu >= k1) continue;
+            const std::int64_t ro = S.roff[i] - f, rou = S.roffU[i] - fu;
+            double x[NB], u[NB];
+#pragma unroll
+            for (int p = 0; p < NB; ++p) {
+                const int gc = k0 + p;
+                x[p] = p < kb && gc >= f ? S.L[ro + gc] : 0.0;
+                u[p] = p < kb && gc >= fu ? S.U[rou + gc] : 0.0;
+            }
+#pragma unroll
+            for (int p = 0; p < NB; ++p) {
+                if (p < kb) {
+                    double s = x[p];
+#pragma unroll
+                    for (int q = 0; q < p; ++q) s -= x[q] * A11[q * (NB + 1) + p];
+                    x[p] = s / A11[p * (NB + 1) + p];
+                }
+            }
+#pragma unroll
+            for (int p = 0; p < NB; ++p) {
+                if (p < kb) {
+                    double s = u[p];
+#pragma unroll
+                    for (int q = 0; q < p; ++q) s -= A11[p * (NB + 1) + q] * u[q];
+                    u[p] = s;
+                }
+            }
+#pragma unroll
+            for (int p = 0; p < NB; ++p) {
+                const int gc = k0 + p;
+                if (p < kb && gc >= f) S.L[ro + gc] = x[p];
+                if (p < kb && gc >= fu) S.U[rou + gc] = u[p];
+            }
+        }
+        // (5) trailing update of rows/cols [k1, R]
+        const int m = R - k1 + 1;
+        const int nblk = m > 0 ? (m + TILE - 1) / TILE : 0;
+        // active blocks: some row carries an L or U entry in the panel columns
+        for (int b = warp; b < nblk; b += kF2Threads / 32) {
+            bool a = false;
+            for (int q = lane; q < TILE; q += 32) {
+                const int r = k1 + b * TILE + q;
+                if (r <= R && min(S.first[r], S.firstU[r]) < k1) a = true;
+            }
+            a = __any_sync(0xffffffffu, a);
+            if (lane == 0) actf[b] = a;
+        }
+        __syncthreads();  // panels written, block flags set
+        if (warp == 0) {  // compaction in block order
+            int cnt = 0;
+            for (int b0 = 0; b0 < nblk; b0 += 32) {
+                const bool a = b0 + lane < nblk && actf[b0 + lane];
+                const unsigned bal = __ballot_sync(0xffffffffu, a);
+                if (a) act[cnt + __popc(bal & ((1u << lane) - 1u))] = b0 + lane;
+                cnt += __popc(bal);
+            }
+            if (lane == 0) n_act = cnt;
+        }
+        __syncthreads();
+        const int na = n_act;
+        const int ntiles = na * (na + 1) / 2;
+        // staging: thread -> (array, row) = (tid >> 7, (tid >> 1) & 63), 8 column pairs (tid & 1) * 8 ..
+        const int sarr = tid >> 7, srow = (tid >> 1) & 63, spp0 = (tid & 1) * 8;
+        auto tile_of = [&](int t, int& bi, int& bj) {
+            int b = static_cast<int>((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+            while ((b + 1) * (b + 2) / 2 <= t) ++b;
+            while (b * (b + 1) / 2 > t) --b;
+            bi = act[b];
+            bj = act[t - b * (b + 1) / 2];
+        };
+        auto stage = [&](int t, int buf) {
+            int bi, bj;
+            tile_of(t, bi, bj);
+            const int g = k1 + (sarr < 2 ? bi : bj) * TILE + srow;  // X_i, Y_i, X_j, Y_j
+            const bool isY = sarr & 1;
+            const unsigned dst = bufs_s + static_cast<unsigned>(((buf * 4 + sarr) * kF2Arr + srow * kF2Stride + 2 * spp0) * 8);
+            int f = INT_MAX;
+            const double* src = S.L;
+            if (g <= R) {
+                f = isY ? S.firstU[g] : S.first[g];
+                src = (isY ? S.U + S.roffU[g] : S.L + S.roff[g]) - f;
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int p = 2 * (spp0 + q), gc = k0 + p;
+                const int bytes = (gc >= f && p < kb) ? (p + 1 < kb ? 16 : 8) : 0;
+                const double* sp = bytes ? src + gc : S.L;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst + 16 * q), "l"(sp), "r"(bytes)
+                             : "memory");
+            }
+        };
+        const int rb = warp & 7, ch = warp >> 3;
+        const int lr = lane >> 2, lk = lane & 3;
+        if (ntiles > 0) stage(0, 0);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        for (int t = 0; t < ntiles; ++t) {
+            if (t + 1 < ntiles) stage(t + 1, (t + 1) & 1);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            int bi, bj;
+            tile_of(t, bi, bj);
+            const int i0 = k1 + bi * TILE, j0 = k1 + bj * TILE;
+            // old values of this warp's 8 x 32 block (issued before the MMAs)
+            const int gi = i0 + rb * 8 + lr;
+            int f = 0, fu = 0;
+            std::int64_t ro = 0, rou = 0;
+            if (gi <= R) {
+                f = S.first[gi];
+                fu = S.firstU[gi];
+                ro = S.roff[gi] - f;
+                rou = S.roffU[gi] - fu;
+            }
+            double oL[4][2], oU[4][2];
+#pragma unroll
+            for (int cb = 0; cb < 4; ++cb)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int gc = j0 + ch * 32 + cb * 8 + 2 * lk + e;
+                    const bool in = gi <= R && gc <= R && gc < gi;
+                    oL[cb][e] = in && gc >= f ? S.L[ro + gc] : 0.0;
+                    oU[cb][e] = in && gc >= fu ? S.U[rou + gc] : 0.0;
+                }
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+            __syncthreads();
+            const double* B = bufs + (t & 1) * kF2Buf;
+            const double* Xi = B;
+            const double* Yi = B + kF2Arr;
+            const double* Xj = B + 2 * kF2Arr;
+            const double* Yj = B + 3 * kF2Arr;
+            double cL[4][2], cU[4][2];
+#pragma unroll
+            for (int cb = 0; cb < 4; ++cb) cL[cb][0] = cL[cb][1] = cU[cb][0] = cU[cb][1] = 0.0;
+            for (int kc = 0; kc < kb; kc += 4) {
+                const int p = kc + lk;
+                const double ax = Xi[(rb * 8 + lr) * kF2Stride + p];
+                const double ay = Yi[(rb * 8 + lr) * kF2Stride + p];
+#pragma unroll
+                for (int cb = 0; cb < 4; ++cb) {
+                    const int col = ch * 32 + cb * 8 + lr;
+                    const double by = Yj[col * kF2Stride + p];
+                    const double bx = Xj[col * kF2Stride + p];
+                    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                                 : "+d"(cL[cb][0]), "+d"(cL[cb][1])
+                                 : "d"(ax), "d"(by));
+                    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                                 : "+d"(cU[cb][0]), "+d"(cU[cb][1])
+                                 : "d"(ay), "d"(bx));
+                }
+            }
+            if (gi <= R) {
+#pragma unroll
+                for (int cb = 0; cb < 4; ++cb)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int gc = j0 + ch * 32 + cb * 8 + 2 * lk + e;
+                        if (gc > R) continue;
+                        if (gc < gi) {
+                            if (gc >= f) S.L[ro + gc] = oL[cb][e] - cL[cb][e];
+                            if (gc >= fu) S.U[rou + gc] = oU[cb][e] - cU[cb][e];
+                        } else if (gc == gi) {
+                            S.diag[gi] -= cL[cb][e];
+                        }
+                    }
+            }
+            __syncthreads();  // this buffer is restaged two tiles on
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();
+    }
+    int bad = 0;
+    double* dinv = dinv_all + vbase[j];
+    for (int i = tid; i < n; i += blockDim.x) {
+        const double d = S.diag[i];
+        if (!(fabs(d) > 0.0) || !isfinite(d)) bad = 1;
+        dinv[i] = 1.0 / d;
+    }
+    bad = __syncthreads_or(bad);
+    if (tid == 0) status[j] = bad;
+}
+
 // ---------------------------------------------------------------- solve
 
 /** Block shape of the pipelined triangular solves: NW warps per CTA (warp 0
@@ -3193,7 +3466,9 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
         CPDDG_CUDA(cudaDeviceSynchronize());
     }
     first.reserve(static_cast<std::size_t>(vb));
+    int max_reach = 0;  // longest trailing window of the factorisation (k_factor2's block list)
     for (auto& S : subs) {
+        for (int i = 0; i < S.n; ++i) max_reach = std::max(max_reach, S.rlast[static_cast<std::size_t>(i)] - i);
         append(first, S.first);
         append(firstU, S.firstU);
         append(rlast, S.rlast);
@@ -3260,10 +3535,18 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
     pc->analyse_seconds = std::chrono::duration<double>(t1 - t0).count();
 
     // device factorisation
-    const int fsm = static_cast<int>(sizeof(double)) * (NB * (NB + 1) + 4 * NB * kTS);
-    CPDDG_CUDA(cudaFuncSetAttribute(k_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm));
-    // two CTAs per SM (256 subdomains in one wave on 148 SMs): full shared-memory carveout
-    CPDDG_CUDA(cudaFuncSetAttribute(k_factor, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    const char* fenv = std::getenv("CPDDG_FACTOR");  // v1: the round-1 kernel (two CTAs per SM, no pipelining)
+    const bool factor_v1_env = fenv && std::string(fenv) == "v1";
+    const bool factor_v1 = factor_v1_env || max_reach + NB > kF2MaxBlk * TILE;
+    const int fsm = factor_v1 ? static_cast<int>(sizeof(double)) * (NB * (NB + 1) + 4 * NB * kTS)
+                              : static_cast<int>(sizeof(double)) * (NB * (NB + 1) + 2 * kF2Buf);
+    if (factor_v1) {
+        CPDDG_CUDA(cudaFuncSetAttribute(k_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm));
+        // two CTAs per SM (256 subdomains in one wave on 148 SMs): full shared-memory carveout
+        CPDDG_CUDA(cudaFuncSetAttribute(k_factor, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    } else {
+        CPDDG_CUDA(cudaFuncSetAttribute(k_factor2, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm));
+    }
     DevBuf<int> status(static_cast<std::size_t>(n_sub));
     status.zero();
     pc->dinv.alloc(static_cast<std::size_t>(vb));
@@ -3273,10 +3556,16 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
     CPDDG_CUDA(cudaEventRecord(e0));
     DevBuf<int> dpre;
     dpre.upload(pre);
-    k_factor<<<n_sub, kFactorThreads, fsm>>>(pc->order.get(), pc->n_rows.get(), pc->vbase.get(), pc->ebase.get(),
-                                           pc->ebaseU.get(), pc->first.get(), pc->roff.get(), pc->firstU.get(),
-                                           pc->roffU.get(), pc->rlast.get(), pc->diag.get(),
-                                           pc->L.get(), pc->U.get(), pc->dinv.get(), status.get(), dpre.get());
+    if (factor_v1)
+        k_factor<<<n_sub, kFactorThreads, fsm>>>(pc->order.get(), pc->n_rows.get(), pc->vbase.get(), pc->ebase.get(),
+                                               pc->ebaseU.get(), pc->first.get(), pc->roff.get(), pc->firstU.get(),
+                                               pc->roffU.get(), pc->rlast.get(), pc->diag.get(),
+                                               pc->L.get(), pc->U.get(), pc->dinv.get(), status.get(), dpre.get());
+    else
+        k_factor2<<<n_sub, kF2Threads, fsm>>>(pc->order.get(), pc->n_rows.get(), pc->vbase.get(), pc->ebase.get(),
+                                             pc->ebaseU.get(), pc->first.get(), pc->roff.get(), pc->firstU.get(),
+                                             pc->roffU.get(), pc->rlast.get(), pc->diag.get(),
+                                             pc->L.get(), pc->U.get(), pc->dinv.get(), status.get(), dpre.get());
     CPDDG_CUDA(cudaGetLastError());
     CPDDG_CUDA(cudaEventRecord(e1));
     CPDDG_CUDA(cudaEventSynchronize(e1));

@@ -219,6 +219,20 @@ def test_staged_extension_matches_gather_kernel(h, monkeypatch):
     assert len({staged.bytes()[1], gather.bytes()[1], tiled.bytes()[1], grouped.bytes()[1]}) == 4
 
 
+@pytest.mark.parametrize("name", ["sphere05_oras_gmres", "torus04_oras_gmres"])
+def test_factor_kernels_agree(name, monkeypatch):
+    """The pipelined factorisation (k_factor2, default) and the round-1 kernel
+    (CPDDG_FACTOR=v1) use the same tensor-core fragments in the same k order:
+    bitwise equal factors, hence bitwise equal M x."""
+    g, cfg, P, A, M, torch = _setup(name)
+    from paper_1909_08734_b200 import api
+    monkeypatch.setenv("CPDDG_FACTOR", "v1")
+    M1 = api.SchwarzPreconditioner.from_problem(P)
+    x = torch.from_numpy(g["x"]).cuda()
+    assert torch.equal(M.apply(x), M1.apply(x))
+    assert M.stats()["max_probe_residual"] == M1.stats()["max_probe_residual"]
+
+
 @pytest.mark.parametrize("name", ["sphere05_oras_gmres", "circle_ras_gmres"])
 def test_factor_layouts_agree(name, monkeypatch):
     """The factor layouts give the same preconditioner: nonsymmetric
