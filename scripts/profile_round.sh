@@ -2,8 +2,9 @@
 # Regenerates the committed profiles of a round on a B200 (run under gpurun):
 #   bash scripts/profile_round.sh TAG
 # 1. the headline bench line (no profiler), 2. the ncu launch list of the same
-# command, 3. one ncu --set full capture of the preconditioner apply
-# (k_solve_win) and of the operator.  Outputs under gpurun_out/TAG_*.
+# command, 3. ncu --set full captures of the preconditioner apply (k_solve_win),
+# the operator (k_extend_union + k_helm_pdl) and the factorisation (k_factor2).
+# Outputs under gpurun_out/TAG_*.
 set -u
 TAG=${1:-r02}
 OUT=gpurun_out
@@ -16,6 +17,9 @@ echo "launch list rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_solve_win -s 2 -c 1 \
     -o $OUT/${TAG}_k_solve_win -f python scripts/profile_pc_mode.py 0 > $OUT/${TAG}_ncu_pc.log 2>&1
 echo "pc capture rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_extend|k_helm|k_op" -s 4 -c 2 \
-    -o $OUT/${TAG}_op -f python scripts/profile_kernels.py > $OUT/${TAG}_ncu_op.log 2>&1
+timeout 900 ncu --set full --clock-control none --cache-control none --import-source on \
+    -k regex:"k_extend_union|k_helm_pdl" -s 2 -c 2 -o $OUT/${TAG}_op -f python scripts/profile_kernels.py > $OUT/${TAG}_ncu_op.log 2>&1
 echo "op capture rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_factor2" -c 1 \
+    -o $OUT/${TAG}_k_factor2 -f python scripts/profile_kernels.py > $OUT/${TAG}_ncu_factor.log 2>&1
+echo "factor capture rc=$?"
