@@ -2034,6 +2034,20 @@ __device__ __forceinline__ void bulk_copy(unsigned dst, const void* src, unsigne
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
 }
+/** bulk_copy with an L2 eviction-priority policy (createpolicy): the factor
+ *  stream of a preconditioner apply (10.5 GB at the headline) is read once, so
+ *  it is marked evict_first and does not push the operator tables, the
+ *  Krylov basis and the vectors out of L2. */
+__device__ __forceinline__ void bulk_copy_hint(unsigned dst, const void* src, unsigned bytes, unsigned bar,
+                                               unsigned long long policy) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(bar), "l"(policy) : "memory");
+}
+__device__ __forceinline__ unsigned long long policy_evict_first() {
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
 __device__ __forceinline__ void step_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kStep) : "memory"); }
 }  // namespace tmas
 
@@ -2464,6 +2478,7 @@ __global__ void __launch_bounds__(win::kThreads, 1) k_solve_win(const int* __res
     using tmas::smem_u32;
     using tmas::mbar_wait;
     using tmas::bulk_copy;
+    using tmas::bulk_copy_hint;
     using win::step_bar;
     using win::lds2;
     using win::sts2;
@@ -2489,6 +2504,7 @@ __global__ void __launch_bounds__(win::kThreads, 1) k_solve_win(const int* __res
     if (warp == kC + 1) {
         // ---------------- producer (one thread): every step's item in step order
         if (lane != 0) return;
+        const unsigned long long pol = tmas::policy_evict_first();
         const unsigned long long RING = static_cast<unsigned long long>(ring_bytes);
         unsigned long long head = 0;  // virtual ring position (bytes)
         int t = 0;
@@ -2535,10 +2551,10 @@ __global__ void __launch_bounds__(win::kThreads, 1) k_solve_win(const int* __res
             const unsigned bar = smem_u32(&mbar[slot]);
             const unsigned tx = static_cast<unsigned>(kHdr + (big ? 0 : cur.bytes));
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(tx) : "memory");
-            bulk_copy(smem_u32(ring + off), cur.desc, 4u * kDesc, bar);
-            bulk_copy(smem_u32(ring + off + 4 * kDesc), cur.rec, 8u * G::kRec, bar);
+            bulk_copy_hint(smem_u32(ring + off), cur.desc, 4u * kDesc, bar, pol);
+            bulk_copy_hint(smem_u32(ring + off + 4 * kDesc), cur.rec, 8u * G::kRec, bar, pol);
             if (!big && cur.bytes > 0)
-                bulk_copy(smem_u32(ring + off + kHdr), cur.data, static_cast<unsigned>(cur.bytes), bar);
+                bulk_copy_hint(smem_u32(ring + off + kHdr), cur.data, static_cast<unsigned>(cur.bytes), bar, pol);
             head = start + need;
             cur = nxt;
             ++t;
