@@ -485,9 +485,9 @@ def main():
             else:
                 line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                                         "sample": "unavailable: oracle/_ref not built"}
-        except Exception as exc:  # the baseline is reported, never fatal to the device number
+        except (Exception, SystemExit) as exc:  # the baseline is reported, never fatal to the device number
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
-                                    "sample": f"failed: {exc}"}
+                                    "sample": f"unavailable: {exc}"}
     if rank == 0:
         print(json.dumps(line))
     if dist:
