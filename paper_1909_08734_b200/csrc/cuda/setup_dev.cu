@@ -906,7 +906,7 @@ int decompose_device(const DevBand& B, const Band<D>& g, std::vector<int>& part,
     const int na = B.na;
     if (static_cast<int>(part.size()) != na) throw InternalError("partition size does not match grid");
     const int n_parts = *std::max_element(part.begin(), part.end()) + 1;
-    if (n_parts > 1023) throw ConfigError("device subdomain sets support at most 1023 subdomains");
+    if (n_parts > 1023) throw DeviceSetLimit("device subdomain sets support at most 1023 subdomains");
     cudaStream_t st = nullptr;
     const auto t0 = std::chrono::steady_clock::now();
     const double h = B.h;
@@ -1063,7 +1063,7 @@ int decompose_device(const DevBand& B, const Band<D>& g, std::vector<int>& part,
         sort_u64_pairs(n_be, bkey.get(), bkey_s.get(), btag.get(), btag_s.get(), 64, st);
     }
     pull();
-    if (hc.err & kErrRange) throw ConfigError("lattice index out of the device subdomain-set range");
+    if (hc.err & kErrRange) throw DeviceSetLimit("lattice index out of the device subdomain-set range");
 
     const std::vector<std::uint64_t> h_ov = download(ovs.get(), static_cast<std::size_t>(n_ov), st);
     const std::vector<std::uint64_t> h_gh = download(ghs.get(), static_cast<std::size_t>(n_gh), st);

@@ -92,9 +92,19 @@ void decompose_impl(cpddg_setup* s, const int32_t* part, int n_part, int n_overl
     I.part.assign(part, part + I.band.n_active);
     validate_partition(I.part, I.band.n_active);
     I.robin = robin;
+    bool done = false;
     if (s->device_setup && I.dev) {
-        I.moves = decompose_device<D>(*I.dev, I.band, I.part, n_overlap, robin, I.subs, &I.t_align, &I.t_sets);
-    } else {
+        // device sets; past their index limits (> 1023 subdomains, |lattice index| >= 2^17) the
+        // host restatement below produces the identical result
+        const std::vector<int> part0 = I.part;
+        try {
+            I.moves = decompose_device<D>(*I.dev, I.band, I.part, n_overlap, robin, I.subs, &I.t_align, &I.t_sets);
+            done = true;
+        } catch (const DeviceSetLimit&) {
+            I.part = part0;
+        }
+    }
+    if (!done) {
         const auto t0 = std::chrono::steady_clock::now();
         I.moves = align_interfaces<D>(I.band, I.part, I.band.p);
         const auto t1 = std::chrono::steady_clock::now();

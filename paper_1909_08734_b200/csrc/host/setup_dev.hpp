@@ -12,6 +12,12 @@ namespace cpddg {
 
 struct DevBand;  // device band of a setup (setup_dev.cuh)
 
+/** Thrown by decompose_device when the problem exceeds its index packing
+ *  (the caller then runs the host restatement). */
+struct DeviceSetLimit : ConfigError {
+    using ConfigError::ConfigError;
+};
+
 /** build_band_tube (band.hpp:150-182) on the device; the host copy is
  *  returned (with its lattice map), the device band kept in *keep. */
 template <int D>

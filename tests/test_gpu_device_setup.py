@@ -97,3 +97,18 @@ def test_device_subdomain_sets_are_identical_to_host(name):
         lh, lg = H.local(j), G.local(j)
         for k in ("ptr", "col", "val", "scatter_local", "scatter_global"):
             assert lh[k].tobytes() == lg[k].tobytes(), (j, k)
+
+
+def test_device_sets_beyond_limits_fall_back_to_host():
+    """More than 1023 subdomains exceed the device sets' index packing: the
+    host restatement runs instead and the result is the host's."""
+    from paper_1909_08734_b200 import inputs
+    w = dict(surface="sphere", h=0.025)
+    H = _problem(w, False)
+    G = _problem(w, True)
+    part = inputs.rcb_partition(H.active_cp, 1024)
+    ah, mh = H.decompose(part, 1, "oras", 4.0, 40.0)
+    ag, mg = G.decompose(part, 1, "oras", 4.0, 40.0)
+    assert mg == mh and np.array_equal(ag, ah) and G.n_sub == H.n_sub == 1024
+    for j in (0, 511, 1023):
+        assert np.array_equal(H.subdomain(j)["overlap"], G.subdomain(j)["overlap"])
