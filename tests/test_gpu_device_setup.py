@@ -103,7 +103,7 @@ def test_device_sets_beyond_limits_fall_back_to_host():
     """More than 1023 subdomains exceed the device sets' index packing: the
     host restatement runs instead and the result is the host's."""
     from paper_1909_08734_b200 import inputs
-    w = dict(surface="sphere", h=0.025)
+    w = dict(surface="sphere", h=0.0125)
     H = _problem(w, False)
     G = _problem(w, True)
     part = inputs.rcb_partition(H.active_cp, 1024)
