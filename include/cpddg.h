@@ -240,6 +240,9 @@ CPDDG_API int cpddg_pc_apply_mode(cpddg_pc* pc, const double* r_dev, double* z_d
 /** Per-block timing trace of CTA 0 from the last solve run with
  *  CPDDG_SOLVE_DEBUG & 16 (1024 x 20 clock64 values). */
 CPDDG_API int cpddg_dev_trace(long long* out);
+/** Exact zeros among the stored factor entries: out[6] = L entries, L zeros,
+ *  all-zero 16-entry L segments, U entries, U zeros, U zero segments. */
+CPDDG_API int cpddg_pc_debug_zero_stats(const cpddg_pc* pc, int64_t* out);
 
 #ifdef __cplusplus
 }

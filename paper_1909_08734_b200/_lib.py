@@ -79,6 +79,7 @@ _SIGS = {
                                         _i32p, C.POINTER(C.c_int)]),
     "cpddg_setup_n_subdomains": (C.c_int, [_vp]),
     "cpddg_setup_timings": (C.c_int, [_vp, _f64p]),
+    "cpddg_pc_debug_zero_stats": (C.c_int, [_vp, _i64p]),
     "cpddg_setup_subdomain_counts": (C.c_int, [_vp, C.c_int, _i32p]),
     "cpddg_setup_subdomain_sets": (C.c_int, [_vp, C.c_int, _i32p, _i32p, _i32p, _i32p, _i32p, _f64p]),
     "cpddg_setup_local_sizes": (C.c_int, [_vp, C.c_int, _i64p]),

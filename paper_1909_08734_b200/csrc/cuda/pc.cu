@@ -3956,6 +3956,27 @@ static cpddg_pc* pc_build_pivoting(int n_global, int n_sub, const cpddg_local_de
 
 using namespace cpddg;
 
+namespace cpddg {
+__global__ void k_zero_stats(std::int64_t n, const double* __restrict__ a, unsigned long long* out) {
+    unsigned long long z = 0, zs = 0;
+    for (std::int64_t s = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; s < (n + 15) / 16;
+         s += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        int cnt = 0, len = 0;
+        for (int q = 0; q < 16; ++q) {
+            const std::int64_t i = 16 * s + q;
+            if (i < n) {
+                ++len;
+                if (a[i] == 0.0) ++cnt;
+            }
+        }
+        z += cnt;
+        zs += cnt == len ? 1 : 0;
+    }
+    atomicAdd(out, z);
+    atomicAdd(out + 1, zs);
+}
+}  // namespace cpddg
+
 extern "C" {
 
 int cpddg_pc_create(int n_global, int n_sub, const cpddg_local_desc* locals, const cpddg_pc_options* opt,
@@ -4017,6 +4038,30 @@ int cpddg_pc_stats_get(const cpddg_pc* pc, cpddg_pc_stats* st) {
 
 /** Development hooks (include/cpddg.h, last section): the per-block trace and
  *  one pass of the preconditioner (mode 1 forward, 2 backward, 0 both, 3 probe). */
+
+/** Development: exact zeros among the stored factor entries (L, U arrays as
+ *  streamed by the solve) and all-zero 16-entry segments: out[6] = L size,
+ *  L zeros, L zero segments, U size, U zeros, U zero segments. */
+int cpddg_pc_debug_zero_stats(const cpddg_pc* pc, int64_t* out) {
+    return guarded([&] {
+        if (!pc || !out) throw InternalError("null argument");
+        DevBuf<unsigned long long> d(4);
+        d.zero();
+        const std::int64_t nl = static_cast<std::int64_t>(pc->L.size()), nu = static_cast<std::int64_t>(pc->U.size());
+        k_zero_stats<<<4 * sm_count(), 256>>>(nl, pc->L.get(), d.get());
+        k_zero_stats<<<4 * sm_count(), 256>>>(nu, pc->U.get(), d.get() + 2);
+        CPDDG_CUDA(cudaGetLastError());
+        unsigned long long h[4];
+        CPDDG_CUDA(cudaMemcpy(h, d.get(), sizeof(h), cudaMemcpyDeviceToHost));
+        out[0] = nl;
+        out[1] = static_cast<int64_t>(h[0]);
+        out[2] = static_cast<int64_t>(h[1]);
+        out[3] = nu;
+        out[4] = static_cast<int64_t>(h[2]);
+        out[5] = static_cast<int64_t>(h[3]);
+    });
+}
+
 int cpddg_dev_trace(long long* out) {  // development: copy g_trace
     return guarded([&] { CPDDG_CUDA(cudaMemcpyFromSymbol(out, g_trace, sizeof(long long) * 1024 * 20)); });
 }
