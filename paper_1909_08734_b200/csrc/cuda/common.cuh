@@ -91,6 +91,7 @@ constexpr int kExtStageCap = CPDDG_EXT_CAP; // max staged x entries per tile (8 
 constexpr int kGrpThreads = 128;
 constexpr int kUnionMax = 768;   // staged x values per chunk of k_extend_union
 constexpr int kGrpMax = 36;
+static_assert(kGrpMax <= 64, "k_extend_union packs the base slot in 6 bits of the slot byte");
 constexpr int kGrpSS = 82;
 constexpr int kGrpAS = 18;
 

@@ -121,12 +121,16 @@ __global__ void __launch_bounds__(256) k_extend(int nb, const double* __restrict
 /** Cubic (p = 3) weights in product (Lagrange) form -- no divisions -- with
  *  the reference's exact-hit rule (interp.hpp:39-44).  Differs from the
  *  barycentric evaluation only in the last bits; operator parity is 1e-12. */
-__device__ __forceinline__ void weights_p3(double t, double* w) {
+__device__ __forceinline__ void weights_p3_nohit(double t, double* w) {
     const double t0 = t, t1 = t - 1.0, t2 = t - 2.0, t3 = t - 3.0;
     w[0] = -(t1 * t2 * t3) * (1.0 / 6.0);
     w[1] = (t0 * t2 * t3) * 0.5;
     w[2] = -(t0 * t1 * t3) * 0.5;
     w[3] = (t0 * t1 * t2) * (1.0 / 6.0);
+}
+__device__ __forceinline__ void weights_p3(double t, double* w) {
+    const double t0 = t, t1 = t - 1.0, t2 = t - 2.0, t3 = t - 3.0;
+    weights_p3_nohit(t, w);
     // exact hit: at most one |t - j| < 1e-12; branch-free selects
     const bool h0 = fabs(t0) < 1e-12, h1 = fabs(t1) < 1e-12, h2 = fabs(t2) < 1e-12, h3 = fabs(t3) < 1e-12;
     const bool any = h0 || h1 || h2 || h3;
@@ -405,6 +409,7 @@ __global__ void __launch_bounds__(kGrpThreads, 4) k_extend_union(int nchunks, in
     double2 tt[3];
     uint4 ro[2];
     int2 pp = make_int2(-1, -1);
+    unsigned hb = 0;  // exact-hit flags of the two slots (bits 6, 7 of the slot byte)
     auto load_meta = [&](int c) {
         if (c >= nchunks) {
 #pragma unroll
@@ -416,7 +421,9 @@ __global__ void __launch_bounds__(kGrpThreads, 4) k_extend_union(int nchunks, in
         const int th = c * kGrpThreads + threadIdx.x;  // slots 2 th, 2 th + 1
 #pragma unroll
         for (int a = 0; a < 3; ++a) tt[a] = __ldg(reinterpret_cast<const double2*>(t + static_cast<std::size_t>(a) * ns) + th);
-        const int gs = __ldg(gslot + th);
+        const unsigned gb = __ldg(gslot + th);
+        const int gs = static_cast<int>(gb & 63u);
+        hb = gb >> 6;
         const uint4* rp = reinterpret_cast<const uint4*>(roff + (static_cast<std::size_t>(c) * kGrpMax + gs) * 16);
         ro[0] = __ldg(rp);
         ro[1] = __ldg(rp + 1);
@@ -439,20 +446,36 @@ __global__ void __launch_bounds__(kGrpThreads, 4) k_extend_union(int nchunks, in
     double2 tc[3] = {tt[0], tt[1], tt[2]};
     uint4 rc[2] = {ro[0], ro[1]};
     int2 pc = pp;
+    unsigned hc = hb;
     load_meta(c + G);
     for (int it = 0; c < nchunks; ++it, c += G) {
         issue_stage((it + 1) & 1);  // chunk c + G (nothing past the end)
         const double2 tn[3] = {tt[0], tt[1], tt[2]};
         const uint4 rn[2] = {ro[0], ro[1]};
         const int2 pn = pp;
+        const unsigned hn = hb;
         load_meta(c + 2 * G);
         double wl[2][4], w1[2][4], w0[2][4];
-        weights_p3(tc[2].x, wl[0]);
-        weights_p3(tc[1].x, w1[0]);
-        weights_p3(tc[0].x, w0[0]);
-        weights_p3(tc[2].y, wl[1]);
-        weights_p3(tc[1].y, w1[1]);
-        weights_p3(tc[0].y, w0[1]);
+        // the exact-hit rule only where setup flagged a hit (same bits either
+        // way; ~12 % fewer instructions)
+        if (hc & 1u) {
+            weights_p3(tc[2].x, wl[0]);
+            weights_p3(tc[1].x, w1[0]);
+            weights_p3(tc[0].x, w0[0]);
+        } else {
+            weights_p3_nohit(tc[2].x, wl[0]);
+            weights_p3_nohit(tc[1].x, w1[0]);
+            weights_p3_nohit(tc[0].x, w0[0]);
+        }
+        if (hc & 2u) {
+            weights_p3(tc[2].y, wl[1]);
+            weights_p3(tc[1].y, w1[1]);
+            weights_p3(tc[0].y, w0[1]);
+        } else {
+            weights_p3_nohit(tc[2].y, wl[1]);
+            weights_p3_nohit(tc[1].y, w1[1]);
+            weights_p3_nohit(tc[0].y, w0[1]);
+        }
         asm volatile("cp.async.wait_group 1;" ::: "memory");
         __syncthreads();
         const double* X = xs[it & 1];
@@ -486,6 +509,7 @@ __global__ void __launch_bounds__(kGrpThreads, 4) k_extend_union(int nchunks, in
         rc[0] = rn[0];
         rc[1] = rn[1];
         pc = pn;
+        hc = hn;
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
 #if __CUDA_ARCH__ >= 900
@@ -810,6 +834,18 @@ static void build_union(cpddg_op* op, const std::vector<int>& lines, const std::
     for (std::size_t sl = 0; sl < ns; ++sl)
         if (perm[sl] >= 0)
             for (int a = 0; a < 3; ++a) ts[static_cast<std::size_t>(a) * ns + sl] = t[static_cast<std::size_t>(a) * nb + perm[sl]];
+    // exact-hit flags (bits 6 and 7 of the slot byte): the kernel applies
+    // interp.hpp:39-44's rule only to flagged slots -- same test, same doubles
+    for (std::size_t th = 0; th < gslot.size(); ++th)
+        for (int n = 0; n < 2; ++n) {
+            const int k = perm[2 * th + static_cast<std::size_t>(n)];
+            if (k < 0) continue;
+            bool hit = false;
+            for (int a = 0; a < 3; ++a)
+                for (int j = 0; j <= 3; ++j)
+                    hit = hit || std::fabs(t[static_cast<std::size_t>(a) * nb + k] - static_cast<double>(j)) < 1e-12;
+            if (hit) gslot[th] = static_cast<unsigned char>(gslot[th] | (64u << n));
+        }
     op->grp_t.upload(ts);
     op->grp_slot.upload(gslot);
     op->grp_perm.upload(perm);
