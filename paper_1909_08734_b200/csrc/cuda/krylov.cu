@@ -294,6 +294,120 @@ __global__ void __launch_bounds__(NT) k_mgs_block(int n, int m, const double* co
         }
 }
 
+/** k_mgs_block for n <= NT E with the latency trimmed out of its passes
+ *  (small systems, BASELINE config 1, are bound by the m + 2 sequential
+ *  passes of the orthogonalisation):
+ *   - w in registers (E entries per thread, i = tid + e NT: k_mgs_block's
+ *     per-thread order), the subtraction w -= h_p V_p folded into the end of
+ *     pass p;
+ *   - the basis pointers staged in shared memory once, V_{p+2} copied into
+ *     a 3-slice shared ring by cp.async while pass p reduces (each thread
+ *     copies and reads only its own entries);
+ *   - two barriers per pass instead of four (warp partials; block_sum's
+ *     final butterfly in warp 0, h broadcast) and no global store inside the
+ *     loop -- the h values go out together at the end.
+ *  NT = 1024: same partition, same butterflies, so h, ||w||^2 and V_{m+1}
+ *  are bitwise those of k_mgs_block (tests/test_gpu_parity.py). */
+template <int NT, int E>
+__global__ void __launch_bounds__(NT) k_mgs_block_reg(int n, int m, const double* const* __restrict__ V,
+                                                      double* __restrict__ w, double* __restrict__ vnext,
+                                                      double* hout, double* wn0, const int* __restrict__ mdev,
+                                                      double* __restrict__ vin) {
+    static_assert(NT % 32 == 0 && NT <= 1024, "warp partials fit one warp");
+    constexpr int kMaxV = 64;
+    extern __shared__ __align__(16) double vs[];  // [3][E][NT]: V_p, V_{p+1}, V_{p+2} slices
+    __shared__ double sh[2][2][NT / 32];
+    __shared__ double hs[kMaxV + 2];  // h of every pass; [kMaxV + 1]: ||w||^2
+    __shared__ const double* vp_s[kMaxV];
+    if (mdev) m = *mdev;
+    if (threadIdx.x <= m && threadIdx.x < kMaxV) vp_s[threadIdx.x] = V[threadIdx.x];
+    if (mdev) {
+        vnext = const_cast<double*>(V[m + 1]);
+        wn0 = hout + m + 2;
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double wr[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int i = threadIdx.x + e * NT;
+        wr[e] = i < n ? w[i] : 0.0;
+    }
+    __syncthreads();
+    // each thread copies (cp.async, 8 bytes) and later reads only its own
+    // entries: no barrier orders the slices, and -- unlike register
+    // prefetches -- the copies in flight do not hold up the pass barriers
+    const unsigned vs_u = static_cast<unsigned>(__cvta_generic_to_shared(vs));
+    auto fetch = [&](int q) {
+        if (q <= m) {
+            const double* src = vp_s[q];
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const int i = threadIdx.x + e * NT;
+                if (i < n)
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                                     vs_u + 8u * static_cast<unsigned>(((q % 3) * E + e) * NT + threadIdx.x)),
+                                 "l"(src + i)
+                                 : "memory");
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    fetch(0);
+    fetch(1);
+    for (int pass = 0; pass <= m + 1; ++pass) {
+        const bool has_v = pass <= m;  // pass m + 1: the norm of the orthogonalised w
+        fetch(pass + 2);
+        asm volatile("cp.async.wait_group 2;" ::: "memory");  // V_pass has landed
+        const double* cur = vs + (pass % 3) * E * NT + threadIdx.x;
+        double a1 = 0.0, a2 = 0.0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            if (threadIdx.x + e * NT < n) {
+                a1 = fma(has_v ? cur[e * NT] : wr[e], wr[e], a1);
+                if (pass == 0) a2 = fma(wr[e], wr[e], a2);
+            }
+        }
+        a1 = warp_sum(a1);
+        if (pass == 0) a2 = warp_sum(a2);
+        if (lane == 0) {
+            sh[pass & 1][0][warp] = a1;
+            sh[pass & 1][1][warp] = a2;
+        }
+        __syncthreads();
+        if (warp == 0) {  // block_sum's final butterfly, then broadcast
+            const double t1 = warp_sum(lane < NT / 32 ? sh[pass & 1][0][lane] : 0.0);
+            const double t2 = pass == 0 ? warp_sum(lane < NT / 32 ? sh[0][1][lane] : 0.0) : 0.0;
+            if (lane == 0) {
+                hs[pass] = t1;  // to hout after the loop: a global store before
+                if (pass == 0) hs[kMaxV + 1] = t2;  // the next barrier would hold it up
+            }
+        }
+        __syncthreads();
+        const double h = hs[pass];
+        if (has_v) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) wr[e] -= h * cur[e * NT];
+        } else {
+            const double sub = sqrt(h);
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const int i = threadIdx.x + e * NT;
+                if (i < n) {
+                    w[i] = wr[e];
+                    if (vnext) {
+                        const double v = wr[e] / sub;
+                        vnext[i] = v;
+                        if (vin) vin[i] = v;
+                    }
+                }
+            }
+        }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    if (threadIdx.x <= m + 1) hout[threadIdx.x] = hs[threadIdx.x];
+    if (threadIdx.x == 0) *wn0 = hs[kMaxV + 1];
+}
+
 __global__ void k_scale(int n, const double* __restrict__ src, double s, double* __restrict__ dst) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = src[i] / s;
 }
@@ -590,6 +704,27 @@ struct Workspace {
         prepare_mgs(m);
         int nn = n, mm = m;
         const double* const* vpd = kc.vptr.get();
+        const char* me = std::getenv("CPDDG_MGS");  // development: "block" = k_mgs_block for every small n
+        const bool block_only = me && std::string(me) == "block";
+        if (n <= 4 * 1024 && !block_only && m < 60) {  // k_mgs_block_reg stages <= 64 basis pointers
+            static const bool attr = [] {
+                for (const void* k : {reinterpret_cast<const void*>(k_mgs_block_reg<1024, 1>),
+                                      reinterpret_cast<const void*>(k_mgs_block_reg<1024, 2>),
+                                      reinterpret_cast<const void*>(k_mgs_block_reg<1024, 4>)})
+                    CPDDG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 4 * 1024 * 8));
+                return true;
+            }();
+            (void)attr;
+            if (n <= 1024)
+                k_mgs_block_reg<1024, 1><<<1, 1024, 3 * 1 * 1024 * 8, st>>>(nn, mm, vpd, w, vnext, hout, wn0, mdev, vin);
+            else if (n <= 2 * 1024)
+                k_mgs_block_reg<1024, 2><<<1, 1024, 3 * 2 * 1024 * 8, st>>>(nn, mm, vpd, w, vnext, hout, wn0, mdev, vin);
+            else
+                k_mgs_block_reg<1024, 4><<<1, 1024, 3 * 4 * 1024 * 8, st>>>(nn, mm, vpd, w, vnext, hout, wn0, mdev, vin);
+            CPDDG_CUDA(cudaGetLastError());
+            ++launches;
+            return;
+        }
         if (n <= kSmallMgs) {
             k_mgs_block<1024><<<1, 1024, 0, st>>>(nn, mm, vpd, w, vnext, hout, wn0, mdev, vin);
             CPDDG_CUDA(cudaGetLastError());

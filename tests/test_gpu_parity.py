@@ -326,6 +326,30 @@ def test_graph_gmres_matches_host_loop(name, monkeypatch):
         assert kt["pc_launches"] >= dp.log.iterations and kt["pc_seconds"] > 0 and kt["op_seconds"] > 0
 
 
+@pytest.mark.parametrize("name", ["circle_oras_gmres", "circle_ras_gmres"])
+def test_register_mgs_matches_block_mgs(name, monkeypatch):
+    """The latency-trimmed single-CTA orthogonalisation (k_mgs_block_reg,
+    n <= 4096) reproduces k_mgs_block (CPDDG_MGS=block) bit for bit: residual
+    histories and solutions, graph- and host-driven.  (Circle ORAS amplifies
+    any roundoff difference to ~1e-7 of the initial residual by the last
+    iterations, so bitwise equality is the meaningful check.)"""
+    g, cfg, P, A, M, torch = _setup(name)
+    from paper_1909_08734_b200 import api
+    assert P.n_active <= 4096
+    b = torch.from_numpy(g["b"]).cuda()
+    monkeypatch.setenv("CPDDG_MGS", "block")
+    A_blk = api.DeviceHelmholtz.from_problem(P)  # own Krylov workspace and graph
+    for graph in ("1", "0"):
+        monkeypatch.setenv("CPDDG_GMRES_GRAPH", graph)
+        monkeypatch.delenv("CPDDG_MGS")
+        d = api.gmres_solve(A, b, M, 1e-10, 500, 50)
+        monkeypatch.setenv("CPDDG_MGS", "block")
+        h = api.gmres_solve(A_blk, b, M, 1e-10, 500, 50)
+        assert d.log.iterations == h.log.iterations
+        assert np.array_equal(np.asarray(d.log.residuals), np.asarray(h.log.residuals))
+        assert torch.equal(d.u, h.u)
+
+
 @pytest.mark.parametrize("name", ["circle_ras_stationary", "sphere10_oras_stationary"])
 def test_graph_stationary_matches_host_loop(name, monkeypatch):
     """The stationary iteration as one graph launch (device checks, while
