@@ -186,6 +186,9 @@ typedef struct {
                                    3: windowed TMA-streamed record solve (k_solve_win, the default);
                                    4: k_solve_win with the local vector in HBM (windows beyond shared memory) */
     int n_pivoted;              /* local systems factored with partial pivoting (host band LU fallback) */
+    int win_cuts;               /* k_solve_win: subdomains cut across two SMs by the balanced schedule (0: LPT lists) */
+    double win_lpt_efficiency;  /* modelled work / (SMs x longest list), whole subdomains per SM (LPT) */
+    double win_bal_efficiency;  /* the same for the balanced (cut) schedule */
 } cpddg_pc_stats;
 
 CPDDG_API int cpddg_pc_create(int n_global, int n_sub, const cpddg_local_desc* locals,

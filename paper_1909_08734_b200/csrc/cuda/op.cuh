@@ -135,7 +135,11 @@ struct cpddg_pc {
     bool win = false, win_gy = false;
     int win_rb = 16, win_grid = 0, win_smem = 0, win_wmask = 0, win_dback = 0, win_ring = 0;
     int win_reach_l = 0, win_reach_u = 0;
-    cpddg::DevBuf<int> win_cta_begin, win_cta_subs, win_desc;
+    cpddg::DevBuf<int> win_cta_begin, win_cta_subs, win_desc;  // whole-subdomain segment lists (LPT)
+    cpddg::DevBuf<int> win_bal_begin, win_bal_segs, win_hand_flag;  // balanced lists: subdomains cut once
+    cpddg::DevBuf<double> win_hand_buf;
+    int win_hand_stride = 0, win_cuts = 0;
+    double win_lpt_eff = 0.0, win_bal_eff = 0.0;  // modelled load / (grid * makespan)
     cpddg::DevBuf<std::int64_t> win_itbase;
     cpddg::DevBuf<unsigned char> win_items;
     cpddg::DevBuf<double> ybuf;

@@ -28,6 +28,7 @@
 //   columns), and the restricted scatter Rt_j^T of the owned rows.
 // Storage: L row i and U column i (transposed) are contiguous runs over
 // [f_i, i); per-row tables are concatenated over subdomains.
+#include "../host/ordering.hpp"
 #include "../host/setup.hpp"
 #include "common.cuh"
 #include "op.cuh"
@@ -79,80 +80,6 @@ struct HostSub {
     std::vector<std::int64_t> roff, roffU;
 
 };
-
-/** Reverse Cuthill-McKee of a symmetric pattern (sorted, no diagonal).
- *  Components in order of their lowest-degree node; each starts at a
- *  pseudo-peripheral node (repeated BFS, min-degree node of the last level);
- *  neighbours enqueued by (degree, index).  Returns perm[new] = old. */
-/** Symmetric pattern in CSR form: neighbours of v are adj[xadj[v] .. xadj[v+1]), sorted. */
-struct Graph {
-    std::vector<int> xadj, adj;
-    int size() const { return static_cast<int>(xadj.size()) - 1; }
-    const int* begin(int v) const { return adj.data() + xadj[static_cast<std::size_t>(v)]; }
-    const int* end(int v) const { return adj.data() + xadj[static_cast<std::size_t>(v) + 1]; }
-    int degree(int v) const { return xadj[static_cast<std::size_t>(v) + 1] - xadj[static_cast<std::size_t>(v)]; }
-};
-
-std::vector<int> rcm(const Graph& g) {
-    const int n = g.size();
-    std::vector<int> order;
-    order.reserve(static_cast<std::size_t>(n));
-    std::vector<char> done(static_cast<std::size_t>(n), 0);
-    std::vector<int> level(static_cast<std::size_t>(n), -1);
-    auto deg = [&](int v) { return g.degree(v); };
-    auto far_node = [&](int s, int& ecc) {
-        std::vector<int> q{s};
-        level[static_cast<std::size_t>(s)] = 0;
-        for (std::size_t h = 0; h < q.size(); ++h) {
-            const int v = q[h];
-            for (const int* pw = g.begin(v); pw != g.end(v); ++pw)
-                if (const int w = *pw; !done[static_cast<std::size_t>(w)] && level[static_cast<std::size_t>(w)] < 0) {
-                    level[static_cast<std::size_t>(w)] = level[static_cast<std::size_t>(v)] + 1;
-                    q.push_back(w);
-                }
-        }
-        ecc = level[static_cast<std::size_t>(q.back())];
-        int best = -1;
-        for (int v : q)
-            if (level[static_cast<std::size_t>(v)] == ecc && (best < 0 || deg(v) < deg(best) || (deg(v) == deg(best) && v < best)))
-                best = v;
-        for (int v : q) level[static_cast<std::size_t>(v)] = -1;
-        return best;
-    };
-    std::vector<int> by_deg(static_cast<std::size_t>(n));
-    std::iota(by_deg.begin(), by_deg.end(), 0);
-    std::stable_sort(by_deg.begin(), by_deg.end(), [&](int a, int b) { return deg(a) < deg(b); });
-    std::vector<int> nb;
-    for (int s0 : by_deg) {
-        if (done[static_cast<std::size_t>(s0)]) continue;
-        int ecc = 0, s = s0;
-        int cand = far_node(s, ecc);
-        for (int it = 0; it < 6; ++it) {
-            int ecc2 = 0;
-            const int nxt = far_node(cand, ecc2);
-            if (ecc2 <= ecc) break;
-            ecc = ecc2;
-            s = cand;
-            cand = nxt;
-        }
-        s = cand;
-        const std::size_t start = order.size();
-        order.push_back(s);
-        done[static_cast<std::size_t>(s)] = 1;
-        for (std::size_t h = start; h < order.size(); ++h) {
-            nb.clear();
-            for (const int* pw = g.begin(order[h]); pw != g.end(order[h]); ++pw)
-                if (!done[static_cast<std::size_t>(*pw)]) nb.push_back(*pw);
-            std::sort(nb.begin(), nb.end(), [&](int a, int b) { return deg(a) != deg(b) ? deg(a) < deg(b) : a < b; });
-            for (int w : nb) {
-                done[static_cast<std::size_t>(w)] = 1;
-                order.push_back(w);
-            }
-        }
-    }
-    std::reverse(order.begin(), order.end());
-    return order;
-}
 
 /** Sparse-row LU with partial pivoting (the explicit form P A = L U of
  *  LAPACK getrf) of an n x n system in factor order with lower bandwidth bl.
@@ -256,8 +183,59 @@ HostSub analyse(const cpddg_local_desc& d, int n_global, bool pivot = false, int
             gr.xadj[static_cast<std::size_t>(v) + 1] = static_cast<int>(gr.adj.size());
         }
     }
-    const std::vector<int> perm = rcm(gr);
+    // Ordering: reverse Cuthill-McKee, or (default) Sloan's profile ordering when
+    // it stores fewer envelope entries without pushing the longest row / column
+    // into a larger y window of k_solve_win (CPDDG_ORDER=rcm|sloan).
+    std::vector<int> perm = rcm(gr);
     std::vector<int> inv(static_cast<std::size_t>(n));
+    struct Profile {
+        std::int64_t entries = 0;
+        int reach = 0;
+    };
+    auto profile_of = [&](const std::vector<int>& pm) {
+        for (int k = 0; k < n; ++k) inv[static_cast<std::size_t>(pm[static_cast<std::size_t>(k)])] = k;
+        std::vector<int> fl(static_cast<std::size_t>(n)), fu(static_cast<std::size_t>(n));
+        std::iota(fl.begin(), fl.end(), 0);
+        std::iota(fu.begin(), fu.end(), 0);
+        for (int r = 0; r < n; ++r)
+            for (std::int64_t k = rp[r]; k < rp[r + 1]; ++k) {
+                const int c = d.col[k];
+                if (c >= n || c == r) continue;
+                const int pi = inv[static_cast<std::size_t>(r)], pj = inv[static_cast<std::size_t>(c)];
+                if (pj < pi)
+                    fl[static_cast<std::size_t>(pi)] = std::min(fl[static_cast<std::size_t>(pi)], pj);
+                else
+                    fu[static_cast<std::size_t>(pj)] = std::min(fu[static_cast<std::size_t>(pj)], pi);
+            }
+        Profile P;
+        for (int i = 0; i < n; ++i) {
+            P.entries += (i - fl[static_cast<std::size_t>(i)]) + (i - fu[static_cast<std::size_t>(i)]);
+            P.reach = std::max({P.reach, i - fl[static_cast<std::size_t>(i)], i - fu[static_cast<std::size_t>(i)]});
+        }
+        return P;
+    };
+    static const bool use_sloan = [] {
+        const char* e = std::getenv("CPDDG_ORDER");
+        return !(e && std::string(e) == "rcm");
+    }();
+    if (use_sloan && n > 64) {
+        auto window = [](int reach) {  // k_solve_win's window class (win_geometry, RB = 16)
+            int W = 2048;
+            while (W < reach + 96) W *= 2;
+            return W;
+        };
+        const Profile base = profile_of(perm);
+        Profile best = base;
+        for (int w1 : {8, 32}) {
+            std::vector<int> cand = sloan(gr, w1, 1);
+            const Profile P = profile_of(cand);
+            if (P.entries < best.entries && window(P.reach) <= window(base.reach)) {
+                best = P;
+                perm = std::move(cand);
+                break;
+            }
+        }
+    }
     for (int k = 0; k < n; ++k) inv[static_cast<std::size_t>(perm[static_cast<std::size_t>(k)])] = k;
     PivLU F;
     if (pivot) {
@@ -2433,7 +2411,33 @@ __global__ void __launch_bounds__(tmas::kThreads, 1) k_solve_tma(const int* __re
 // every row above, thread per row pair); one named barrier per step.
 // GY = true keeps y in ybuf itself (global memory, no window): the fallback
 // for windows that do not fit shared memory.
+//
+// Work units are SEGMENTS: a range [t0, t1) of the 2 nblk steps of one
+// subdomain (t < nblk: forward step k = t; else backward step
+// K = 2 nblk - 1 - t; the item of step t is items[itbase[j] + t]).  The
+// default table balances the SMs exactly by McNaughton's wrap-around rule
+// (setup_win): a subdomain may be cut once, its first part at the head of one
+// CTA's list and its second part at the tail of the previous CTA's, with the
+// state handed over through global memory -- ybuf holds every solved row; a
+// cut inside the forward pass adds the partial dots of the next block
+// (red[][]), a cut inside the backward pass the window itself (pending column
+// updates) -- behind a release / acquire flag that the receiver clears.  The
+// handed-over values are the ones the unsplit kernel would hold, so results
+// are bitwise independent of the cuts.
 namespace win {
+struct Seg {
+    int j, t0, t1;  // subdomain, step range
+    int hand;       // hand-over slot (flag + scratch) of the subdomain's cut, -1: none
+};
+static_assert(sizeof(Seg) == 16, "segments are 16 bytes");
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 constexpr int kConsumers = 8;                     // consumer warps 1 .. 8
 constexpr int kThreads = 32 * (kConsumers + 2);   // + warp 0 (solve, helpers) + producer warp
 constexpr int kStep = kThreads - 32;              // warps 0 .. 8: named barrier 1
@@ -2464,15 +2468,16 @@ __device__ __forceinline__ void sts2(unsigned a, double2 v) {
 }
 }  // namespace win
 
-template <int RB, int MODE, bool GY>
+template <int RB, bool GY>
 __global__ void __launch_bounds__(win::kThreads, 1) k_solve_win(const int* __restrict__ cta_begin,
-                                                                const int* __restrict__ cta_subs,
+                                                                const win::Seg* __restrict__ segs,
                                                                 const int* __restrict__ n_rows,
                                                                 const std::int64_t* __restrict__ vbase,
                                                                 const std::int64_t* __restrict__ itbase,
                                                                 const win::Item* __restrict__ items,
                                                                 double* ybuf, int wmask, int dback, int ring_bytes,
-                                                                int dbg) {
+                                                                int mode, int* hand_flag, double* hand_buf,
+                                                                int hand_stride, int dbg) {
     using G = win::Geo<RB>;
     constexpr int TS = G::TS, kDesc = G::kDesc, kHdr = G::kHdr, NS = win::NS, kC = win::kConsumers;
     using tmas::smem_u32;
@@ -2493,7 +2498,11 @@ __global__ void __launch_bounds__(win::kThreads, 1) k_solve_win(const int* __res
     __shared__ double red[2][kC][RB];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int s0 = cta_begin[blockIdx.x], s1 = cta_begin[blockIdx.x + 1];
-    constexpr bool kFwd = MODE != 2, kBwd = MODE != 1;
+    // mode 1 / 2 (timing experiments): the forward / backward steps only, no hand-overs
+    auto clip = [&](const win::Seg& g, int nblk, int& a, int& b) {
+        a = mode == 2 ? max(g.t0, nblk) : g.t0;
+        b = mode == 1 ? min(g.t1, nblk) : g.t1;
+    };
     if (tid == 0) {
         for (int q = 0; q < NS; ++q) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar[q])));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -2508,29 +2517,30 @@ __global__ void __launch_bounds__(win::kThreads, 1) k_solve_win(const int* __res
         const unsigned long long RING = static_cast<unsigned long long>(ring_bytes);
         unsigned long long head = 0;  // virtual ring position (bytes)
         int t = 0;
-        int si = s0, pass = kFwd ? 0 : 1, q = 0;
-        int nblk = si < s1 ? (n_rows[cta_subs[si]] + RB - 1) / RB : 0;
-        auto item_at = [&](int s, int ps, int qq) -> const win::Item* {
-            const int j = cta_subs[s];
-            const int nb = (n_rows[j] + RB - 1) / RB;
-            return items + itbase[j] + static_cast<std::int64_t>(ps) * nb + qq;
+        int si = s0, q = 0, qe = 0;  // segment, its current and end step
+        const win::Item* ibase = nullptr;
+        auto open_seg = [&]() {  // first non-empty segment at or after si
+            for (; si < s1; ++si) {
+                const win::Seg g = segs[si];
+                clip(g, (n_rows[g.j] + RB - 1) / RB, q, qe);
+                if (q < qe) {
+                    ibase = items + itbase[g.j];
+                    return;
+                }
+            }
         };
         auto advance = [&]() {
-            if (++q < nblk) return;
-            q = 0;
-            if (pass == 0 && kBwd) {
-                pass = 1;
-                return;
-            }
-            pass = kFwd ? 0 : 1;
-            if (++si < s1) nblk = (n_rows[cta_subs[si]] + RB - 1) / RB;
+            if (++q < qe) return;
+            ++si;
+            open_seg();
         };
+        open_seg();
         win::Item cur{};
-        if (si < s1) cur = *item_at(si, pass, q);
+        if (si < s1) cur = ibase[q];
         while (si < s1) {
             advance();
             win::Item nxt{};
-            if (si < s1) nxt = *item_at(si, pass, q);  // in flight while this item is issued
+            if (si < s1) nxt = ibase[q];  // in flight while this item is issued
             const int slot = t % NS;
             const bool big = kHdr + cur.bytes > ring_bytes;  // data read from HBM by the consumers
             const unsigned long long need = (kHdr + (big ? 0 : cur.bytes) + 127) & ~127ULL;
@@ -2574,9 +2584,18 @@ __global__ void __launch_bounds__(win::kThreads, 1) k_solve_win(const int* __res
     int t = 0;
     double hv0 = 0.0, hv1 = 0.0;  // helper registers: hv[b & 1] holds block b's entering value
     for (int si = s0; si < s1; ++si) {
-        const int j = cta_subs[si];
+        const win::Seg sg = segs[si];
+        const int j = sg.j;
         const int n = n_rows[j];
         const int nblk = (n + RB - 1) / RB;
+        int t0, t1;
+        clip(sg, nblk, t0, t1);
+        if (t0 >= t1) continue;
+        const bool handover = mode == 0 && sg.hand >= 0;
+        const bool resume = handover && sg.t0 > 0;          // another CTA ran steps [0, t0)
+        const bool publish = handover && sg.t1 < 2 * nblk;  // another CTA runs steps [t1, 2 nblk)
+        int* hflag = hand_flag + (handover ? sg.hand : 0);
+        double* hbuf = hand_buf + static_cast<std::int64_t>(handover ? sg.hand : 0) * hand_stride;
         double* yb = ybuf + vbase[j];
         double* y = GY ? yb : ywin;
         const int wm = GY ? -1 : wmask;
@@ -2589,18 +2608,51 @@ __global__ void __launch_bounds__(win::kThreads, 1) k_solve_win(const int* __res
             else
                 return lds2(ywin_u + 8u * static_cast<unsigned>(row & wm));
         };
+        // ybuf is read past L1 (rows next to another CTA's subdomain share its lines)
         auto ldblk = [&](int b) -> double {  // row b RB + h of ybuf (0 past the ends)
             const int row = b * RB + h;
-            return b >= 0 && row < n ? yb[row] : 0.0;
+            return b >= 0 && row < n ? __ldcg(yb + row) : 0.0;
         };
-        if constexpr (kFwd) {
-            if (!GY && helper) {
-                ywin[h & wm] = ldblk(0);
-                hv1 = ldblk(1);
-                hv0 = ldblk(2);
+        if (resume) {
+            // the first part's rows, partial dots / window are published before its flag
+            if (tid == 0) {
+                while (win::ld_acquire(hflag) == 0) __nanosleep(100);
+                *hflag = 0;  // one waiter per cut: ready for the next apply
+                __threadfence();
             }
-            if (warp == 0) __syncwarp();
-            for (int k = 0; k < nblk; ++k, ++t) {
+            step_bar();
+        }
+        if (t0 < nblk) {
+            const int k1 = min(t1, nblk);
+            if (t0 == 0) {
+                if (!GY && helper) {
+                    ywin[h & wm] = ldblk(0);
+                    hv1 = ldblk(1);
+                    hv0 = ldblk(2);
+                }
+                if (warp == 0) __syncwarp();
+            } else {
+                // resume at forward step t0: the window's rows below block t0 + 1 (solved rows,
+                // block t0's right-hand side), the next two entering blocks, block t0's partial dots
+                if (!GY) {
+                    const int hi = (t0 + 1) * RB;
+                    for (int row = max(0, hi - (wm + 1)) + (warp == 0 ? lane : 32 + ct); row < hi; row += win::kStep)
+                        ywin[row & wm] = row < n ? __ldcg(yb + row) : 0.0;
+                    if (helper) {
+                        if (t0 & 1) {
+                            hv0 = ldblk(t0 + 1);
+                            hv1 = ldblk(t0 + 2);
+                        } else {
+                            hv1 = ldblk(t0 + 1);
+                            hv0 = ldblk(t0 + 2);
+                        }
+                    }
+                }
+                for (int e = (warp == 0 ? lane : 32 + ct); e < kC * RB; e += win::kStep)
+                    (&red[t0 & 1][0][0])[e] = __ldcg(hbuf + e);
+                step_bar();
+            }
+            for (int k = t0; k < k1; ++k, ++t) {
                 const int slot = t % NS;
                 mbar_wait(smem_u32(&mbar[slot]), static_cast<unsigned>((t / NS) & 1));
                 const int hoff = item_pos[slot];
@@ -2711,15 +2763,32 @@ __global__ void __launch_bounds__(win::kThreads, 1) k_solve_win(const int* __res
                 step_bar();
                 if (tid == 0) done = t + 1;
             }
+            if (publish && t1 <= nblk) {
+                // cut inside (or at the end of) the forward pass: block t1's partial dots
+                if (t1 < nblk)
+                    for (int e = (warp == 0 ? lane : 32 + ct); e < kC * RB; e += win::kStep)
+                        hbuf[e] = (&red[t1 & 1][0][0])[e];
+                step_bar();
+                if (tid == 0) {
+                    __threadfence();
+                    win::st_release(hflag, 1);
+                }
+            }
         }
-        if constexpr (kBwd) {
-            // window: the last D + 2 blocks (the forward results, 0 past n)
+        if (t1 > nblk) {
+            const int Khi = 2 * nblk - 1 - max(t0, nblk), Klo = 2 * nblk - t1;
             if (!GY) {
-                const int lo = max(0, (nblk - 2 - dback) * RB);
-                for (int row = lo + (warp == 0 ? lane : 32 + ct); row < nblk * RB; row += win::kStep)
-                    ywin[row & wm] = row < n ? yb[row] : 0.0;
+                if (t0 <= nblk) {
+                    // window: the last D + 2 blocks (the forward results, 0 past n)
+                    const int lo = max(0, (nblk - 2 - dback) * RB);
+                    for (int row = lo + (warp == 0 ? lane : 32 + ct); row < nblk * RB; row += win::kStep)
+                        ywin[row & wm] = row < n ? __ldcg(yb + row) : 0.0;
+                } else {
+                    // resume inside the backward pass: the first part's window (pending column updates)
+                    for (int e = (warp == 0 ? lane : 32 + ct); e <= wm; e += win::kStep) ywin[e] = __ldcg(hbuf + e);
+                }
                 if (helper) {
-                    const int e = nblk - 1 - dback;
+                    const int e = Khi - dback;
                     if (e & 1) {
                         hv1 = ldblk(e);
                         hv0 = ldblk(e - 1);
@@ -2730,7 +2799,7 @@ __global__ void __launch_bounds__(win::kThreads, 1) k_solve_win(const int* __res
                 }
                 step_bar();
             }
-            for (int K = nblk - 1; K >= 0; --K, ++t) {
+            for (int K = Khi; K >= Klo; --K, ++t) {
                 const int slot = t % NS;
                 mbar_wait(smem_u32(&mbar[slot]), static_cast<unsigned>((t / NS) & 1));
                 const int hoff = item_pos[slot];
@@ -2820,6 +2889,16 @@ __global__ void __launch_bounds__(win::kThreads, 1) k_solve_win(const int* __res
                 }
                 step_bar();
                 if (tid == 0) done = t + 1;
+            }
+            if (publish) {
+                // cut inside the backward pass: the window goes with the flag
+                if (!GY)
+                    for (int e = (warp == 0 ? lane : 32 + ct); e <= wm; e += win::kStep) hbuf[e] = ywin[e];
+                step_bar();
+                if (tid == 0) {
+                    __threadfence();
+                    win::st_release(hflag, 1);
+                }
             }
         }
     }
@@ -3008,17 +3087,19 @@ void pc_apply_mode(const cpddg_pc* pc, const double* r, double* z, bool accumula
             k_win_gather<<<gblocks, 256, 0, st>>>(rows, pc->gidx.get(), r, yb);
         }
         const int m = mode == 3 ? 0 : mode;
+        // balanced (cut) lists for full applies with the shared-memory window
+        const bool bal = m == 0 && !pc->win_gy && pc->win_cuts > 0;
         auto pick = [&](auto rbc) {
             constexpr int RB = decltype(rbc)::value;
-            if (pc->win_gy)
-                return m == 1 ? k_solve_win<RB, 1, true> : m == 2 ? k_solve_win<RB, 2, true> : k_solve_win<RB, 0, true>;
-            return m == 1 ? k_solve_win<RB, 1, false> : m == 2 ? k_solve_win<RB, 2, false> : k_solve_win<RB, 0, false>;
+            return pc->win_gy ? k_solve_win<RB, true> : k_solve_win<RB, false>;
         };
         auto kern = rb == 8 ? pick(std::integral_constant<int, 8>{}) : pick(std::integral_constant<int, 16>{});
         kern<<<pc->win_grid, win::kThreads, pc->win_smem, st>>>(
-            pc->win_cta_begin.get(), pc->win_cta_subs.get(), pc->n_rows.get(), pc->vbase.get(), pc->win_itbase.get(),
-            reinterpret_cast<const win::Item*>(pc->win_items.get()), yb, pc->win_wmask, pc->win_dback, pc->win_ring,
-            dbg);
+            (bal ? pc->win_bal_begin : pc->win_cta_begin).get(),
+            reinterpret_cast<const win::Seg*>((bal ? pc->win_bal_segs : pc->win_cta_subs).get()), pc->n_rows.get(),
+            pc->vbase.get(), pc->win_itbase.get(), reinterpret_cast<const win::Item*>(pc->win_items.get()), yb,
+            pc->win_wmask, pc->win_dback, pc->win_ring, m, pc->win_hand_flag.get(), pc->win_hand_buf.get(),
+            pc->win_hand_stride, dbg);
         CPDDG_CUDA(cudaGetLastError());
         if (mode != 3) {
             k_win_scatter<<<gblocks, 256, 0, st>>>(rows, pc->sidx.get(), yb, z, accumulate ? 1 : 0);
@@ -3319,10 +3400,95 @@ static bool setup_win(cpddg_pc* pc, const std::vector<int>& n_rows, const std::v
         lists[static_cast<std::size_t>(m)].push_back(j);
         load[static_cast<std::size_t>(m)] += cost[static_cast<std::size_t>(j)];
     }
-    std::vector<int> begin{0}, subs;
-    for (const auto& L : lists) {
-        subs.insert(subs.end(), L.begin(), L.end());
-        begin.push_back(static_cast<int>(subs.size()));
+    // whole-subdomain segments (modes 1 / 2, the global-y variant, CPDDG_WIN_SPLIT=0)
+    std::vector<int> begin{0}, segs;
+    std::int64_t total = 0, lpt_span = 0, chain = 0;
+    for (std::size_t m = 0; m < lists.size(); ++m) {
+        for (int j : lists[m]) {
+            const int nblk = (n_rows[static_cast<std::size_t>(j)] + RB - 1) / RB;
+            segs.insert(segs.end(), {j, 0, 2 * nblk, -1});
+        }
+        begin.push_back(static_cast<int>(segs.size() / 4));
+        lpt_span = std::max(lpt_span, load[m]);
+    }
+    for (int j = 0; j < n_sub; ++j) {
+        total += cost[static_cast<std::size_t>(j)];
+        chain = std::max(chain, cost[static_cast<std::size_t>(j)]);
+    }
+    pc->win_lpt_eff = static_cast<double>(total) / (static_cast<double>(grid) * static_cast<double>(lpt_span));
+    // balanced segments: McNaughton's wrap-around rule.  The subdomains lie end
+    // to end on a line cut every `quota` (>= the longest chain); a subdomain
+    // across a cut runs its FIRST steps at the head of the next CTA's list and
+    // its LAST steps at the tail of this CTA's, so the two parts never overlap
+    // in time (cost <= quota) and the tail part finds its flag set.
+    {
+        const std::int64_t quota = std::max((total + grid - 1) / grid, chain);
+        std::vector<std::vector<int>> bl(static_cast<std::size_t>(grid));
+        std::vector<std::int64_t> bload(static_cast<std::size_t>(grid), 0);
+        auto step_cost = [&](int j, int t) {
+            return c0 * 1024 + c1 * (G::kHdr + items[static_cast<std::size_t>(itbase[static_cast<std::size_t>(j)] + t)].bytes);
+        };
+        std::int64_t pos = 0;
+        int cuts = 0;
+        for (int j : by_cost) {
+            const int nsteps = 2 * ((n_rows[static_cast<std::size_t>(j)] + RB - 1) / RB);
+            const std::int64_t cj = cost[static_cast<std::size_t>(j)];
+            const int m = static_cast<int>(std::min<std::int64_t>(pos / quota, grid - 1));
+            const std::int64_t room = static_cast<std::int64_t>(m + 1) * quota - pos;  // left on CTA m
+            int x = 0;  // steps [x, nsteps) stay on CTA m, [0, x) go to CTA m + 1
+            if (cj > room && m + 1 < grid) {
+                std::int64_t tail = 0;
+                x = nsteps;
+                while (x > 0 && tail + step_cost(j, x - 1) <= room) tail += step_cost(j, --x);
+                // nearest step boundary to the cut
+                if (x > 0 && room - tail > (tail + step_cost(j, x - 1)) - room) tail += step_cost(j, --x);
+                if (x == 0) x = 0;
+            }
+            if (x == 0) {
+                bl[static_cast<std::size_t>(m)].insert(bl[static_cast<std::size_t>(m)].end(), {j, 0, nsteps, -1});
+                bload[static_cast<std::size_t>(m)] += cj;
+            } else if (x == nsteps) {
+                bl[static_cast<std::size_t>(m) + 1].insert(bl[static_cast<std::size_t>(m) + 1].end(), {j, 0, nsteps, -1});
+                bload[static_cast<std::size_t>(m) + 1] += cj;
+            } else {
+                std::int64_t headc = 0;
+                for (int t = 0; t < x; ++t) headc += step_cost(j, t);
+                bl[static_cast<std::size_t>(m)].insert(bl[static_cast<std::size_t>(m)].end(), {j, x, nsteps, cuts});
+                bl[static_cast<std::size_t>(m) + 1].insert(bl[static_cast<std::size_t>(m) + 1].end(), {j, 0, x, cuts});
+                bload[static_cast<std::size_t>(m)] += cj - headc;
+                bload[static_cast<std::size_t>(m) + 1] += headc;
+                ++cuts;
+            }
+            pos += cj;
+        }
+        // a CTA's list: the head part (pushed by the previous CTA's last subdomain)
+        // first, then whole subdomains, then the tail part
+        std::vector<int> bbegin{0}, bsegs;
+        for (auto& L : bl) {
+            std::vector<int> headp, mid, tailp;
+            for (std::size_t e = 0; e < L.size(); e += 4) {
+                std::vector<int>& dst = L[e + 3] < 0 ? mid : L[e + 1] == 0 ? headp : tailp;
+                dst.insert(dst.end(), L.begin() + static_cast<std::ptrdiff_t>(e), L.begin() + static_cast<std::ptrdiff_t>(e) + 4);
+            }
+            bsegs.insert(bsegs.end(), headp.begin(), headp.end());
+            bsegs.insert(bsegs.end(), mid.begin(), mid.end());
+            bsegs.insert(bsegs.end(), tailp.begin(), tailp.end());
+            bbegin.push_back(static_cast<int>(bsegs.size() / 4));
+        }
+        const std::int64_t bal_span = *std::max_element(bload.begin(), bload.end());
+        pc->win_bal_eff = static_cast<double>(total) / (static_cast<double>(grid) * static_cast<double>(bal_span));
+        pc->win_cuts = cuts;
+        if (const char* e = std::getenv("CPDDG_WIN_SPLIT"))  // development: 0 = whole subdomains per CTA (LPT)
+            if (std::atoi(e) == 0) pc->win_cuts = 0;
+        pc->win_hand_stride = std::max(W, win::kConsumers * RB);
+        pc->win_bal_begin.upload(bbegin);
+        pc->win_bal_segs.upload(bsegs);
+        std::vector<int> zero(static_cast<std::size_t>(std::max(cuts, 1)), 0);
+        pc->win_hand_flag.upload(zero);
+        pc->win_hand_buf.alloc(static_cast<std::size_t>(std::max(cuts, 1)) * static_cast<std::size_t>(pc->win_hand_stride));
+        if (std::getenv("CPDDG_VERBOSE"))
+            std::fprintf(stderr, "[cpddg] win schedule: %d CTAs, modelled efficiency LPT %.3f, balanced %.3f (%d cuts)\n", grid,
+                         pc->win_lpt_eff, pc->win_bal_eff, cuts);
     }
     CPDDG_CUDA(cudaMemcpy(ddesc.get(), desc.data(), desc.size() * sizeof(int), cudaMemcpyHostToDevice));
     pc->win_desc = std::move(ddesc);
@@ -3330,7 +3496,7 @@ static bool setup_win(cpddg_pc* pc, const std::vector<int>& n_rows, const std::v
     CPDDG_CUDA(cudaMemcpy(pc->win_items.get(), items.data(), items.size() * sizeof(win::Item), cudaMemcpyHostToDevice));
     pc->win_itbase.upload(itbase);
     pc->win_cta_begin.upload(begin);
-    pc->win_cta_subs.upload(subs);
+    pc->win_cta_subs.upload(segs);
     pc->win_grid = grid;
     pc->win_gy = gy;
     pc->win_wmask = W - 1;
@@ -3340,8 +3506,7 @@ static bool setup_win(cpddg_pc* pc, const std::vector<int>& n_rows, const std::v
     pc->win_reach_l = reachL;
     pc->win_reach_u = reachU;
     pc->ybuf.alloc(static_cast<std::size_t>(std::max<std::int64_t>(pc->rows_total, 1)));
-    for (auto kern : {k_solve_win<RB, 0, false>, k_solve_win<RB, 1, false>, k_solve_win<RB, 2, false>,
-                      k_solve_win<RB, 0, true>, k_solve_win<RB, 1, true>, k_solve_win<RB, 2, true>})
+    for (auto kern : {k_solve_win<RB, false>, k_solve_win<RB, true>})
         raise_smem_limit(reinterpret_cast<const void*>(kern), pc->win_smem);
     pc->win = true;
     return true;
@@ -4033,6 +4198,9 @@ int cpddg_pc_stats_get(const cpddg_pc* pc, cpddg_pc_stats* st) {
         st->max_probe_residual = pc->max_probe_residual;
         st->apply_mode = pc->dense ? 1 : pc->tma ? 2 : pc->win ? (pc->win_gy ? 4 : 3) : 0;
         st->n_pivoted = pc->n_pivoted;
+        st->win_cuts = pc->win && !pc->win_gy ? pc->win_cuts : 0;
+        st->win_lpt_efficiency = pc->win ? pc->win_lpt_eff : 0.0;
+        st->win_bal_efficiency = pc->win ? pc->win_bal_eff : 0.0;
     });
 }
 

@@ -412,7 +412,9 @@ def test_streamed_record_and_chain_solves_agree(monkeypatch):
     subdomain) at the usual 1e-9:
 
     * k_solve_win, the default: windowed, TMA-streamed record solve, RB = 16
-      (apply_mode 3); also with RB = 8, with y kept in global memory
+      (apply_mode 3) on the balanced schedule (subdomains cut across two SMs,
+      state handed over through global memory: bitwise equal to whole
+      subdomains per SM, CPDDG_WIN_SPLIT=0); also with RB = 8, with y kept in global memory
       (CPDDG_WIN_GY=1, apply_mode 4: the path for windows larger than shared
       memory), and with a ring so small that every item's data is read from
       HBM (CPDDG_WIN_RING);
@@ -440,8 +442,12 @@ def test_streamed_record_and_chain_solves_agree(monkeypatch):
 
     M = build()
     assert M.stats()["apply_mode"] == 3
+    # 256 subdomains on fewer SMs: the balanced schedule cuts subdomains across two SMs
+    assert M.stats()["win_cuts"] > 0 and M.stats()["win_bal_efficiency"] >= M.stats()["win_lpt_efficiency"]
     variants = {
+        "win_unsplit": (build(CPDDG_WIN_SPLIT="0"), 3),
         "win_rb8": (build(CPDDG_WIN_RB="8"), 3),
+        "win_rb8_unsplit": (build(CPDDG_WIN_RB="8", CPDDG_WIN_SPLIT="0"), 3),
         "win_global_y": (build(CPDDG_WIN_GY="1"), 4),
         "win_items_from_hbm": (build(CPDDG_WIN_RING="9216"), 3),
         "tma": (build(CPDDG_SOLVE="tma"), 2),
@@ -460,6 +466,11 @@ def test_streamed_record_and_chain_solves_agree(monkeypatch):
         assert np.linalg.norm(m.apply(xd).cpu().numpy() - zc) <= 1e-12 * nz, name
     assert np.linalg.norm(z - zc) <= 1e-12 * nz
     assert np.array_equal(z, M.apply(xd).cpu().numpy())  # bitwise reproducible
+    # the hand-over of a cut subdomain carries exactly the state the unsplit kernel holds
+    assert variants["win_unsplit"][0].stats()["win_cuts"] == 0
+    assert np.array_equal(z, variants["win_unsplit"][0].apply(xd).cpu().numpy())
+    assert np.array_equal(variants["win_rb8"][0].apply(xd).cpu().numpy(),
+                          variants["win_rb8_unsplit"][0].apply(xd).cpu().numpy())
     locs = [P.local(j) for j in range(P.n_sub)]
     z_ref = O.schwarz_apply(locs, x)
     assert np.linalg.norm(z - z_ref) <= 1e-9 * np.linalg.norm(z_ref)
