@@ -189,6 +189,8 @@ typedef struct {
     int win_cuts;               /* k_solve_win: subdomains cut across two SMs by the balanced schedule (0: LPT lists) */
     double win_lpt_efficiency;  /* modelled work / (SMs x longest list), whole subdomains per SM (LPT) */
     double win_bal_efficiency;  /* the same for the balanced (cut) schedule */
+    int64_t n_dropped;          /* local unknowns no other row refers to and no scatter returns (ORAS ring /
+                                   ghost-type closure rows, transmission.hpp:84-92), removed before the factorisation */
 } cpddg_pc_stats;
 
 CPDDG_API int cpddg_pc_create(int n_global, int n_sub, const cpddg_local_desc* locals,

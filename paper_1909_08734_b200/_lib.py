@@ -51,7 +51,8 @@ class cpddg_pc_stats(C.Structure):
                 ("algorithmic_bytes", C.c_int64), ("max_rows", C.c_int),
                 ("factor_seconds", C.c_double), ("analyse_seconds", C.c_double),
                 ("max_probe_residual", C.c_double), ("apply_mode", C.c_int), ("n_pivoted", C.c_int),
-                ("win_cuts", C.c_int), ("win_lpt_efficiency", C.c_double), ("win_bal_efficiency", C.c_double)]
+                ("win_cuts", C.c_int), ("win_lpt_efficiency", C.c_double), ("win_bal_efficiency", C.c_double),
+                ("n_dropped", C.c_int64)]
 
 
 class cpddg_solve_params(C.Structure):

@@ -83,6 +83,7 @@ struct cpddg_op {
 struct cpddg_pc {
     int n_global = 0, n_sub = 0, max_rows = 0;
     int n_reduced = 0, n_pivoted = 0;  // Dirichlet-reduced / host-pivoted local systems
+    std::int64_t n_dropped = 0;        // local unknowns nothing depends on, removed before the analysis
     std::int64_t rows_total = 0, entries = 0;
     // per subdomain (device)
     cpddg::DevBuf<int> n_rows;         // [n_sub]

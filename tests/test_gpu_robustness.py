@@ -111,3 +111,66 @@ def test_large_subdomains_run_with_the_window_in_hbm(monkeypatch):
     locs = [P.local(j) for j in range(P.n_sub)]
     z_ref = O.schwarz_apply(locs, x)
     assert np.linalg.norm(z - z_ref) <= 1e-9 * np.linalg.norm(z_ref)
+
+
+def test_unreferenced_closure_unknowns_are_dropped(monkeypatch):
+    """ORAS closures hold ring / ghost-type unknowns that only their own
+    transmission row refers to (transmission.hpp:84-92) and that are never
+    scattered back (:66-69): the device path removes them before the analysis.
+    The reduced preconditioner equals the whole one (CPDDG_DROP=0) and the
+    oracle restatement; RAS closures (unit rows) reduce as before; a hand-made
+    chain of such unknowns is removed to the fixed point."""
+    import torch
+
+    import cpdd_oracle as O
+    from paper_1909_08734_b200 import api, inputs
+    P = api.Problem("sphere", h=0.05, p=3, c=1.0)
+    P.decompose(inputs.rcb_partition(P.active_cp, 64), 2, "oras", 4.0, 40.0)
+    A = api.DeviceHelmholtz.from_problem(P)
+    M = api.SchwarzPreconditioner.from_problem(P)
+    monkeypatch.setenv("CPDDG_DROP", "0")
+    Mw = api.SchwarzPreconditioner.from_problem(P)
+    monkeypatch.delenv("CPDDG_DROP")
+    st, sw = M.stats(), Mw.stats()
+    assert sw["n_dropped"] == 0 and st["n_dropped"] > 0
+    assert st["n_rows_total"] == sw["n_rows_total"] - st["n_dropped"]
+    assert st["n_dropped"] >= 0.2 * sw["n_rows_total"]       # ~26 % of the unknowns at this size
+    assert st["factor_entries"] <= 0.8 * sw["factor_entries"]  # and ~30 % of the streamed entries
+    x = inputs.uniform_vector(P.n_active, 11)
+    xd = torch.from_numpy(x).cuda()
+    z, zw = M.apply(xd).cpu().numpy(), Mw.apply(xd).cpu().numpy()
+    assert np.linalg.norm(z - zw) <= 1e-12 * np.linalg.norm(zw)
+    locs = [P.local(j) for j in range(P.n_sub)]
+    z_ref = O.schwarz_apply(locs, x)
+    assert np.linalg.norm(z - z_ref) <= 1e-9 * np.linalg.norm(z_ref)
+    b = torch.from_numpy(inputs.rhs_sphere(P.active_cp)).cuda()
+    r, rw = (api.gmres_solve(A, b, m, 1e-10, 1000, 50) for m in (M, Mw))
+    assert r.log.iterations == rw.log.iterations
+    assert np.linalg.norm(r.u.cpu().numpy() - rw.u.cpu().numpy()) <= 1e-9 * np.linalg.norm(rw.u.cpu().numpy())
+
+    # RAS: the closure rows are unit rows; ghost-type ones drop, the rest is the Dirichlet reduction
+    P.decompose(inputs.rcb_partition(P.active_cp, 64), 2, "ras")
+    Mr = api.SchwarzPreconditioner.from_problem(P)
+    assert Mr.stats()["n_reduced"] == 64
+    zr = Mr.apply(xd).cpu().numpy()
+    zr_ref = O.schwarz_apply([P.local(j) for j in range(P.n_sub)], x)
+    assert np.linalg.norm(zr - zr_ref) <= 1e-9 * np.linalg.norm(zr_ref)
+
+    # a chain: unknown 5 is referenced only by row 6, unknown 6 only by its own row
+    import scipy.sparse as sp
+    rng = np.random.default_rng(5)
+    n = 7
+    B = np.zeros((n, n))
+    B[:5, :5] = rng.uniform(-1, 1, (5, 5)) + 6 * np.eye(5)
+    B[5, 5], B[5, :3] = 2.0, (0.5, -0.25, 0.125)
+    B[6, 6], B[6, 5], B[6, 1] = 4.0, 1.0, -1.0
+    Bs = sp.csr_matrix(B)
+    idx = np.arange(5, dtype=np.int32)
+    loc = dict(n_overlap=5, n_bc=2, overlap=idx, scatter_local=idx, scatter_global=idx,
+               ptr=Bs.indptr.astype(np.int64), col=Bs.indices.astype(np.int32), val=Bs.data.astype(np.float64))
+    Mc = api.SchwarzPreconditioner.from_locals(5, [loc])
+    assert Mc.stats()["n_dropped"] == 2 and Mc.stats()["n_rows_total"] == 5
+    rhs = rng.uniform(-1, 1, 5)
+    want = np.linalg.solve(B, np.concatenate([rhs, np.zeros(2)]))[:5]
+    got = Mc.apply(torch.from_numpy(rhs).cuda()).cpu().numpy()
+    assert np.linalg.norm(got - want) <= 1e-13 * np.linalg.norm(want)
