@@ -116,7 +116,9 @@ def oracle_lu_ratio(w, stored):
     if d.get("config") != workload_name(w):
         return None
     return {"ratio_entries": stored / d["sum_nnz_LU"], "oracle_sum_nnz_LU": d["sum_nnz_LU"],
-            "ratio_bytes_vs_12B_per_nz": 8.0 * stored / (12.0 * d["sum_nnz_LU"]), "source": "profiles/r02_factor_format.json"}
+            "ratio_bytes_vs_12B_per_nz": 8.0 * stored / (12.0 * d["sum_nnz_LU"]), "source": "profiles/r02_factor_format.json",
+            "note": "oracle: SuperLU-COLAMD on the WHOLE local systems (what the reference's DirectSolver factors); "
+                    "stored: envelopes of the reduced systems (details.pc.n_dropped unknowns removed)"}
 
 
 def ncu_traffic():
@@ -453,7 +455,7 @@ def main():
                         "device_factor": pcs["factor_seconds"], "host_analyse": pcs["analyse_seconds"],
                         "phases": P.phase_seconds(), "device_setup": P.device_setup},
             "pc": {k: pcs[k] for k in ("factor_entries", "profile_entries", "factor_bytes", "n_rows_total",
-                                       "max_rows", "n_reduced", "max_probe_residual", "apply_mode")},
+                                       "max_rows", "n_reduced", "n_dropped", "max_probe_residual", "apply_mode")},
             "pc_stored_over_profile": pcs["factor_entries"] / pcs["profile_entries"],
             "pc_stored_over_oracle_lu": oracle_lu_ratio(WORKLOAD, pcs["factor_entries"]),
             "kernel_ms": {"pc_apply_avg": 1e3 * avg_pc, "op_apply_avg": 1e3 * op_s / max(op_n, 1)},
