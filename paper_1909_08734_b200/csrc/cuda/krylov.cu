@@ -874,11 +874,7 @@ static void ensure_cycle_graph(cpddg_op* op, cpddg_pc* pc, Workspace& ws, int cy
             z = kc.tmp.get();
         }
         if (prof) k_stamp<<<1, 32, 0, cs>>>(gb, stamps, 1);
-        static const bool graph_pdl = [] {
-            const char* e = std::getenv("CPDDG_GRAPH_PDL");  // programmatic edges inside the captured body
-            return e && std::atoi(e) != 0;
-        }();
-        op_apply(op, z, kc.w.get(), cs, graph_pdl);
+        op_apply(op, z, kc.w.get(), cs, false);
         if (prof) k_stamp<<<1, 32, 0, cs>>>(gb, stamps, 2);
         ws.mgs_all_dev(cycle, kc.w.get(), hd, mdev, kc.vin.get());
         k_givens<<<1, 32, 0, cs>>>(gb, cap, hd, cond);

@@ -442,11 +442,6 @@ __global__ void __launch_bounds__(kGrpThreads, 4) k_extend_union(int nchunks, in
     };
     int c = blockIdx.x;
     load_meta(c);
-#if __CUDA_ARCH__ >= 900
-    // launched as a programmatic dependent (CPDDG_OP_PDL): the tables above are
-    // constant, x and v belong to the preceding kernels
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-#endif
     issue_stage(0);
     double2 tc[3] = {tt[0], tt[1], tt[2]};
     uint4 rc[2] = {ro[0], ro[1]};
@@ -533,9 +528,6 @@ __global__ void __launch_bounds__(256) k_helm_pdl(int na, double cg, double ih2,
                                                   const double* __restrict__ v, const double* __restrict__ x,
                                                   double* __restrict__ y) {
     const int i = blockIdx.x * 256 + threadIdx.x;
-#if __CUDA_ARCH__ >= 900
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // a following extension may load its tables
-#endif
     int2 nb[D];
     double xi = 0.0;
     if (i < na) {
@@ -961,25 +953,10 @@ static void launch_apply(const cpddg_op* op, const double* x, const double* b, d
     const int nb = op->na + op->ng;
     const int thr = 256;
     if (op->uni) {
-        static const bool ext_pdl = [] {
-            const char* e = std::getenv("CPDDG_OP_PDL");  // extension as a programmatic dependent of its predecessor
-            return e && std::atoi(e) != 0;
-        }();
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(op->grp_grid);
-        cfg.blockDim = dim3(kGrpThreads);
-        cfg.stream = st;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[0].val.programmaticStreamSerializationAllowed = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = (pdl && ext_pdl) ? 1 : 0;
-        CPDDG_CUDA(cudaLaunchKernelEx(&cfg, k_extend_union, op->grp_chunks, op->grp_slots,
-                                      static_cast<const double*>(op->grp_t.get()),
-                                      static_cast<const unsigned char*>(op->grp_slot.get()),
-                                      static_cast<const int*>(op->grp_perm.get()),
-                                      static_cast<const int*>(op->uni_stage.get()),
-                                      static_cast<const unsigned short*>(op->uni_roff.get()), x, op->v.get()));
+        k_extend_union<<<op->grp_grid, kGrpThreads, 0, st>>>(op->grp_chunks, op->grp_slots, op->grp_t.get(),
+                                                            op->grp_slot.get(), op->grp_perm.get(),
+                                                            op->uni_stage.get(), op->uni_roff.get(), x,
+                                                            op->v.get());
     } else if (op->grp_chunks) {
         k_extend_grouped<<<op->grp_grid, kGrpThreads, 0, st>>>(op->grp_chunks, op->grp_slots, op->grp_t.get(),
                                                                   op->grp_slot.get(), op->grp_perm.get(),

@@ -2917,9 +2917,6 @@ __global__ void k_win_gather(std::int64_t rows, const int* __restrict__ gidx, co
 /** z[sidx[p]] (+)= ybuf[p] over the owned rows (Rt_j^T; disjoint writes). */
 __global__ void k_win_scatter(std::int64_t rows, const int* __restrict__ sidx, const double* __restrict__ ybuf,
                               double* __restrict__ z, int accumulate) {
-#if __CUDA_ARCH__ >= 900
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the operator's extension may load its tables
-#endif
     for (std::int64_t p = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; p < rows;
          p += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
         const int s = sidx[p];
