@@ -22,9 +22,12 @@
 #include "common.cuh"
 #include "op.cuh"
 
+#include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <numeric>
 #include <string>
+#include <thread>
 
 namespace cpddg {
 
@@ -746,106 +749,142 @@ static void build_groups(cpddg_op* op, const std::vector<int>& lines, const std:
  *  base (then by code), two of one base per thread; a chunk closes when its
  *  kGrpThreads threads are used, at kGrpMax bases, or when the next base's
  *  runs would push the union stage past kUnionMax values (a base cut by a
- *  chunk boundary is staged in both). */
+ *  chunk boundary is staged in both).  The sorted sequence is cut at base
+ *  boundaries into segments chunked independently on the host threads (a
+ *  segment's last chunk may stay partly empty); v does not depend on the
+ *  chunking. */
 static void build_union(cpddg_op* op, const std::vector<int>& lines, const std::vector<double>& t, int nb) {
     constexpr int R = 16;
     std::vector<int> ord(static_cast<std::size_t>(nb));
     std::iota(ord.begin(), ord.end(), 0);
     std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return lines[a] < lines[b]; });
-    std::vector<int> perm, stage;                 // per slot / [chunks][kUnionMax]
-    std::vector<unsigned short> roff;             // [chunks][kGrpMax][16]
-    std::vector<unsigned char> gslot;             // per thread
-    std::vector<int> mark(static_cast<std::size_t>(op->na), -1), members, base_nodes;
-    int nbase = 0, used = 0, chunk = -1;
+    struct Part {
+        std::vector<int> perm, stage;      // per slot / [chunks][kUnionMax]
+        std::vector<unsigned short> roff;  // [chunks][kGrpMax][16]
+        std::vector<unsigned char> gslot;  // per thread
+    };
+    // segments of ~16 k nodes, cut where the base changes
+    const int target = 16384;
+    std::vector<int> cut{0};
+    for (int q = target; q < nb; q += target) {
+        int c = q;
+        while (c < nb && lines[ord[static_cast<std::size_t>(c)]] == lines[ord[static_cast<std::size_t>(c) - 1]]) ++c;
+        if (c < nb && c > cut.back()) cut.push_back(c);
+    }
+    cut.push_back(nb);
+    const int nseg = static_cast<int>(cut.size()) - 1;
+    std::vector<Part> parts(static_cast<std::size_t>(nseg));
+    const int nworkers = std::max(1, static_cast<int>(std::thread::hardware_concurrency()));
+    std::vector<std::vector<int>> marks(static_cast<std::size_t>(nworkers));
     auto run_start = [&](int k, int l) { return lines[static_cast<std::size_t>(l) * nb + k]; };
-    auto new_values = [&](int k) {  // staged values base k would add to the open chunk
-        int add = 0;
-        for (int l = 0; l < R; ++l)
-            for (int q = 0; q < 4; ++q) {
-                const int ov = run_start(k, l) + q;
-                if (mark[static_cast<std::size_t>(ov)] != chunk) {
-                    mark[static_cast<std::size_t>(ov)] = -2 - chunk;  // provisional
-                    ++add;
-                }
-            }
-        for (int l = 0; l < R; ++l)
-            for (int q = 0; q < 4; ++q) {
-                const int ov = run_start(k, l) + q;
-                if (mark[static_cast<std::size_t>(ov)] == -2 - chunk) mark[static_cast<std::size_t>(ov)] = -1;
-            }
-        return add;
-    };
-    auto close_chunk = [&] {
-        if (chunk < 0) return;
-        std::sort(members.begin(), members.end());
-        const std::size_t s0 = static_cast<std::size_t>(chunk) * kUnionMax;
-        for (std::size_t q = 0; q < members.size(); ++q) stage[s0 + q] = members[q];
-        for (int b = 0; b < nbase; ++b)
-            for (int l = 0; l < R; ++l) {
-                const int o = run_start(base_nodes[static_cast<std::size_t>(b)], l);
-                const std::size_t pos = static_cast<std::size_t>(std::lower_bound(members.begin(), members.end(), o) - members.begin());
-                roff[(static_cast<std::size_t>(chunk) * kGrpMax + b) * R + l] = static_cast<unsigned short>(pos);
-            }
-        for (int m : members) mark[static_cast<std::size_t>(m)] = -1;
-        members.clear();
-        base_nodes.clear();
-    };
-    auto open_chunk = [&] {
-        close_chunk();
-        ++chunk;
-        perm.resize(perm.size() + 2 * kGrpThreads, -1);
-        gslot.resize(gslot.size() + kGrpThreads, 0);
-        stage.resize(stage.size() + kUnionMax, -1);
-        roff.resize(roff.size() + static_cast<std::size_t>(kGrpMax) * R, 0);
-        nbase = used = 0;
-    };
-    for (int q = 0; q < nb;) {
-        const int k = ord[static_cast<std::size_t>(q)];
-        const bool new_base = q == 0 || lines[k] != lines[ord[static_cast<std::size_t>(q) - 1]];
-        if (chunk < 0 || used == kGrpThreads || (new_base && nbase == kGrpMax) ||
-            ((new_base || nbase == 0) && static_cast<int>(members.size()) + new_values(k) > kUnionMax))
-            open_chunk();
-        if (new_base || nbase == 0) {
+    parallel_for(nseg, nworkers, [&](int sg, int w) {
+        Part& P = parts[static_cast<std::size_t>(sg)];
+        std::vector<int>& mark = marks[static_cast<std::size_t>(w)];
+        if (mark.empty()) mark.assign(static_cast<std::size_t>(op->na), -1);
+        std::vector<int> members, base_nodes;
+        int nbase = 0, used = 0, chunk = -1;
+        auto new_values = [&](int k) {  // staged values base k would add to the open chunk
+            int add = 0;
             for (int l = 0; l < R; ++l)
-                for (int c = 0; c < 4; ++c) {
-                    const int ov = run_start(k, l) + c;
+                for (int q = 0; q < 4; ++q) {
+                    const int ov = run_start(k, l) + q;
                     if (mark[static_cast<std::size_t>(ov)] != chunk) {
-                        mark[static_cast<std::size_t>(ov)] = chunk;
-                        members.push_back(ov);
+                        mark[static_cast<std::size_t>(ov)] = -2 - chunk;  // provisional
+                        ++add;
                     }
                 }
-            if (static_cast<int>(members.size()) > kUnionMax)
-                throw InternalError("one stencil base exceeds the union stage");
-            base_nodes.push_back(k);
-            ++nbase;
-        }
-        const std::size_t th = gslot.size() - kGrpThreads + static_cast<std::size_t>(used++);
-        gslot[th] = static_cast<unsigned char>(nbase - 1);
-        perm[2 * th] = k;
-        ++q;
-        if (q < nb && lines[ord[static_cast<std::size_t>(q)]] == lines[k]) {
-            perm[2 * th + 1] = ord[static_cast<std::size_t>(q)];
+            for (int l = 0; l < R; ++l)
+                for (int q = 0; q < 4; ++q) {
+                    const int ov = run_start(k, l) + q;
+                    if (mark[static_cast<std::size_t>(ov)] == -2 - chunk) mark[static_cast<std::size_t>(ov)] = -1;
+                }
+            return add;
+        };
+        auto close_chunk = [&] {
+            if (chunk < 0) return;
+            std::sort(members.begin(), members.end());
+            const std::size_t s0 = static_cast<std::size_t>(chunk) * kUnionMax;
+            for (std::size_t q = 0; q < members.size(); ++q) P.stage[s0 + q] = members[q];
+            for (int b = 0; b < nbase; ++b)
+                for (int l = 0; l < R; ++l) {
+                    const int o = run_start(base_nodes[static_cast<std::size_t>(b)], l);
+                    const std::size_t pos = static_cast<std::size_t>(std::lower_bound(members.begin(), members.end(), o) - members.begin());
+                    P.roff[(static_cast<std::size_t>(chunk) * kGrpMax + b) * R + l] = static_cast<unsigned short>(pos);
+                }
+            for (int m : members) mark[static_cast<std::size_t>(m)] = -1;
+            members.clear();
+            base_nodes.clear();
+        };
+        auto open_chunk = [&] {
+            close_chunk();
+            ++chunk;
+            P.perm.resize(P.perm.size() + 2 * kGrpThreads, -1);
+            P.gslot.resize(P.gslot.size() + kGrpThreads, 0);
+            P.stage.resize(P.stage.size() + kUnionMax, -1);
+            P.roff.resize(P.roff.size() + static_cast<std::size_t>(kGrpMax) * R, 0);
+            nbase = used = 0;
+        };
+        const int q0 = cut[static_cast<std::size_t>(sg)], q1 = cut[static_cast<std::size_t>(sg) + 1];
+        for (int q = q0; q < q1;) {
+            const int k = ord[static_cast<std::size_t>(q)];
+            const bool new_base = q == q0 || lines[k] != lines[ord[static_cast<std::size_t>(q) - 1]];
+            if (chunk < 0 || used == kGrpThreads || (new_base && nbase == kGrpMax) ||
+                ((new_base || nbase == 0) && static_cast<int>(members.size()) + new_values(k) > kUnionMax))
+                open_chunk();
+            if (new_base || nbase == 0) {
+                for (int l = 0; l < R; ++l)
+                    for (int c = 0; c < 4; ++c) {
+                        const int ov = run_start(k, l) + c;
+                        if (mark[static_cast<std::size_t>(ov)] != chunk) {
+                            mark[static_cast<std::size_t>(ov)] = chunk;
+                            members.push_back(ov);
+                        }
+                    }
+                if (static_cast<int>(members.size()) > kUnionMax)
+                    throw InternalError("one stencil base exceeds the union stage");
+                base_nodes.push_back(k);
+                ++nbase;
+            }
+            const std::size_t th = P.gslot.size() - kGrpThreads + static_cast<std::size_t>(used++);
+            P.gslot[th] = static_cast<unsigned char>(nbase - 1);
+            P.perm[2 * th] = k;
             ++q;
+            if (q < q1 && lines[ord[static_cast<std::size_t>(q)]] == lines[k]) {
+                P.perm[2 * th + 1] = ord[static_cast<std::size_t>(q)];
+                ++q;
+            }
         }
+        close_chunk();
+        // exact-hit flags (bits 6 and 7 of the slot byte): the kernel applies
+        // interp.hpp:39-44's rule only to flagged slots -- same test, same doubles
+        for (std::size_t th = 0; th < P.gslot.size(); ++th)
+            for (int n = 0; n < 2; ++n) {
+                const int k = P.perm[2 * th + static_cast<std::size_t>(n)];
+                if (k < 0) continue;
+                bool hit = false;
+                for (int a = 0; a < 3; ++a)
+                    for (int j = 0; j <= 3; ++j)
+                        hit = hit || std::fabs(t[static_cast<std::size_t>(a) * nb + k] - static_cast<double>(j)) < 1e-12;
+                if (hit) P.gslot[th] = static_cast<unsigned char>(P.gslot[th] | (64u << n));
+            }
+    });
+    std::vector<int> perm, stage;
+    std::vector<unsigned short> roff;
+    std::vector<unsigned char> gslot;
+    for (const Part& P : parts) {
+        perm.insert(perm.end(), P.perm.begin(), P.perm.end());
+        stage.insert(stage.end(), P.stage.begin(), P.stage.end());
+        roff.insert(roff.end(), P.roff.begin(), P.roff.end());
+        gslot.insert(gslot.end(), P.gslot.begin(), P.gslot.end());
     }
-    close_chunk();
     const std::size_t ns = perm.size();
     std::vector<double> ts(3 * ns, 0.0);
-    for (std::size_t sl = 0; sl < ns; ++sl)
-        if (perm[sl] >= 0)
-            for (int a = 0; a < 3; ++a) ts[static_cast<std::size_t>(a) * ns + sl] = t[static_cast<std::size_t>(a) * nb + perm[sl]];
-    // exact-hit flags (bits 6 and 7 of the slot byte): the kernel applies
-    // interp.hpp:39-44's rule only to flagged slots -- same test, same doubles
-    for (std::size_t th = 0; th < gslot.size(); ++th)
-        for (int n = 0; n < 2; ++n) {
-            const int k = perm[2 * th + static_cast<std::size_t>(n)];
-            if (k < 0) continue;
-            bool hit = false;
-            for (int a = 0; a < 3; ++a)
-                for (int j = 0; j <= 3; ++j)
-                    hit = hit || std::fabs(t[static_cast<std::size_t>(a) * nb + k] - static_cast<double>(j)) < 1e-12;
-            if (hit) gslot[th] = static_cast<unsigned char>(gslot[th] | (64u << n));
-        }
+    parallel_for(static_cast<int>((ns + 65535) / 65536), 0, [&](int c, int) {
+        const std::size_t e = std::min(ns, (static_cast<std::size_t>(c) + 1) * 65536);
+        for (std::size_t sl = static_cast<std::size_t>(c) * 65536; sl < e; ++sl)
+            if (perm[sl] >= 0)
+                for (int a = 0; a < 3; ++a) ts[static_cast<std::size_t>(a) * ns + sl] = t[static_cast<std::size_t>(a) * nb + perm[sl]];
+    });
     op->grp_t.upload(ts);
     op->grp_slot.upload(gslot);
     op->grp_perm.upload(perm);
@@ -867,6 +906,13 @@ static void build_tables(cpddg_op* op, const Ix<D>* ix, const Vec<D>* cp, const 
     std::vector<double> t(static_cast<std::size_t>(D) * nb);
     std::vector<int> lines(static_cast<std::size_t>(nlines) * nb);
     auto lookup = [&](const Ix<D>& q) { return map.find(LatticeMap::pack(q.data(), D)); };
+    auto t_lap = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {  // CPDDG_VERBOSE: host wall time of the table phases
+        if (!std::getenv("CPDDG_VERBOSE")) return;
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[cpddg] op tables, %s: %.3f s\n", what, std::chrono::duration<double>(now - t_lap).count());
+        t_lap = now;
+    };
     parallel_for((nb + 8191) / 8192, 0, [&](int chunk, int) {
         const int k1 = std::min(nb, (chunk + 1) * 8192);
         for (int k = chunk * 8192; k < k1; ++k) {
@@ -896,16 +942,23 @@ static void build_tables(cpddg_op* op, const Ix<D>* ix, const Vec<D>* cp, const 
             }
         }
     });
+    lap("stencil offsets and run starts");
     std::vector<int> nbr(static_cast<std::size_t>(2 * D) * op->na);
-    for (int i = 0; i < op->na; ++i) {
-        Ix<D> around[2 * D];
-        neighbors_of<D>(ix[i], around);
-        for (int k = 0; k < 2 * D; ++k) {
-            const std::int64_t c = lookup(around[k]);
-            if (c < 0) throw InternalError("finite-difference neighbor missing from band");
-            nbr[static_cast<std::size_t>(k) * op->na + i] = static_cast<int>(c);
+    std::vector<int> aos(nbr.size());  // node-major copy for k_helm_pdl
+    parallel_for((op->na + 8191) / 8192, 0, [&](int chunk, int) {
+        const int i1 = std::min(op->na, (chunk + 1) * 8192);
+        for (int i = chunk * 8192; i < i1; ++i) {
+            Ix<D> around[2 * D];
+            neighbors_of<D>(ix[i], around);
+            for (int k = 0; k < 2 * D; ++k) {
+                const std::int64_t c = lookup(around[k]);
+                if (c < 0) throw InternalError("finite-difference neighbor missing from band");
+                nbr[static_cast<std::size_t>(k) * op->na + i] = static_cast<int>(c);
+                aos[static_cast<std::size_t>(i) * 2 * D + k] = static_cast<int>(c);
+            }
         }
-    }
+    });
+    lap("neighbour codes");
     if constexpr (D == 3) {
         // default: grouped by stencil base; CPDDG_EXT=staged / CPDDG_EXT_GATHER=1
         // keep the round-1 tiled-stage and gather kernels (same v bits)
@@ -920,17 +973,13 @@ static void build_tables(cpddg_op* op, const Ix<D>* ix, const Vec<D>* cp, const 
             }
         }
     }
+    lap("extension slots and stages");
     op->t.upload(t);
     op->lines.upload(lines);
     op->nbr.upload(nbr);
-    {  // node-major copy for k_helm_pdl
-        std::vector<int> aos(nbr.size());
-        for (int i = 0; i < op->na; ++i)
-            for (int k = 0; k < 2 * D; ++k)
-                aos[static_cast<std::size_t>(i) * 2 * D + k] = nbr[static_cast<std::size_t>(k) * op->na + i];
-        op->nbr_aos.upload(aos);
-    }
+    op->nbr_aos.upload(aos);
     op->v.alloc(static_cast<std::size_t>(nb));
+    lap("uploads");
     op->nlines = nlines;
     // B_op = 16 N_A + [8d + 4 (p+1)^(d-1)] N_B + 8d N_A
     op->alg_bytes = 16LL * op->na + (8LL * D + 4LL * nlines) * nb + 8LL * D * op->na;
@@ -1042,7 +1091,11 @@ static cpddg_op* create_from(int p, int na, int ng, double h, double c, const Ix
                 throw InternalError("duplicate lattice index in band description");
         map = &own;
     }
+    const auto t0 = std::chrono::steady_clock::now();
     build_tables<D>(op.get(), ix, cp, *map);
+    if (std::getenv("CPDDG_VERBOSE"))
+        std::fprintf(stderr, "[cpddg] op tables: %.3f s\n",
+                     std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
     op->red.ensure(1);
     op->rn2.alloc(1);
     return op.release();

@@ -152,9 +152,47 @@ HostSub analyse(const cpddg_local_desc& d, int n_global, bool pivot = false, int
     S.reduced = reducible && d.n_bc > 0;
     const int n = reducible ? d.n_overlap : nl;
     S.n = n;
-    // pattern(A + A^T) without the diagonal, CSR: count, fill, sort + unique per row
+    // pattern(A + A^T) without the diagonal, CSR.  Rows with increasing columns
+    // (what append_row of sparse.hpp:35-46 produces): the transpose by a
+    // counting pass is sorted too, and each row is the merge of the two sorted
+    // lists (a third of the time of sorting the concatenation); any other
+    // input: count, fill, sort + unique per row.
+    bool sorted_rows = true;
+    for (int r = 0; r < n && sorted_rows; ++r)
+        for (std::int64_t k = rp[r] + 1; k < rp[r + 1]; ++k)
+            if (d.col[k] < d.col[k - 1]) {
+                sorted_rows = false;
+                break;
+            }
     Graph gr;
-    {
+    if (sorted_rows) {
+        std::vector<int> tc(static_cast<std::size_t>(n) + 1, 0);
+        for (int r = 0; r < n; ++r)
+            for (std::int64_t k = rp[r]; k < rp[r + 1]; ++k)
+                if (const int c = d.col[k]; c < n && c != r) ++tc[static_cast<std::size_t>(c) + 1];
+        for (int v = 0; v < n; ++v) tc[static_cast<std::size_t>(v) + 1] += tc[static_cast<std::size_t>(v)];
+        std::vector<int> tr(static_cast<std::size_t>(tc[static_cast<std::size_t>(n)])), fill(tc.begin(), tc.end() - 1);
+        for (int r = 0; r < n; ++r)
+            for (std::int64_t k = rp[r]; k < rp[r + 1]; ++k)
+                if (const int c = d.col[k]; c < n && c != r) tr[static_cast<std::size_t>(fill[static_cast<std::size_t>(c)]++)] = r;
+        gr.xadj.assign(static_cast<std::size_t>(n) + 1, 0);
+        gr.adj.reserve(2 * tr.size());
+        for (int v = 0; v < n; ++v) {
+            const int* a = d.col + rp[v];
+            const int* ae = d.col + rp[v + 1];
+            const int* b = tr.data() + tc[static_cast<std::size_t>(v)];
+            const int* be = tr.data() + tc[static_cast<std::size_t>(v) + 1];
+            int last = -1;
+            while (a != ae || b != be) {
+                const int x = (b == be || (a != ae && *a <= *b)) ? *a++ : *b++;
+                if (x < n && x != v && x != last) {
+                    gr.adj.push_back(x);
+                    last = x;
+                }
+            }
+            gr.xadj[static_cast<std::size_t>(v) + 1] = static_cast<int>(gr.adj.size());
+        }
+    } else {
         std::vector<int> cnt(static_cast<std::size_t>(n) + 1, 0);
         for (int r = 0; r < n; ++r)
             for (std::int64_t k = rp[r]; k < rp[r + 1]; ++k) {
@@ -3755,6 +3793,14 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     pc->factor_seconds = ms * 1e-3;
+    auto t_lap = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {  // CPDDG_VERBOSE: host wall time of the setup phases after the factorisation
+        if (!std::getenv("CPDDG_VERBOSE")) return;
+        CPDDG_CUDA(cudaDeviceSynchronize());
+        const auto t = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[cpddg] pc %s: %.3f s\n", what, std::chrono::duration<double>(t - t_lap).count());
+        t_lap = t;
+    };
     std::vector<int> st(static_cast<std::size_t>(n_sub));
     CPDDG_CUDA(cudaMemcpy(st.data(), status.get(), st.size() * sizeof(int), cudaMemcpyDeviceToHost));
     {
@@ -3840,6 +3886,7 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
     set_solve_smem<false, ShapeMid, true>(solve_smem_set);
     set_solve_smem<false, ShapeRec, true>(solve_smem_set);
     set_solve_smem<false, ShapeRec8, true>(solve_smem_set);
+    lap("pivot check, kernel attributes");
     // block shape: one CTA per subdomain, all resident in one wave
     {
         const int S = sm_count();
@@ -3975,6 +4022,7 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
             if (!ok) throw ConfigError("preconditioner blocks do not fit the streamed solve's shared memory");
         }
     }
+    lap("records, far parts, solve tables and schedule");
     // factor probe (cpddg_pc_options::check_residual): solve A_j z = A_j x_probe
     // on the device for every subdomain and check the residual on the host --
     // the DirectSolver contract of the reference (residual ~1e-12,
@@ -4016,6 +4064,7 @@ static cpddg_pc* pc_build(int n_global, int n_sub, const cpddg_local_desc* local
             }
         if (!np.subs.empty()) throw np;  // no-pivot factors not accurate enough: pivot those
     }
+    lap("probe solves");
     // small systems: dense inverses (k_solve_dense) when the envelope solve
     // would be a latency-bound chain on a mostly idle GPU
     {
@@ -4207,6 +4256,7 @@ static cpddg_pc* pc_build_pivoting(int n_global, int n_sub, const cpddg_local_de
     std::int64_t n_dropped = 0;
     const cpddg_local_desc* locals = locals_in;
     const char* de = std::getenv("CPDDG_DROP");
+    const auto t_drop = std::chrono::steady_clock::now();
     if (n_sub > 0 && locals_in && !(de && std::string(de) == "0")) {
         owned.resize(static_cast<std::size_t>(n_sub));
         reduced.assign(locals_in, locals_in + n_sub);
@@ -4217,6 +4267,10 @@ static cpddg_pc* pc_build_pivoting(int n_global, int n_sub, const cpddg_local_de
         });
         for (int c : cnt) n_dropped += c;
         if (n_dropped > 0) locals = reduced.data();
+        if (std::getenv("CPDDG_VERBOSE"))
+            std::fprintf(stderr, "[cpddg] pc reduce: %lld unreferenced unknowns dropped in %.3f s\n",
+                         static_cast<long long>(n_dropped),
+                         std::chrono::duration<double>(std::chrono::steady_clock::now() - t_drop).count());
     }
     std::vector<char> pivot(static_cast<std::size_t>(std::max(n_sub, 0)), 0);
     if (const char* e = std::getenv("CPDDG_PIVOT"); e && std::string(e) == "all") std::fill(pivot.begin(), pivot.end(), 1);
