@@ -196,6 +196,11 @@ typedef struct {
 CPDDG_API int cpddg_pc_create(int n_global, int n_sub, const cpddg_local_desc* locals,
                     const cpddg_pc_options* opt, cpddg_pc** out);
 CPDDG_API int cpddg_pc_create_from_setup(const cpddg_setup* s, const cpddg_pc_options* opt, cpddg_pc** out);
+/** Host only (no device call): dropped[q] = 1 for the local unknowns cpddg_pc_create removes before
+ *  the factorisation -- closure unknowns that no row but their own refers to and that no scatter
+ *  returns (transmission.hpp:84-92, :66-69), to the fixed point; dropped has n_overlap + n_bc
+ *  entries.  The remaining unknowns' solution is unchanged. */
+CPDDG_API int cpddg_local_unreferenced(const cpddg_local_desc* d, unsigned char* dropped, int* n_dropped);
 /** z_dev = M r_dev (sizes n_global). */
 CPDDG_API int cpddg_pc_apply(cpddg_pc* pc, const double* r_dev, double* z_dev, void* stream);
 CPDDG_API int cpddg_pc_stats_get(const cpddg_pc* pc, cpddg_pc_stats* st);

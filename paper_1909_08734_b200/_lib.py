@@ -96,6 +96,7 @@ _SIGS = {
     "cpddg_pc_create": (C.c_int, [C.c_int, C.c_int, C.POINTER(cpddg_local_desc),
                                   C.POINTER(cpddg_pc_options), C.POINTER(_vp)]),
     "cpddg_pc_create_from_setup": (C.c_int, [_vp, C.POINTER(cpddg_pc_options), C.POINTER(_vp)]),
+    "cpddg_local_unreferenced": (C.c_int, [C.POINTER(cpddg_local_desc), C.POINTER(C.c_ubyte), C.POINTER(C.c_int)]),
     "cpddg_pc_apply": (C.c_int, [_vp, _vp, _vp, _vp]),
     "cpddg_pc_stats_get": (C.c_int, [_vp, C.POINTER(cpddg_pc_stats)]),
     "cpddg_pc_destroy": (C.c_int, [_vp]),

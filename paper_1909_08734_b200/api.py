@@ -239,6 +239,33 @@ class DeviceHelmholtz:
 
 # ---------------------------------------------------------------- preconditioner
 
+def _local_desc(L: dict):
+    """cpddg_local_desc over a LocalOperator-shaped dict (the arrays are returned to keep them alive)."""
+    arrs = [np.ascontiguousarray(L["overlap"], np.int32),
+            np.ascontiguousarray(L["scatter_local"], np.int32),
+            np.ascontiguousarray(L["scatter_global"], np.int32),
+            np.ascontiguousarray(L["ptr"], np.int64),
+            np.ascontiguousarray(L["col"], np.int32),
+            np.ascontiguousarray(L["val"], np.float64)]
+    d = _lib.cpddg_local_desc(n_overlap=int(L["n_overlap"]), n_bc=int(L["n_bc"]),
+                              overlap=arrs[0].ctypes.data, n_scatter=int(arrs[1].size),
+                              scatter_local=arrs[1].ctypes.data, scatter_global=arrs[2].ctypes.data,
+                              row_ptr=arrs[3].ctypes.data, col=arrs[4].ctypes.data, val=arrs[5].ctypes.data)
+    return d, arrs
+
+
+def unreferenced_unknowns(L: dict) -> np.ndarray:
+    """Mask of the local unknowns the device preconditioner removes before the
+    factorisation (closure unknowns only their own row refers to and no scatter
+    returns; transmission.hpp:84-92, :66-69).  Host only."""
+    d, _keep = _local_desc(L)
+    out = np.zeros(int(L["n_overlap"]) + int(L["n_bc"]), np.uint8)
+    n = C.c_int()
+    check(lib().cpddg_local_unreferenced(C.byref(d), out.ctypes.data_as(C.POINTER(C.c_ubyte)), C.byref(n)))
+    assert n.value == int(out.sum())
+    return out.astype(bool)
+
+
 class SchwarzPreconditioner:
     """Device RAS / ORAS preconditioner (SchwarzPreconditioner, solve.hpp:64-86);
     the local factorisations run on the device at construction."""
@@ -262,18 +289,8 @@ class SchwarzPreconditioner:
         keep = []
         descs = (_lib.cpddg_local_desc * len(locals_))()
         for k, L in enumerate(locals_):
-            arrs = [np.ascontiguousarray(L["overlap"], np.int32),
-                    np.ascontiguousarray(L["scatter_local"], np.int32),
-                    np.ascontiguousarray(L["scatter_global"], np.int32),
-                    np.ascontiguousarray(L["ptr"], np.int64),
-                    np.ascontiguousarray(L["col"], np.int32),
-                    np.ascontiguousarray(L["val"], np.float64)]
+            descs[k], arrs = _local_desc(L)
             keep.append(arrs)
-            descs[k] = _lib.cpddg_local_desc(n_overlap=int(L["n_overlap"]), n_bc=int(L["n_bc"]),
-                                             overlap=arrs[0].ctypes.data, n_scatter=int(arrs[1].size),
-                                             scatter_local=arrs[1].ctypes.data,
-                                             scatter_global=arrs[2].ctypes.data, row_ptr=arrs[3].ctypes.data,
-                                             col=arrs[4].ctypes.data, val=arrs[5].ctypes.data)
         opt = _lib.cpddg_pc_options(workers=workers, check_residual=1)
         h = C.c_void_p()
         check(lib().cpddg_pc_create(int(n_global), len(locals_), descs, C.byref(opt), C.byref(h)))

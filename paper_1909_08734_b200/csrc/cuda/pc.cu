@@ -4162,8 +4162,11 @@ struct OwnedLocal {
     std::vector<double> val;
 };
 
-static int drop_unreferenced(const cpddg_local_desc& d, OwnedLocal& o, cpddg_local_desc& out) {
+/** gone[q] = 1 for every unknown drop_unreferenced removes; returns their count
+ *  (0 for malformed input, which analyse() reports). */
+static int mark_unreferenced(const cpddg_local_desc& d, std::vector<char>& gone) {
     const int nl = d.n_overlap + d.n_bc;
+    gone.assign(static_cast<std::size_t>(std::max(nl, 0)), 0);
     if (d.n_overlap < 0 || d.n_bc <= 0 || !d.row_ptr || !d.col || !d.val) return 0;
     const std::int64_t* rp = d.row_ptr;
     // malformed input is left for analyse() to report
@@ -4182,7 +4185,7 @@ static int drop_unreferenced(const cpddg_local_desc& d, OwnedLocal& o, cpddg_loc
             else
                 ++ref[static_cast<std::size_t>(d.col[k])];
         }
-    std::vector<char> fixed(static_cast<std::size_t>(nl), 0), gone(static_cast<std::size_t>(nl), 0);
+    std::vector<char> fixed(static_cast<std::size_t>(nl), 0);
     for (int k = 0; k < d.n_scatter; ++k) fixed[static_cast<std::size_t>(d.scatter_local[k])] = 1;
     auto free_unknown = [&](int c) {
         return c >= d.n_overlap && !fixed[static_cast<std::size_t>(c)] && !gone[static_cast<std::size_t>(c)] &&
@@ -4210,7 +4213,15 @@ static int drop_unreferenced(const cpddg_local_desc& d, OwnedLocal& o, cpddg_loc
             }
         }
     }
+    return dropped;
+}
+
+static int drop_unreferenced(const cpddg_local_desc& d, OwnedLocal& o, cpddg_local_desc& out) {
+    std::vector<char> gone;
+    const int dropped = mark_unreferenced(d, gone);
     if (dropped == 0) return 0;
+    const int nl = d.n_overlap + d.n_bc;
+    const std::int64_t* rp = d.row_ptr;
     std::vector<int> id(static_cast<std::size_t>(nl));
     int m = 0;
     std::int64_t nnz = 0;
@@ -4322,6 +4333,15 @@ int cpddg_pc_create(int n_global, int n_sub, const cpddg_local_desc* locals, con
     return guarded([&] {
         if (!out) throw InternalError("null argument");
         *out = pc_build_pivoting(n_global, n_sub, locals, opt);
+    });
+}
+
+int cpddg_local_unreferenced(const cpddg_local_desc* d, unsigned char* dropped, int* n_dropped) {
+    return guarded([&] {
+        if (!d || !dropped || !n_dropped) throw InternalError("null argument");
+        std::vector<char> gone;
+        *n_dropped = mark_unreferenced(*d, gone);
+        for (std::size_t q = 0; q < gone.size(); ++q) dropped[q] = static_cast<unsigned char>(gone[q]);
     });
 }
 
