@@ -159,6 +159,15 @@ class Problem:
                     bc_real=br[: nbc * (4 * D + 1)].reshape(nbc, 4 * D + 1),
                     fallback_count=int(cnt[5]), n_lambda=int(cnt[6]), n_cross_flagged=int(cnt[7]))
 
+    def fallback_anchors(self) -> int:
+        """Sum of Subdomain::fallback_count (pipeline.hpp:203-204)."""
+        cnt = np.zeros(8, np.int32)
+        total = 0
+        for j in range(self.n_sub):
+            check(lib().cpddg_setup_subdomain_counts(self._h, j, cnt))
+            total += int(cnt[5])
+        return total
+
     def local(self, j: int) -> dict:
         s = np.zeros(4, np.int64)
         check(lib().cpddg_setup_local_sizes(self._h, j, s))
@@ -391,14 +400,19 @@ def effective_max_iter(mode: str, max_iter: int) -> int:
     return 2000 if mode == "gmres" else 5000
 
 
-def run_solve(cfg: dict, part=None, rhs=None) -> dict:
+def run_solve(cfg: dict, part=None, rhs=None, exact=None) -> dict:
     """run_solve (pipeline.hpp:183-241) on the device path.  cfg keys follow
     RunConfig (config.hpp:19-48): surface, h, p, c, radius, major_radius,
     minor_radius, obj, method, mode, rel_tol, max_iter, gmres_restart,
-    n_overlap, n_subdomains, alpha, alpha_cross, tube_radius, workers.
+    n_overlap, n_subdomains, alpha, alpha_cross, tube_radius, workers;
+    device_setup (default True: band / closest points and alignment /
+    subdomain sets on the GPU, bit-identical to the host).
     `part` (labels) and `rhs` (host array) are required: this path consumes
     partition and right-hand-side files (partition.hpp:519-552,
-    pipeline.hpp:103-117), it does not generate them."""
+    pipeline.hpp:103-117), it does not generate them.  `exact`, a function of
+    the (n, d) closest points, fills err_inf / err_rms (problems.hpp:93-111);
+    the result carries the SolveOutputs fields (pipeline.hpp:171-180) except
+    diff_direct (check_direct is a CPU verification aid of the reference)."""
     torch = _torch()
     t = PhaseTimings()
     t0 = time.perf_counter()
@@ -406,7 +420,8 @@ def run_solve(cfg: dict, part=None, rhs=None) -> dict:
                 c=float(cfg.get("c", 1.0)), radius=float(cfg.get("radius", 1.0)),
                 major_radius=float(cfg.get("major_radius", 2.0 / 3.0)),
                 minor_radius=float(cfg.get("minor_radius", 1.0 / 3.0)), obj_path=cfg.get("obj"),
-                tube_radius=float(cfg.get("tube_radius", 0.0)), workers=int(cfg.get("workers", 0)))
+                tube_radius=float(cfg.get("tube_radius", 0.0)), workers=int(cfg.get("workers", 0)),
+                device_setup=bool(cfg.get("device_setup", True)))
     t.global_matrix = time.perf_counter() - t0
     from . import io as _io
     if part is None and cfg.get("partition_in"):
@@ -452,6 +467,13 @@ def run_solve(cfg: dict, part=None, rhs=None) -> dict:
         _io.write_solution(os.path.join(d, "solution.csv"), x, u_host)
         _io.write_iterations(os.path.join(d, "iterations.csv"), res.log.residuals)
         _io.write_timings(os.path.join(d, "timings.csv"), t, mode == "gmres")
+    err_inf = err_rms = -1.0
+    if exact is not None:
+        d = u_host - np.asarray(exact(P.active_cp), np.float64)
+        err_inf = float(np.max(np.abs(d))) if d.size else 0.0
+        err_rms = float(np.sqrt(np.sum(d * d) / max(1, d.size)))
     return dict(u=u_host, log=res.log, part=aligned, align_moves=moves,
+                fallback_anchors=P.fallback_anchors(),
                 final_relative_residual=res.log.final_true_residual / b0 if b0 > 0 else 0.0,
+                err_inf=err_inf, err_rms=err_rms,
                 problem=P, operator=A, preconditioner=M)

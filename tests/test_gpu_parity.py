@@ -396,7 +396,13 @@ def test_run_solve_pipeline_with_files(tmp_path):
                rel_tol=1e-10, max_iter=2000, n_overlap=2, n_subdomains=8, alpha=1.0,
                partition_in=str(tmp_path / "part.txt"), rhs="file:" + str(tmp_path / "rhs.txt"),
                partition_out=str(tmp_path / "aligned.txt"), output_dir=str(tmp_path))
-    out = api.run_solve(cfg)
+    out = api.run_solve(cfg, exact=lambda cp: np.sin(np.arctan2(cp[:, 1], cp[:, 0])) +
+                        np.sin(12 * np.arctan2(cp[:, 1], cp[:, 0])))
+    assert out["problem"].device_setup and 0 <= out["err_rms"] <= out["err_inf"]
+    host = api.run_solve(dict(cfg, device_setup=False, partition_out="", output_dir=""))
+    assert not host["problem"].device_setup and host["err_inf"] == -1.0
+    assert np.array_equal(out["u"], host["u"]) and np.array_equal(out["part"], host["part"])
+    assert out["fallback_anchors"] == host["fallback_anchors"] >= 0
     assert out["log"].converged and abs(out["log"].iterations - int(g["iterations"])) <= 2
     assert np.linalg.norm(out["u"] - g["u"]) <= 1e-8 * np.linalg.norm(g["u"])
     assert np.array_equal(io.read_partition(str(tmp_path / "aligned.txt"), len(g["b"])), g["part_aligned"])
