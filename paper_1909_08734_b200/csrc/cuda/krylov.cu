@@ -741,11 +741,12 @@ struct Workspace {
         const long long threads = static_cast<long long>(coop_grid) * kRedThreads;
         const int ept = static_cast<int>((n + threads - 1) / threads);
         const void* kern = reinterpret_cast<const void*>(k_mgs_all);
-        if (!streamed && ept <= 8)
+        if (!streamed && ept <= 16)
             kern = ept <= 1   ? reinterpret_cast<const void*>(k_mgs_reg<1>)
                    : ept <= 2 ? reinterpret_cast<const void*>(k_mgs_reg<2>)
                    : ept <= 4 ? reinterpret_cast<const void*>(k_mgs_reg<4>)
-                              : reinterpret_cast<const void*>(k_mgs_reg<8>);
+                   : ept <= 8 ? reinterpret_cast<const void*>(k_mgs_reg<8>)
+                              : reinterpret_cast<const void*>(k_mgs_reg<16>);
         if (kern != reinterpret_cast<const void*>(k_mgs_all)) {
             int per_sm = 0;  // the whole grid must be resident
             CPDDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRedThreads, 0));
