@@ -174,3 +174,51 @@ def test_unreferenced_closure_unknowns_are_dropped(monkeypatch):
     want = np.linalg.solve(B, np.concatenate([rhs, np.zeros(2)]))[:5]
     got = Mc.apply(torch.from_numpy(rhs).cuda()).cpu().numpy()
     assert np.linalg.norm(got - want) <= 1e-13 * np.linalg.norm(want)
+
+
+def test_unsorted_rows_and_duplicate_entries():
+    """cpddg_pc_create accepts any CSR a LocalOperator could hold: columns in any
+    order within a row and duplicate (row, column) entries, which are summed
+    (SparseOperator rows are sorted and merged, sparse.hpp:35-46, but the ABI
+    does not rely on it).  The pattern analysis takes its general path, the
+    reduction still finds the unknown nothing depends on, and the solve equals
+    the dense solve."""
+    import scipy.sparse as sp
+    import torch
+
+    from paper_1909_08734_b200 import api
+    rng = np.random.default_rng(11)
+    n_ov, n_bc = 300, 3
+    n = n_ov + n_bc
+    B = sp.random(n, n, density=0.03, random_state=3, format="lil")
+    B.setdiag(8.0 + rng.uniform(0, 1, n))
+    B = B.toarray()
+    B[:, n - 1] = 0.0          # the last closure unknown: only its own row refers to it
+    B[n - 1, n - 1] = 3.0
+    B[n - 1, :5] = rng.uniform(-1, 1, 5)
+    B[n_ov, n_ov + 1] = 0.25   # the other two closure unknowns stay (referenced from overlap rows)
+    B[3, n_ov] = -0.5
+    B[7, n_ov + 1] = 0.75
+    ptr, col, val = [0], [], []
+    for r in range(n):
+        cs = np.flatnonzero(B[r])
+        cs = cs[rng.permutation(cs.size)]            # unsorted
+        for c in cs:
+            if rng.uniform() < 0.3:                   # a duplicate entry: two halves
+                col += [c, c]
+                val += [0.5 * B[r, c], 0.5 * B[r, c]]
+            else:
+                col.append(c)
+                val.append(B[r, c])
+        ptr.append(len(col))
+    idx = np.arange(n_ov, dtype=np.int32)
+    loc = dict(n_overlap=n_ov, n_bc=n_bc, overlap=idx, scatter_local=idx, scatter_global=idx,
+               ptr=np.asarray(ptr, np.int64), col=np.asarray(col, np.int32), val=np.asarray(val, np.float64))
+    mask = api.unreferenced_unknowns(loc)
+    assert mask.sum() == 1 and mask[n - 1]
+    M = api.SchwarzPreconditioner.from_locals(n_ov, [loc])
+    assert M.stats()["n_dropped"] == 1 and M.stats()["n_rows_total"] == n - 1
+    rhs = rng.uniform(-1, 1, n_ov)
+    want = np.linalg.solve(B, np.concatenate([rhs, np.zeros(n_bc)]))[:n_ov]
+    got = M.apply(torch.from_numpy(rhs).cuda()).cpu().numpy()
+    assert np.linalg.norm(got - want) <= 1e-12 * np.linalg.norm(want)
