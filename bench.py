@@ -337,6 +337,10 @@ def main():
     ap.add_argument("--ref-iters", type=int, default=0,
                     help="GMRES iterations per reference sample step (default: ~5 s of host work)")
     ap.add_argument("--cpu-baseline", default="auto", choices=["auto", "off"])
+    ap.add_argument("--host-loop", action="store_true",
+                    help="timed solves in the host-driven Arnoldi loop with CUDA events per launch (what ncu can "
+                         "list kernel by kernel: it does not see inside the while-conditional graph nodes of the "
+                         "default device-driven cycles)")
     ap.add_argument("--config", default="headline", choices=sorted(CONFIGS),
                     help="workload (default: BASELINE's headline; the others are parity / scaling cases)")
     args = ap.parse_args()
@@ -394,7 +398,8 @@ def main():
     # cycle) with device timestamps around the preconditioner and the operator in the graph body
     # (CPDDG_GMRES_GRAPH=1 keeps the graph when per-launch timing is asked for); the warm-up uses
     # the same graph, so nothing is captured inside the timed region
-    os.environ["CPDDG_GMRES_GRAPH"] = "1"
+    if not args.host_loop:
+        os.environ["CPDDG_GMRES_GRAPH"] = "1"
     for _ in range(args.warmup):
         api.gmres_solve(A, b, M, tol, mi, rs, profile=True)
     torch.cuda.synchronize()
@@ -485,7 +490,9 @@ def main():
             "pc_stored_over_profile": pcs["factor_entries"] / pcs["profile_entries"],
             "pc_stored_over_oracle_lu": oracle_lu_ratio(WORKLOAD, pcs["factor_entries"]),
             "kernel_ms": {"pc_apply_avg": 1e3 * avg_pc, "op_apply_avg": 1e3 * op_s / max(op_n, 1),
-                          "timing": "device timestamps (%globaltimer, one-thread kernels on the launching stream) "
+                          "timing": "CUDA events around each launch in the host-driven loop (--host-loop)"
+                                    if args.host_loop else
+                                    "device timestamps (%globaltimer, one-thread kernels on the launching stream) "
                                     "around each preconditioner apply (gather + k_solve + scatter) and operator "
                                     "apply inside the CUDA-graph loop body of the timed solves"},
             "kernel_ms_cuda_events": dict(events_ms, timing="CUDA events around the same launches in one extra "

@@ -12,12 +12,14 @@ mkdir -p $OUT
 timeout 900 python bench.py --steps 5 --warmup 3 > $OUT/${TAG}_bench.json 2> $OUT/${TAG}_bench.err
 echo "bench rc=$?"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file $OUT/${TAG}_launches.csv \
-    python bench.py --steps 1 --warmup 3 --cpu-baseline off > $OUT/${TAG}_ncu_bench.log 2>&1
+    python bench.py --steps 1 --warmup 3 --cpu-baseline off --host-loop > $OUT/${TAG}_ncu_bench.log 2>&1
 echo "launch list rc=$?"
-# the timed region only (bench.py's NVTX range "timed": one complete solve)
+# the timed region only (bench.py's NVTX range "timed": one complete solve).  --host-loop: the same
+# kernels launched one by one from the host; ncu does not list the kernels inside the
+# while-conditional graph nodes of the default device-driven cycles
 timeout 900 ncu --nvtx --nvtx-include "timed/" --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \
     --log-file $OUT/${TAG}_launches_step.csv \
-    python bench.py --steps 1 --warmup 3 --cpu-baseline off > $OUT/${TAG}_ncu_bench_step.log 2>&1
+    python bench.py --steps 1 --warmup 3 --cpu-baseline off --host-loop > $OUT/${TAG}_ncu_bench_step.log 2>&1
 echo "step launch list rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_solve_win -s 2 -c 1 \
     -o $OUT/${TAG}_k_solve_win -f python scripts/profile_pc_mode.py 0 > $OUT/${TAG}_ncu_pc.log 2>&1
