@@ -408,7 +408,10 @@ def main():
     # each nvidia-smi query stalls the CUDA driver for milliseconds: harmless
     # for the 0.3 s headline solves, but it would dominate the millisecond
     # configurations, which are sampled once a second instead (over >= 1 s)
-    clocks = ClockSampler(local_rank, 200 if args.config not in ("circle", "sphere05") else 1000)
+    clock_ms = 200 if args.config not in ("circle", "sphere05") else 1000
+    if os.environ.get("CPDDG_BENCH_CLOCK_MS"):  # experiment knob: sampling interval of the clocks line
+        clock_ms = int(os.environ["CPDDG_BENCH_CLOCK_MS"])
+    clocks = ClockSampler(local_rank, clock_ms)
     clocks.start()
     barrier()
     torch.cuda.synchronize()
