@@ -245,6 +245,182 @@ __global__ void __launch_bounds__(kRedThreads) k_mgs_reg(int n, int m, const dou
     }
 }
 
+/** Three block sums behind one pair of barriers (results valid in thread 0). */
+template <int NT>
+__device__ __forceinline__ void block_sum3(double& a, double& b, double& c, double* sh /* [3 NT / 32] */) {
+    a = warp_sum(a);
+    b = warp_sum(b);
+    c = warp_sum(c);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) {
+        sh[w] = a;
+        sh[NT / 32 + w] = b;
+        sh[2 * (NT / 32) + w] = c;
+    }
+    __syncthreads();
+    if (w == 0) {
+        a = warp_sum(l < NT / 32 ? sh[l] : 0.0);
+        b = warp_sum(l < NT / 32 ? sh[NT / 32 + l] : 0.0);
+        c = warp_sum(l < NT / 32 ? sh[2 * (NT / 32) + l] : 0.0);
+    }
+    __syncthreads();
+}
+
+/** k_mgs_reg with TWO projections per grid barrier.  A pass loads the basis
+ *  vectors V_a, V_b (a = 2 pass, b = a + 1) and reduces
+ *      d1 = V_a . w,   d2 = V_b . w,   c = V_b . V_a
+ *  together; then h_a = d1 and h_b = d2 - h_a c, which IS the modified
+ *  Gram-Schmidt coefficient V_b . (w - h_a V_a) with the subtraction moved
+ *  across the dot product (exact algebra; c is the basis' own loss of
+ *  orthogonality, ~1e-16).  w is then updated as MGS does, one vector after
+ *  the other.  Half the grid barriers of k_mgs_reg (the barriers, not the
+ *  bytes, are what an MGS step costs: ~3.4 us each, j + 2 of them at step j);
+ *  coefficients agree with k_mgs_reg to rounding (tests/test_gpu_parity.py).
+ *  Pass 0 also reduces ||w||^2; the last pass reduces ||w||^2 of the
+ *  orthogonalised w.  Same index mapping and fixed summation orders: bitwise
+ *  reproducible run to run. */
+template <int EPT>
+__global__ void __launch_bounds__(kRedThreads, 2) k_mgs_pair(int n, int m, const double* const* __restrict__ V,
+                                                          double* __restrict__ w, double* __restrict__ vnext,
+                                                          double* partials, double* hout, double* wn0,
+                                                          const int* __restrict__ mdev, double* __restrict__ vin) {
+    if (mdev) {
+        m = *mdev;
+        vnext = const_cast<double*>(V[m + 1]);
+        wn0 = hout + m + 2;
+    }
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double sh[3 * (kRedThreads / 32)];
+    __shared__ double hb[3];
+    const int nb = gridDim.x;
+    const int stride = gridDim.x * blockDim.x;
+    const int i0 = blockIdx.x * blockDim.x + threadIdx.x;
+    const int npair = (m + 2) / 2;  // dot passes: vectors (0, 1), (2, 3), ...; the last may be single
+    double wr[EPT], pa[EPT], pb[EPT], ca[EPT], cb[EPT];
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) {
+        const int i = i0 + k * stride;
+        wr[k] = i < n ? w[i] : 0.0;
+        pa[k] = pb[k] = 0.0;
+        ca[k] = (i < n && m >= 0) ? __ldcg(V[0] + i) : 0.0;
+        cb[k] = (i < n && m >= 1) ? __ldcg(V[1] + i) : 0.0;
+    }
+    double ha = 0.0, hbv = 0.0;  // the previous pair's coefficients
+    for (int pass = 0; pass <= npair; ++pass) {
+        const bool dots = pass < npair;
+        const bool two = dots && 2 * pass + 1 <= m;
+        double s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+        for (int k = 0; k < EPT; ++k) {
+            const int i = i0 + k * stride;
+            if (i < n) {
+                double wi = wr[k];
+                if (pass > 0) {  // MGS update with the previous pair, one vector after the other
+                    wi -= ha * pa[k];
+                    wi -= hbv * pb[k];
+                    wr[k] = wi;
+                }
+                if (dots) {
+                    s1 = fma(ca[k], wi, s1);
+                    if (two) {
+                        s2 = fma(cb[k], wi, s2);
+                        s3 = fma(cb[k], ca[k], s3);
+                    }
+                } else {
+                    s1 = fma(wi, wi, s1);  // ||w||^2 after the last update
+                }
+            }
+        }
+        // pass 0 carries ||w0||^2 in a fourth sum
+        double s4 = 0.0;
+        if (pass == 0) {
+#pragma unroll
+            for (int k = 0; k < EPT; ++k) {
+                const int i = i0 + k * stride;
+                if (i < n) s4 = fma(wr[k], wr[k], s4);
+            }
+        }
+        if (dots) {
+#pragma unroll
+            for (int k = 0; k < EPT; ++k) {
+                pa[k] = ca[k];
+                pb[k] = two ? cb[k] : 0.0;
+            }
+            const int na = 2 * pass + 2, nbv = 2 * pass + 3;
+            if (na <= m) {
+                const double* va = V[na];
+#pragma unroll
+                for (int k = 0; k < EPT; ++k) {
+                    const int i = i0 + k * stride;
+                    ca[k] = i < n ? __ldcg(va + i) : 0.0;
+                }
+            }
+            if (nbv <= m) {
+                const double* vb = V[nbv];
+#pragma unroll
+                for (int k = 0; k < EPT; ++k) {
+                    const int i = i0 + k * stride;
+                    cb[k] = i < n ? __ldcg(vb + i) : 0.0;
+                }
+            }
+        }
+        block_sum3<kRedThreads>(s1, s2, s3, sh);
+        const double b4 = pass == 0 ? block_sum<kRedThreads>(s4, sh) : 0.0;
+        double* slot = partials + static_cast<std::size_t>(pass) * 4 * nb;
+        if (threadIdx.x == 0) {
+            slot[blockIdx.x] = s1;
+            slot[nb + blockIdx.x] = s2;
+            slot[2 * nb + blockIdx.x] = s3;
+            slot[3 * nb + blockIdx.x] = b4;
+        }
+        grid.sync();
+        double t1 = 0.0, t2 = 0.0, t3 = 0.0, t4 = 0.0;
+        for (int q = threadIdx.x; q < nb; q += blockDim.x) {
+            t1 += slot[q];
+            if (two) {
+                t2 += slot[nb + q];
+                t3 += slot[2 * nb + q];
+            }
+            if (pass == 0) t4 += slot[3 * nb + q];
+        }
+        block_sum3<kRedThreads>(t1, t2, t3, sh);
+        if (pass == 0) t4 = block_sum<kRedThreads>(t4, sh);
+        if (threadIdx.x == 0) {
+            const double h1 = t1;
+            const double h2 = two ? t2 - h1 * t3 : 0.0;
+            hb[0] = h1;
+            hb[1] = h2;
+            if (blockIdx.x == 0) {
+                if (dots) {
+                    hout[2 * pass] = h1;
+                    if (two) hout[2 * pass + 1] = h2;
+                } else {
+                    hout[m + 1] = h1;
+                }
+                if (pass == 0) *wn0 = t4;
+            }
+        }
+        __syncthreads();
+        ha = hb[0];
+        hbv = hb[1];
+    }
+    // ha = ||w||^2 after the last pass: speculative next basis vector
+    const double sub = sqrt(ha);
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) {
+        const int i = i0 + k * stride;
+        if (i < n) {
+            w[i] = wr[k];
+            if (vnext) {
+                const double v = wr[k] / sub;
+                vnext[i] = v;
+                if (vin) vin[i] = v;
+            }
+        }
+    }
+}
+
 /** Single-CTA variant of k_mgs_all for small systems (n below a few 10^4):
  *  the same passes and fixed-order sums with __syncthreads instead of grid
  *  barriers, so a whole Arnoldi orthogonalisation costs a few microseconds. */
@@ -740,8 +916,15 @@ struct Workspace {
         }();
         const long long threads = static_cast<long long>(coop_grid) * kRedThreads;
         const int ept = static_cast<int>((n + threads - 1) / threads);
+        const char* se = std::getenv("CPDDG_MGS");  // "single" = one projection per grid barrier (k_mgs_reg)
+        const bool single = se && std::string(se) == "single";
         const void* kern = reinterpret_cast<const void*>(k_mgs_all);
-        if (!streamed && ept <= 16)
+        if (!streamed && !single && ept <= 8)
+            kern = ept <= 1   ? reinterpret_cast<const void*>(k_mgs_pair<1>)
+                   : ept <= 2 ? reinterpret_cast<const void*>(k_mgs_pair<2>)
+                   : ept <= 4 ? reinterpret_cast<const void*>(k_mgs_pair<4>)
+                              : reinterpret_cast<const void*>(k_mgs_pair<8>);
+        else if (!streamed && ept <= 16)
             kern = ept <= 1   ? reinterpret_cast<const void*>(k_mgs_reg<1>)
                    : ept <= 2 ? reinterpret_cast<const void*>(k_mgs_reg<2>)
                    : ept <= 4 ? reinterpret_cast<const void*>(k_mgs_reg<4>)
@@ -770,7 +953,9 @@ struct Workspace {
             if (const char* e = std::getenv("CPDDG_MGS_BPS")) bps = std::max(1, std::atoi(e));  // development knob
             coop_grid = std::max(1, std::min(per_sm, bps)) * sm_count();
         }
-        const std::size_t need = static_cast<std::size_t>(2 * coop_grid) * (m + 2);
+        // k_mgs_reg / k_mgs_all: 2 sums x (m + 2) passes; k_mgs_pair: 4 sums x ((m + 2) / 2 + 1) passes
+        const std::size_t need = std::max(static_cast<std::size_t>(2 * coop_grid) * (m + 2),
+                                          static_cast<std::size_t>(4 * coop_grid) * ((m + 2) / 2 + 2));
         if (mgs_partials.size() < need) mgs_partials.alloc(std::max(need, static_cast<std::size_t>(2 * coop_grid) * 64));
         // basis pointer table (V_0..V_m) on the device: basis buffers never
         // move once allocated, so the table is uploaded only when it grows

@@ -383,6 +383,38 @@ def test_graph_gmres_short_cycles_and_max_iter(monkeypatch):
         assert torch.equal(d.u, h.u)
 
 
+def test_paired_mgs_matches_single_projection_mgs(monkeypatch):
+    """The cooperative orthogonalisation takes two projections per grid barrier
+    (k_mgs_pair: h_b = V_b.w - h_a (V_b.V_a), the modified Gram-Schmidt
+    coefficient with the subtraction moved across the dot product); one
+    projection per barrier (CPDDG_MGS=single, k_mgs_reg) gives the same
+    iteration count, residual history and solution to rounding, in the
+    device-driven cycles and in the host loop, over several restart cycles."""
+    import torch
+
+    from paper_1909_08734_b200 import api, inputs
+    P = api.Problem("sphere", h=0.05, p=3, c=1.0)
+    P.decompose(inputs.rcb_partition(P.active_cp, 64), 2, "oras", 4.0, 40.0)
+    A = api.DeviceHelmholtz.from_problem(P)
+    M = api.SchwarzPreconditioner.from_problem(P)
+    b = torch.from_numpy(inputs.rhs_sphere(P.active_cp)).cuda()
+    for graph in ("1", "0"):
+        monkeypatch.setenv("CPDDG_GMRES_GRAPH", graph)
+        for restart in (50, 7):
+            pair = api.gmres_solve(A, b, M, 1e-10, 1000, restart)
+            monkeypatch.setenv("CPDDG_MGS", "single")
+            single = api.gmres_solve(A, b, M, 1e-10, 1000, restart)
+            monkeypatch.delenv("CPDDG_MGS")
+            assert pair.log.converged and pair.log.iterations == single.log.iterations
+            rp, rs_ = np.asarray(pair.log.residuals), np.asarray(single.log.residuals)
+            assert np.max(np.abs(rp - rs_) / rs_[0]) <= 1e-12
+            up, us = pair.u.cpu().numpy(), single.u.cpu().numpy()
+            assert np.linalg.norm(up - us) <= 1e-11 * np.linalg.norm(us)
+            again = api.gmres_solve(A, b, M, 1e-10, 1000, restart)
+            assert torch.equal(again.u, pair.u)  # bitwise reproducible
+    monkeypatch.delenv("CPDDG_GMRES_GRAPH")
+
+
 def test_run_solve_pipeline_with_files(tmp_path):
     """run_solve (pipeline.hpp:183-241) fed through a partition file and an rhs
     file, writing the reference's output files."""
