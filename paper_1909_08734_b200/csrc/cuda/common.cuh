@@ -25,17 +25,20 @@ public:
     explicit DevBuf(std::size_t n) { alloc(n); }
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
-    DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_) {
+    DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_), owns_(o.owns_) {
         o.p_ = nullptr;
         o.n_ = 0;
+        o.owns_ = true;
     }
     DevBuf& operator=(DevBuf&& o) noexcept {
         if (this != &o) {
             release();
             p_ = o.p_;
             n_ = o.n_;
+            owns_ = o.owns_;
             o.p_ = nullptr;
             o.n_ = 0;
+            o.owns_ = true;
         }
         return *this;
     }
@@ -59,15 +62,24 @@ public:
     T* get() const { return p_; }
     std::size_t size() const { return n_; }
     std::size_t bytes() const { return n_ * sizeof(T); }
+    /** Become a non-owning view of n elements at p (storage owned by a slab that outlives this). */
+    void view(T* p, std::size_t n) {
+        release();
+        p_ = p;
+        n_ = n;
+        owns_ = false;
+    }
 
 private:
     void release() {
-        if (p_) cudaFree(p_);
+        if (p_ && owns_) cudaFree(p_);
+        owns_ = true;
         p_ = nullptr;
         n_ = 0;
     }
     T* p_ = nullptr;
     std::size_t n_ = 0;
+    bool owns_ = true;
 };
 
 /** Number of SMs of the current device (148 on B200). */

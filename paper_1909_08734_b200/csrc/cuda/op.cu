@@ -28,6 +28,7 @@
 #include <numeric>
 #include <string>
 #include <thread>
+#include <type_traits>
 
 namespace cpddg {
 
@@ -898,6 +899,50 @@ static void build_union(cpddg_op* op, const std::vector<int>& lines, const std::
     op->grp_grid = std::max(1, std::min(op->grp_chunks, std::max(1, per_sm) * sm_count()));
 }
 
+/** The union kernel's tables, the node-major neighbour codes and v move into
+ *  one slab, and the device sets aside persisting L2 for it: launch_apply puts
+ *  an access-policy window over the slab (hits persist, everything else the
+ *  two kernels touch streams), so the ~50 MB the operator re-reads every
+ *  iteration survive the preconditioner's and the orthogonalisation's traffic.
+ *  CPDDG_OP_L2=0 leaves the tables where they are (no window). */
+static void pack_tables(cpddg_op* op) {
+    const char* e = std::getenv("CPDDG_OP_L2");
+    if (e && std::string(e) == "0") return;
+    int dev = 0;
+    cudaDeviceProp prop{};
+    CPDDG_CUDA(cudaGetDevice(&dev));
+    CPDDG_CUDA(cudaGetDeviceProperties(&prop, dev));
+    auto up = [](std::size_t b) { return (b + 255) / 256 * 256; };
+    const std::size_t total = up(op->grp_t.bytes()) + up(op->grp_slot.bytes()) + up(op->grp_perm.bytes()) +
+                              up(op->uni_stage.bytes()) + up(op->uni_roff.bytes()) + up(op->nbr_aos.bytes()) +
+                              up(op->v.bytes());
+    if (prop.persistingL2CacheMaxSize <= 0 || prop.accessPolicyMaxWindowSize <= 0 ||
+        total > static_cast<std::size_t>(prop.accessPolicyMaxWindowSize) ||
+        total > static_cast<std::size_t>(prop.persistingL2CacheMaxSize))
+        return;  // does not fit a window / the carve-out: stay with the separate buffers
+    op->slab.alloc(total);
+    std::size_t at = 0;
+    auto move = [&](auto& buf) {
+        using T = std::remove_pointer_t<decltype(buf.get())>;
+        const std::size_t n = buf.size();
+        T* dst = reinterpret_cast<T*>(op->slab.get() + at);
+        if (n) CPDDG_CUDA(cudaMemcpy(dst, buf.get(), n * sizeof(T), cudaMemcpyDeviceToDevice));
+        at += up(n * sizeof(T));
+        buf.view(dst, n);
+    };
+    move(op->grp_t);
+    move(op->grp_slot);
+    move(op->grp_perm);
+    move(op->uni_stage);
+    move(op->uni_roff);
+    move(op->nbr_aos);
+    move(op->v);
+    std::size_t have = 0;
+    CPDDG_CUDA(cudaDeviceGetLimit(&have, cudaLimitPersistingL2CacheSize));
+    if (have < total) CPDDG_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, total));
+    op->l2_window = total;
+}
+
 template <int D>
 static void build_tables(cpddg_op* op, const Ix<D>* ix, const Vec<D>* cp, const LatticeMap& map) {
     const int nb = op->na + op->ng, p = op->p, Q = p + 1;
@@ -979,6 +1024,7 @@ static void build_tables(cpddg_op* op, const Ix<D>* ix, const Vec<D>* cp, const 
     op->nbr.upload(nbr);
     op->nbr_aos.upload(aos);
     op->v.alloc(static_cast<std::size_t>(nb));
+    if (op->uni) pack_tables(op);
     lap("uploads");
     op->nlines = nlines;
     // B_op = 16 N_A + [8d + 4 (p+1)^(d-1)] N_B + 8d N_A
@@ -1001,11 +1047,26 @@ static void launch_apply(const cpddg_op* op, const double* x, const double* b, d
                          cudaStream_t st, bool pdl = true) {
     const int nb = op->na + op->ng;
     const int thr = 256;
+    cudaLaunchAttribute l2attr{};
+    l2attr.id = cudaLaunchAttributeAccessPolicyWindow;
+    l2attr.val.accessPolicyWindow.base_ptr = op->slab.get();
+    l2attr.val.accessPolicyWindow.num_bytes = op->l2_window;
+    l2attr.val.accessPolicyWindow.hitRatio = 1.0f;
+    l2attr.val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    l2attr.val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
     if (op->uni) {
-        k_extend_union<<<op->grp_grid, kGrpThreads, 0, st>>>(op->grp_chunks, op->grp_slots, op->grp_t.get(),
-                                                            op->grp_slot.get(), op->grp_perm.get(),
-                                                            op->uni_stage.get(), op->uni_roff.get(), x,
-                                                            op->v.get());
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(op->grp_grid);
+        cfg.blockDim = dim3(kGrpThreads);
+        cfg.stream = st;
+        cfg.attrs = &l2attr;
+        cfg.numAttrs = op->l2_window ? 1 : 0;
+        CPDDG_CUDA(cudaLaunchKernelEx(&cfg, k_extend_union, op->grp_chunks, op->grp_slots,
+                                      static_cast<const double*>(op->grp_t.get()),
+                                      static_cast<const unsigned char*>(op->grp_slot.get()),
+                                      static_cast<const int*>(op->grp_perm.get()),
+                                      static_cast<const int*>(op->uni_stage.get()),
+                                      static_cast<const unsigned short*>(op->uni_roff.get()), x, op->v.get()));
     } else if (op->grp_chunks) {
         k_extend_grouped<<<op->grp_grid, kGrpThreads, 0, st>>>(op->grp_chunks, op->grp_slots, op->grp_t.get(),
                                                                   op->grp_slot.get(), op->grp_perm.get(),
@@ -1034,11 +1095,16 @@ static void launch_apply(const cpddg_op* op, const double* x, const double* b, d
         cfg.gridDim = dim3((op->na + 255) / 256);
         cfg.blockDim = dim3(256);
         cfg.stream = st;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cudaLaunchAttribute attr[2];
+        int na_ = 0;
+        if (pdl) {
+            attr[na_].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[na_].val.programmaticStreamSerializationAllowed = 1;
+            ++na_;
+        }
+        if (op->l2_window) attr[na_++] = l2attr;
         cfg.attrs = attr;
-        cfg.numAttrs = pdl ? 1 : 0;
+        cfg.numAttrs = na_;
         CPDDG_CUDA(cudaLaunchKernelEx(&cfg, k_helm_pdl<D>, op->na, op->cg, op->ih2,
                                       reinterpret_cast<const int2*>(op->nbr_aos.get()),
                                       static_cast<const double*>(op->v.get()), x, y));
@@ -1181,6 +1247,7 @@ int cpddg_op_bytes(const cpddg_op* op, int64_t* alg, int64_t* streamed) {
 }
 
 int cpddg_op_destroy(cpddg_op* op) {
+    if (op && op->l2_window) cudaCtxResetPersistingL2Cache();  // its persisting lines return to normal use
     delete op;
     return CPDDG_OK;
 }

@@ -73,6 +73,12 @@ struct cpddg_op {
     bool uni = false;
     cpddg::DevBuf<int> uni_stage;                   // [chunks][kUnionMax] active ordinals, -1 unused
     cpddg::DevBuf<unsigned short> uni_roff;         // [chunks][kGrpMax][16] run offsets in the stage
+    // the tables and v of the default kernels packed into one allocation, kept resident in a
+    // persisting L2 carve-out (access-policy window on the operator launches): inside a solve every
+    // preconditioner apply streams GBs and every MGS step hundreds of MB through L2 between two
+    // operator applies
+    cpddg::DevBuf<char> slab;
+    std::size_t l2_window = 0;  // bytes of the window (0: no window)
     cpddg::DevBuf<double> rn2;  // scalar slot for ||b - A x||^2
     cpddg::ReduceWork red;
     std::int64_t alg_bytes = 0, streamed_bytes = 0;
