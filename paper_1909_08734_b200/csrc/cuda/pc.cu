@@ -2611,6 +2611,11 @@ __global__ void __launch_bounds__(win::kThreads, 1) k_solve_win(const int* __res
     }
 
     // ---------------- warp 0 (block solves + helper lanes) and consumer warps 1 .. kC
+#if __CUDA_ARCH__ >= 900
+    // launched as a programmatic dependent of k_win_gather: the producer above reads only the
+    // factors and the setup tables; everything below touches ybuf / the hand-over state
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
     double* ywin = reinterpret_cast<double*>(smem + ring_bytes);
     const unsigned ywin_u = smem_u32(ywin);
     const unsigned ring_u = smem_u32(ring);
@@ -2945,6 +2950,11 @@ __global__ void __launch_bounds__(win::kThreads, 1) k_solve_win(const int* __res
 /** ybuf[p] = r[gidx[p]] (0 for rows outside the overlap: Dirichlet closures). */
 __global__ void k_win_gather(std::int64_t rows, const int* __restrict__ gidx, const double* __restrict__ r,
                              double* __restrict__ ybuf) {
+#if __CUDA_ARCH__ >= 900
+    // k_solve_win may start: its producer streams factor items while this kernel still gathers
+    // (everything that reads ybuf waits in griddepcontrol.wait)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
     for (std::int64_t p = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; p < rows;
          p += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
         const int g = gidx[p];
@@ -2955,6 +2965,9 @@ __global__ void k_win_gather(std::int64_t rows, const int* __restrict__ gidx, co
 /** z[sidx[p]] (+)= ybuf[p] over the owned rows (Rt_j^T; disjoint writes). */
 __global__ void k_win_scatter(std::int64_t rows, const int* __restrict__ sidx, const double* __restrict__ ybuf,
                               double* __restrict__ z, int accumulate) {
+#if __CUDA_ARCH__ >= 900
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent of k_solve_win
+#endif
     for (std::int64_t p = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; p < rows;
          p += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
         const int s = sidx[p];
@@ -3132,16 +3145,35 @@ void pc_apply_mode(const cpddg_pc* pc, const double* r, double* z, bool accumula
             return pc->win_gy ? k_solve_win<RB, true> : k_solve_win<RB, false>;
         };
         auto kern = rb == 8 ? pick(std::integral_constant<int, 8>{}) : pick(std::integral_constant<int, 16>{});
-        kern<<<pc->win_grid, win::kThreads, pc->win_smem, st>>>(
-            (bal ? pc->win_bal_begin : pc->win_cta_begin).get(),
-            reinterpret_cast<const win::Seg*>((bal ? pc->win_bal_segs : pc->win_cta_subs).get()), pc->n_rows.get(),
-            pc->vbase.get(), pc->win_itbase.get(), reinterpret_cast<const win::Item*>(pc->win_items.get()), yb,
-            pc->win_wmask, pc->win_dback, pc->win_ring, m, pc->win_hand_flag.get(), pc->win_hand_buf.get(),
-            pc->win_hand_stride, dbg);
-        CPDDG_CUDA(cudaGetLastError());
+        // gather -> solve -> scatter as programmatic dependents (CPDDG_PC_PDL=0: plain stream order)
+        const char* pe = std::getenv("CPDDG_PC_PDL");
+        const bool pdl = mode != 3 && !(pe && std::string(pe) == "0");
+        cudaLaunchAttribute pattr{};
+        pattr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        pattr.val.programmaticStreamSerializationAllowed = 1;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(pc->win_grid);
+        cfg.blockDim = dim3(win::kThreads);
+        cfg.dynamicSmemBytes = static_cast<std::size_t>(pc->win_smem);
+        cfg.stream = st;
+        cfg.attrs = &pattr;
+        cfg.numAttrs = pdl ? 1 : 0;
+        CPDDG_CUDA(cudaLaunchKernelEx(
+            &cfg, kern, static_cast<const int*>((bal ? pc->win_bal_begin : pc->win_cta_begin).get()),
+            reinterpret_cast<const win::Seg*>((bal ? pc->win_bal_segs : pc->win_cta_subs).get()),
+            static_cast<const int*>(pc->n_rows.get()), static_cast<const std::int64_t*>(pc->vbase.get()),
+            static_cast<const std::int64_t*>(pc->win_itbase.get()),
+            reinterpret_cast<const win::Item*>(pc->win_items.get()), yb, pc->win_wmask, pc->win_dback, pc->win_ring, m,
+            pc->win_hand_flag.get(), pc->win_hand_buf.get(), pc->win_hand_stride, dbg));
         if (mode != 3) {
-            k_win_scatter<<<gblocks, 256, 0, st>>>(rows, pc->sidx.get(), yb, z, accumulate ? 1 : 0);
-            CPDDG_CUDA(cudaGetLastError());
+            cudaLaunchConfig_t sc = {};
+            sc.gridDim = dim3(gblocks);
+            sc.blockDim = dim3(256);
+            sc.stream = st;
+            sc.attrs = &pattr;
+            sc.numAttrs = pdl ? 1 : 0;
+            CPDDG_CUDA(cudaLaunchKernelEx(&sc, k_win_scatter, rows, static_cast<const int*>(pc->sidx.get()),
+                                          static_cast<const double*>(yb), z, accumulate ? 1 : 0));
         }
         return;
     }
