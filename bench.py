@@ -484,6 +484,7 @@ def main():
         "details": {
             "N_G": P.n_ghost, "align_moves": moves, "gmres_iterations": iters[0],
             "time_to_1e-10_s": t_dev / args.steps, "final_true_relative_residual": final_rel,
+            "step_ms": [round(1e3 * r.log.device_seconds, 3) for r in results],
             "replicas": world,
             "setup_s": {"problem": t_problem, "decompose": t_decomp, "factor_and_upload": t_locals,
                         "device_factor": pcs["factor_seconds"], "host_analyse": pcs["analyse_seconds"],

@@ -1060,7 +1060,10 @@ static void ensure_cycle_graph(cpddg_op* op, cpddg_pc* pc, Workspace& ws, int cy
             z = kc.tmp.get();
         }
         if (prof) k_stamp<<<1, 32, 0, cs>>>(gb, stamps, 1);
-        op_apply(op, z, kc.w.get(), cs, false);
+        // programmatic edge extension -> Helmholtz kernel also inside the captured body
+        // (CPDDG_GRAPH_PDL=0: plain edge)
+        const char* gp = std::getenv("CPDDG_GRAPH_PDL");
+        op_apply(op, z, kc.w.get(), cs, !(gp && std::string(gp) == "0"));
         if (prof) k_stamp<<<1, 32, 0, cs>>>(gb, stamps, 2);
         ws.mgs_all_dev(cycle, kc.w.get(), hd, mdev, kc.vin.get());
         k_givens<<<1, 32, 0, cs>>>(gb, cap, hd, cond);
