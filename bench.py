@@ -158,9 +158,12 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
 
-    def stop(self):
+    def stop(self, t_begin=None, t_end=None):
+        """Samples that arrived in [t_begin, t_end] (host clock): the sampler is started before the
+        warm-up, so that nvidia-smi's own start-up (NVML initialisation stalls the driver for tens of
+        milliseconds) does not fall into the timed region, and only the timed region's samples count."""
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -171,7 +174,9 @@ class ClockSampler:
         self.th.join(timeout=2)
         sm, mx, reasons, power = [], [], set(), []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        inside = [ln for (t, ln) in self.lines
+                  if (t_begin is None or t >= t_begin) and (t_end is None or t <= t_end + 1e-3 * self.interval_ms)]
+        for ln in inside:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
@@ -400,30 +405,32 @@ def main():
     # the same graph, so nothing is captured inside the timed region
     if not args.host_loop:
         os.environ["CPDDG_GMRES_GRAPH"] = "1"
-    for _ in range(args.warmup):
-        api.gmres_solve(A, b, M, tol, mi, rs, profile=True)
-    torch.cuda.synchronize()
-
-    # ---- timed region: K complete solves, inputs resident in HBM
     # each nvidia-smi query stalls the CUDA driver for milliseconds: harmless
-    # for the 0.3 s headline solves, but it would dominate the millisecond
+    # for the 0.15 s headline solves, but it would dominate the millisecond
     # configurations, which are sampled once a second instead (over >= 1 s)
     clock_ms = 200 if args.config not in ("circle", "sphere05") else 1000
     if os.environ.get("CPDDG_BENCH_CLOCK_MS"):  # experiment knob: sampling interval of the clocks line
         clock_ms = int(os.environ["CPDDG_BENCH_CLOCK_MS"])
     clocks = ClockSampler(local_rank, clock_ms)
-    clocks.start()
+    clocks.start()  # before the warm-up: see ClockSampler.stop
+    for _ in range(args.warmup):
+        api.gmres_solve(A, b, M, tol, mi, rs, profile=True)
+    torch.cuda.synchronize()
+
+    # ---- timed region: K complete solves, inputs resident in HBM
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_begin = time.perf_counter()
     e0.record()
     torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include "timed/": the launch list of the timed region only
     results = [api.gmres_solve(A, b, M, tol, mi, rs, profile=True) for _ in range(args.steps)]
     torch.cuda.nvtx.range_pop()
     e1.record()
     torch.cuda.synchronize()
+    t_end = time.perf_counter()
     barrier()
-    clk = clocks.stop()
+    clk = clocks.stop(t_begin, t_end)
     t_dev = max_over_ranks(e0.elapsed_time(e1) * 1e-3)
     iters = [r.log.iterations for r in results]
     assert all(r.log.converged for r in results), "solve did not converge"
