@@ -21,6 +21,7 @@ timed region.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -418,6 +419,10 @@ def main():
     torch.cuda.synchronize()
 
     # ---- timed region: K complete solves, inputs resident in HBM
+    # (no Python garbage collection inside the timed regions: a full collection in a process that
+    # has torch imported pauses the host for tens of milliseconds between two solves)
+    gc.collect()
+    gc.disable()
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -462,6 +467,7 @@ def main():
     e3.record()
     torch.cuda.synchronize()
     barrier()
+    gc.enable()
     t_e2e = max_over_ranks(e2.elapsed_time(e3) * 1e-3)
     e2e_value = world * n * e2e_iters / t_e2e
 

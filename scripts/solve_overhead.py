@@ -34,3 +34,15 @@ for keep in (True, False, True, False):
     e1.record(); torch.cuda.synchronize()
     t1 = time.perf_counter()
     print(f"keep results={keep}: events {e0.elapsed_time(e1) / 10:.3f} ms, wall {1e2 * (t1 - t0):.3f} ms, device {np.mean(dev):.3f} ms per solve")
+# outliers over many calls: where does a stalled call spend its time?
+torch.cuda.synchronize()
+ts = []
+for _ in range(150):
+    t0 = time.perf_counter(); r = api.gmres_solve(A, b, M, 1e-10, 2000, 50); t1 = time.perf_counter()
+    ts.append((t0, t1, 1e3 * r.log.device_seconds))
+gaps = [1e3 * (ts[k + 1][0] - ts[k][1]) for k in range(len(ts) - 1)]
+over = [1e3 * (t1 - t0) - d for (t0, t1, d) in ts]
+print(f"150 calls: device ms min/median/max {min(d for *_, d in ts):.2f}/{np.median([d for *_, d in ts]):.2f}/{max(d for *_, d in ts):.2f}; "
+      f"in-call overhead ms median/max {np.median(over):.3f}/{max(over):.3f}; between-call gap ms median/max {np.median(gaps):.3f}/{max(gaps):.3f}")
+print("calls with > 2 ms outside the device time:", [(k, round(o, 2)) for k, o in enumerate(over) if o > 2.0])
+print("device-time outliers (> median + 3 ms):", [(k, round(d, 2)) for k, (*_, d) in enumerate(ts) if d > np.median([x for *_, x in ts]) + 3.0])
