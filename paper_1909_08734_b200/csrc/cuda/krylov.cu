@@ -279,8 +279,8 @@ __device__ __forceinline__ void block_sum3(double& a, double& b, double& c, doub
  *  Pass 0 also reduces ||w||^2; the last pass reduces ||w||^2 of the
  *  orthogonalised w.  Same index mapping and fixed summation orders: bitwise
  *  reproducible run to run. */
-template <int EPT>
-__global__ void __launch_bounds__(kRedThreads, 2) k_mgs_pair(int n, int m, const double* const* __restrict__ V,
+template <int EPT, int NT = kRedThreads>
+__global__ void __launch_bounds__(NT, NT == kRedThreads ? 2 : 1) k_mgs_pair(int n, int m, const double* const* __restrict__ V,
                                                           double* __restrict__ w, double* __restrict__ vnext,
                                                           double* partials, double* hout, double* wn0,
                                                           const int* __restrict__ mdev, double* __restrict__ vin) {
@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(kRedThreads, 2) k_mgs_pair(int n, int m, const
     }
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
-    __shared__ double sh[3 * (kRedThreads / 32)];
+    __shared__ double sh[3 * (NT / 32)];
     __shared__ double hb[3];
     const int nb = gridDim.x;
     const int stride = gridDim.x * blockDim.x;
@@ -365,8 +365,8 @@ __global__ void __launch_bounds__(kRedThreads, 2) k_mgs_pair(int n, int m, const
                 }
             }
         }
-        block_sum3<kRedThreads>(s1, s2, s3, sh);
-        const double b4 = pass == 0 ? block_sum<kRedThreads>(s4, sh) : 0.0;
+        block_sum3<NT>(s1, s2, s3, sh);
+        const double b4 = pass == 0 ? block_sum<NT>(s4, sh) : 0.0;
         double* slot = partials + static_cast<std::size_t>(pass) * 4 * nb;
         if (threadIdx.x == 0) {
             slot[blockIdx.x] = s1;
@@ -384,8 +384,8 @@ __global__ void __launch_bounds__(kRedThreads, 2) k_mgs_pair(int n, int m, const
             }
             if (pass == 0) t4 += slot[3 * nb + q];
         }
-        block_sum3<kRedThreads>(t1, t2, t3, sh);
-        if (pass == 0) t4 = block_sum<kRedThreads>(t4, sh);
+        block_sum3<NT>(t1, t2, t3, sh);
+        if (pass == 0) t4 = block_sum<NT>(t4, sh);
         if (threadIdx.x == 0) {
             const double h1 = t1;
             const double h2 = two ? t2 - h1 * t3 : 0.0;
@@ -930,6 +930,22 @@ struct Workspace {
                    : ept <= 4 ? reinterpret_cast<const void*>(k_mgs_reg<4>)
                    : ept <= 8 ? reinterpret_cast<const void*>(k_mgs_reg<8>)
                               : reinterpret_cast<const void*>(k_mgs_reg<16>);
+        // fewer, larger blocks make the grid barrier cheaper: one 512-thread block per SM when its
+        // slice still fits 8 elements per thread (CPDDG_MGS_WIDE=0: kRedThreads-thread blocks)
+        const char* we = std::getenv("CPDDG_MGS_WIDE");
+        const bool wide_ok = !(we && std::string(we) == "0") && !streamed && !single && coop_grid >= sm_count() &&
+                             static_cast<long long>(sm_count()) * 512 * 8 >= n &&
+                             static_cast<long long>(sm_count()) * 512 * 4 < n;
+        if (wide_ok) {
+            const void* wk = reinterpret_cast<const void*>(k_mgs_pair<8, 512>);
+            int per_sm = 0;
+            CPDDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, wk, 512, 0));
+            if (per_sm >= 1) {
+                CPDDG_CUDA(cudaLaunchCooperativeKernel(wk, dim3(sm_count()), dim3(512), args, 0, st));
+                ++launches;
+                return;
+            }
+        }
         if (kern != reinterpret_cast<const void*>(k_mgs_all)) {
             int per_sm = 0;  // the whole grid must be resident
             CPDDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRedThreads, 0));
