@@ -13,4 +13,4 @@ for _ in range(rep):
         m = statistics.mean(d["details"]["step_ms"])
         e = d["config"]["N_A"] * d["details"]["gmres_iterations"] / d["e2e"]["value"] * 1e3
         print(f"clock_ms {ms:>7}: bracket - mean {d['ms_per_step'] - m:6.2f} ms, e2e - mean {e - m:6.2f} ms, "
-              f"samples {d['clocks']['samples']}", flush=True)
+              f"samples {d['clocks'].get('samples')}", flush=True)
