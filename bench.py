@@ -437,7 +437,13 @@ def main():
     t_begin = time.perf_counter()
     e0.record()
     torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include "timed/": the launch list of the timed region only
-    results = [api.gmres_solve(A, b, M, tol, mi, rs, profile=True) for _ in range(args.steps)]
+    # only the logs are kept: holding every solution tensor makes torch's caching allocator call
+    # cudaMalloc for new segments between two solves (20 - 60 ms each on a loaded device)
+    results, last = [], None
+    for _ in range(args.steps):
+        last = None  # its block returns to the cache before the next solution is allocated
+        last = api.gmres_solve(A, b, M, tol, mi, rs, profile=True)
+        results.append(last.log)
     torch.cuda.nvtx.range_pop()
     e1.record()
     torch.cuda.synchronize()
@@ -445,29 +451,35 @@ def main():
     barrier()
     clk = clocks.stop(t_begin, t_end)
     t_dev = max_over_ranks(e0.elapsed_time(e1) * 1e-3)
-    iters = [r.log.iterations for r in results]
-    assert all(r.log.converged for r in results), "solve did not converge"
+    iters = [lg.iterations for lg in results]
+    assert all(lg.converged for lg in results), "solve did not converge"
     dof_iters = n * sum(iters)
     value = world * dof_iters / t_dev
-    launches = sum(r.log.kernel_launches for r in results)
-    pc_s = sum(r.log.kernel_times["pc_seconds"] for r in results)
-    pc_n = sum(r.log.kernel_times["pc_launches"] for r in results)
-    op_s = sum(r.log.kernel_times["op_seconds"] for r in results)
-    op_n = sum(r.log.kernel_times["op_launches"] for r in results)
-    u = results[-1].u
-    final_rel = results[-1].log.final_true_residual / float(np.linalg.norm(b_host))
+    launches = sum(lg.kernel_launches for lg in results)
+    pc_s = sum(lg.kernel_times["pc_seconds"] for lg in results)
+    pc_n = sum(lg.kernel_times["pc_launches"] for lg in results)
+    op_s = sum(lg.kernel_times["op_seconds"] for lg in results)
+    op_n = sum(lg.kernel_times["op_launches"] for lg in results)
+    u = last.u
+    final_rel = results[-1].final_true_residual / float(np.linalg.norm(b_host))
 
     # ---- e2e: public API with host buffers (pinned H2D of f, D2H of u) in the timed region
     os.environ.pop("CPDDG_GMRES_GRAPH", None)
     b_pin = torch.from_numpy(b_host).pin_memory()
     u_pin = torch.empty(n, dtype=torch.float64).pin_memory()
-    api.gmres_solve(A, b, M, tol, mi, rs)  # untimed: the cycle graph without timestamps is captured here
+    # untimed: the cycle graph without timestamps is captured here, and the device blocks of one
+    # right-hand side and one solution enter the allocator's cache (no cudaMalloc in the timed loop)
+    bd = b_pin.to("cuda", non_blocking=True)
+    r = api.gmres_solve(A, bd, M, tol, mi, rs)
+    u_pin.copy_(r.u, non_blocking=True)
+    torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2.record()
     e2e_iters = 0
     for _ in range(args.steps):
+        bd = r = None  # back to the cache before the step's own copies are allocated
         bd = b_pin.to("cuda", non_blocking=True)
         r = api.gmres_solve(A, bd, M, tol, mi, rs)
         u_pin.copy_(r.u, non_blocking=True)
@@ -505,7 +517,7 @@ def main():
         "details": {
             "N_G": P.n_ghost, "align_moves": moves, "gmres_iterations": iters[0],
             "time_to_1e-10_s": t_dev / args.steps, "final_true_relative_residual": final_rel,
-            "step_ms": [round(1e3 * r.log.device_seconds, 3) for r in results],
+            "step_ms": [round(1e3 * lg.device_seconds, 3) for lg in results],
             "replicas": world,
             "setup_s": {"problem": t_problem, "decompose": t_decomp, "factor_and_upload": t_locals,
                         "device_factor": pcs["factor_seconds"], "host_analyse": pcs["analyse_seconds"],

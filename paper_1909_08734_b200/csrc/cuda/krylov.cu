@@ -17,7 +17,9 @@
 
 #include <cooperative_groups.h>
 
+#include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <string>
 #include <vector>
@@ -1583,7 +1585,19 @@ int cpddg_gmres(cpddg_op* op, cpddg_pc* pc, const double* b, double* u, const cp
         if (!op || !b || !u || !prm) throw InternalError("null argument");
         if (prm->max_iter < 0 || prm->restart < 0) throw ConfigError("max_iter and restart must be >= 0");
         if (!(prm->rel_tol > 0 && prm->rel_tol < 1)) throw ConfigError("rel_tol must lie strictly between 0 and 1");
+        // CPDDG_VERBOSE: host time between two solve calls and inside this call beyond the device time
+        static std::chrono::steady_clock::time_point last_exit{};
+        const auto t_in = std::chrono::steady_clock::now();
         gmres(op, pc, b, u, *prm, log, static_cast<cudaStream_t>(stream));
+        const auto t_out = std::chrono::steady_clock::now();
+        if (std::getenv("CPDDG_VERBOSE") && log) {
+            const double between = last_exit.time_since_epoch().count() ? std::chrono::duration<double>(t_in - last_exit).count() : 0.0;
+            const double inside = std::chrono::duration<double>(t_out - t_in).count() - log->seconds;
+            if (between > 2e-3 || inside > 2e-3)
+                std::fprintf(stderr, "[cpddg] gmres call: %.1f ms since the previous call returned, %.1f ms in the call beyond the device time\n",
+                             1e3 * between, 1e3 * inside);
+        }
+        last_exit = t_out;
     });
 }
 
